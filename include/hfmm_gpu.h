@@ -1,0 +1,174 @@
+/* hfmm_gpu.h -- C ABI of the B200-native MLFMA evaluation engine.
+ *
+ * Drop-in boundary for the evaluation phase of the reference (hfmm, arXiv
+ * 2006.15367).  The reference has no FFI: callers use its C++ API,
+ *
+ *   GlobalSetup build_setup(const std::vector<Particle>&, const RunConfig&)
+ *       /root/reference/proj/include/hfmm/traversal.hpp:120
+ *   EvalResult  evaluate_with_setup(const GlobalSetup&)
+ *       /root/reference/proj/include/hfmm/traversal.hpp:166
+ *   EvalResult  evaluate_potential(const std::vector<Particle>&, const RunConfig&)
+ *       /root/reference/proj/include/hfmm/traversal.hpp:163
+ *   RankEngine::{c2m_phase,m2m_pass,m2l_pass,l2l_pass,l2o_near_phase},
+ *   RankEngine::{multipole,local_expansion}
+ *       /root/reference/proj/include/hfmm/traversal.hpp:129-143
+ *
+ * Every entry point below replaces one of those (cited per function).  Plain
+ * pointers and sizes only; the caller owns host arrays (copied in), handles
+ * own device buffers, outputs are written into caller buffers.  Every call
+ * returns an hfmm_status; the message of the last failure on the calling
+ * thread is available from hfmm_last_error().  Status codes mirror the
+ * exception types the reference throws (traversal.cpp:42-46, operators.cpp:43-50,
+ * kernel.cpp:11, operators.cpp:160), so a C++ wrapper can rethrow the same type.
+ *
+ * Handles are not thread-safe; use one handle per host thread / device.
+ */
+#ifndef HFMM_GPU_H
+#define HFMM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hfmm_status {
+  HFMM_OK = 0,
+  HFMM_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  HFMM_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range     */
+  HFMM_ERR_DOMAIN = 3,           /* std::domain_error     */
+  HFMM_ERR_LOGIC = 4,            /* std::logic_error      */
+  HFMM_ERR_LENGTH = 5,           /* std::length_error     */
+  HFMM_ERR_CUDA = 6,             /* device / driver failure */
+  HFMM_ERR_NO_DEVICE = 7,        /* no CUDA device: there is no CPU fallback */
+  HFMM_ERR_INTERNAL = 8
+} hfmm_status;
+
+typedef enum hfmm_policy { HFMM_POLICY_RANK_ORDERED = 0, HFMM_POLICY_ALIGNED = 1 } hfmm_policy;
+
+/* Mirrors hfmm::RunConfig (traversal.hpp:21-38) field for field.  The
+ * scheduler field has no device meaning (one logical rank per GPU) and is
+ * kept only so configs round-trip. */
+typedef struct hfmm_run_config {
+  double lambda;        /* wavelength, meters (default 1)      */
+  double digits;        /* truncation accuracy knob (default 3) */
+  double leaf_lambda;   /* leaf side in wavelengths (0.25)      */
+  int32_t num_ranks;    /* logical ranks = GPUs (1)             */
+  int32_t policy;       /* hfmm_policy (Aligned)                */
+  uint64_t buffer_limit;/* M_S bytes (UINT64_MAX = unlimited)    */
+  int32_t one_particle_per_leaf;
+  int32_t top_level;    /* highest level carrying expansions (3) */
+  int32_t d_override;   /* 0 = classify from geometry            */
+  int32_t scheduler;    /* 0 deterministic, 1 adversarial, 2 threaded */
+  uint64_t seed;
+} hfmm_run_config;
+
+/* Fills the reference defaults (RunConfig{} in traversal.hpp:21-35). */
+void hfmm_run_config_default(hfmm_run_config* cfg);
+
+/* Thread-local message of the last failed call ("" if none). */
+const char* hfmm_last_error(void);
+
+/* ---------------- host setup (bit-exact with build_setup) ---------------- */
+
+typedef struct hfmm_setup hfmm_setup;
+
+/* Replaces build_setup (traversal.cpp:66-238).  positions: n*3 doubles (x,y,z
+ * per particle), charges: n*2 doubles (re,im), input order. */
+hfmm_status hfmm_setup_build(const double* positions, const double* charges,
+                             size_t n, const hfmm_run_config* cfg,
+                             hfmm_setup** out);
+void hfmm_setup_destroy(hfmm_setup* s);
+
+/* Named flat views of the setup (Morton keys, tree, lists, slices, plans)
+ * used by the bit-exactness tests; see DESIGN.md "setup arrays".  Copies at
+ * most cap bytes into dst (dst may be NULL) and returns the full byte size in
+ * *nbytes.  Unknown names give HFMM_ERR_INVALID_ARGUMENT. */
+hfmm_status hfmm_setup_get(const hfmm_setup* s, const char* name, void* dst,
+                           size_t cap, size_t* nbytes);
+
+/* ---------------- device engine (one logical rank per GPU) ---------------- */
+
+typedef struct hfmm_gpu hfmm_gpu;
+
+typedef enum hfmm_phase {
+  HFMM_PHASE_C2M = 1, /* RankEngine::c2m_phase   traversal.cpp:306 */
+  HFMM_PHASE_M2M = 2, /* RankEngine::m2m_pass    traversal.cpp:322 */
+  HFMM_PHASE_M2L = 3, /* RankEngine::m2l_pass    traversal.cpp:443 */
+  HFMM_PHASE_L2L = 4, /* RankEngine::l2l_pass    traversal.cpp:583 */
+  HFMM_PHASE_L2T = 5, /* l2o part of l2o_near_phase traversal.cpp:717-728 */
+  HFMM_PHASE_NEAR = 6 /* near part of l2o_near_phase traversal.cpp:768-786 */
+} hfmm_phase;
+
+/* Per-phase device milliseconds of the last hfmm_gpu_evaluate (CUDA events
+ * on the engine stream), indexed by hfmm_phase; [0] = T-operator build,
+ * [7] = whole evaluation. */
+typedef struct hfmm_gpu_timing {
+  double ms[8];
+  int64_t kernel_launches;
+} hfmm_gpu_timing;
+
+/* Creates an engine on CUDA device `device` for logical rank `rank` of the
+ * setup's partition.  Uploads the setup (sorted particles, level tables,
+ * lists, samplings, interpolation matrices, translation coefficients).
+ * Replaces RankEngine's constructor (traversal.cpp:242-288). */
+hfmm_status hfmm_gpu_create(const hfmm_setup* s, int device, int rank,
+                            hfmm_gpu** out);
+void hfmm_gpu_destroy(hfmm_gpu* g);
+
+/* Replaces evaluate_with_setup (traversal.cpp:790-817) for one rank:
+ * charges (n*2, input order, may be NULL to keep the uploaded ones) are
+ * copied in, all phases run, and this rank's potentials are scattered to
+ * pot_out (n*2 doubles, input order; entries of other ranks untouched).
+ * timing may be NULL. */
+hfmm_status hfmm_gpu_evaluate(hfmm_gpu* g, const double* charges,
+                              double* pot_out, hfmm_gpu_timing* timing);
+
+/* Device-resident variant used by the benchmark: charges already on the
+ * device in sorted order (n*2), potentials left on the device in sorted
+ * order (n*2).  `stream` is a cudaStream_t (NULL = the engine stream). */
+hfmm_status hfmm_gpu_evaluate_device(hfmm_gpu* g, const double* d_charges_sorted,
+                                     double* d_pot_sorted, void* stream);
+
+/* Runs a single phase (hfmm_phase) on the engine's current state, for
+ * per-phase parity (RankEngine phase drivers, traversal.hpp:129-140).
+ * HFMM_PHASE_C2M resets the state and uploads `charges` if given via
+ * hfmm_gpu_set_charges. */
+hfmm_status hfmm_gpu_set_charges(hfmm_gpu* g, const double* charges);
+hfmm_status hfmm_gpu_run_phase(hfmm_gpu* g, int phase);
+
+/* Copies this rank's multipole (kind 0) or local (kind 1) expansions of all
+ * nodes of `level` it holds, as n_nodes * n_samples complex (re,im) in node
+ * (Morton) order; nodes/samples this rank does not hold are zero.  Mirrors
+ * RankEngine::multipole / local_expansion (traversal.hpp:142-143). */
+hfmm_status hfmm_gpu_get_expansion(hfmm_gpu* g, int kind, int level, double* out,
+                                   size_t cap_doubles);
+
+/* Sorted-order potentials of this rank after HFMM_PHASE_NEAR/L2T (n*2). */
+hfmm_status hfmm_gpu_get_potentials_sorted(hfmm_gpu* g, double* out,
+                                           size_t cap_doubles);
+
+/* One-shot: build_setup + evaluate on one device (evaluate_potential,
+ * traversal.cpp:819-823).  Requires cfg->num_ranks == 1. */
+hfmm_status hfmm_evaluate_potential(const double* positions, const double* charges,
+                                    size_t n, const hfmm_run_config* cfg, int device,
+                                    double* pot_out);
+
+/* O(N*M) direct sum on the device (direct_potential, kernel.cpp:16-41):
+ * observers are given as particle indices into the source set; the first
+ * exact coincidence per observer is skipped as the self term. */
+hfmm_status hfmm_gpu_direct(const double* positions, const double* charges, size_t n,
+                            const int64_t* observer_index, size_t m, double k,
+                            int device, double* pot_out);
+
+/* Frozen seeded generator of the BASELINE inputs:
+ * shape 0 = uniform cube of side `extent`, 1 = sphere surface of radius `extent`. */
+void hfmm_generate_inputs(int shape, size_t n, double extent, uint64_t seed,
+                          double* positions, double* charges);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HFMM_GPU_H */

@@ -1,0 +1,210 @@
+// C ABI (include/hfmm_gpu.h): status codes mirror the reference's exception
+// types; every entry point is wrapped so no C++ exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "hfmm_gpu.h"
+#include "inputs.hpp"
+#include "setup.hpp"
+
+struct hfmm_setup {
+  hfmm_b200::Setup s;
+};
+struct hfmm_gpu {
+  std::unique_ptr<hfmm_b200::Engine> eng;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <class F>
+hfmm_status guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return HFMM_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return HFMM_ERR_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return HFMM_ERR_OUT_OF_RANGE;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return HFMM_ERR_DOMAIN;
+  } catch (const std::length_error& e) {
+    g_err = e.what();
+    return HFMM_ERR_LENGTH;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return HFMM_ERR_LOGIC;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return std::string(e.what()).find("no CUDA device") != std::string::npos ? HFMM_ERR_NO_DEVICE
+                                                                             : HFMM_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HFMM_ERR_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
+}
+
+}  // namespace
+
+extern "C" {
+
+void hfmm_run_config_default(hfmm_run_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->lambda = 1.0;
+  c->digits = 3.0;
+  c->leaf_lambda = 0.25;
+  c->num_ranks = 1;
+  c->policy = HFMM_POLICY_ALIGNED;
+  c->buffer_limit = ~uint64_t(0);
+  c->one_particle_per_leaf = 0;
+  c->top_level = 3;
+  c->d_override = 0;
+  c->scheduler = 0;
+  c->seed = 0;
+}
+
+const char* hfmm_last_error(void) { return g_err.c_str(); }
+
+hfmm_status hfmm_setup_build(const double* positions, const double* charges, size_t n,
+                             const hfmm_run_config* cfg, hfmm_setup** out) {
+  return guard([&] {
+    need(cfg, "hfmm_setup_build(cfg)");
+    need(out, "hfmm_setup_build(out)");
+    if (n > 0) {
+      need(positions, "hfmm_setup_build(positions)");
+      need(charges, "hfmm_setup_build(charges)");
+    }
+    auto h = std::make_unique<hfmm_setup>();
+    h->s = hfmm_b200::build_setup(positions, charges, n, *cfg);
+    *out = h.release();
+  });
+}
+
+void hfmm_setup_destroy(hfmm_setup* s) { delete s; }
+
+hfmm_status hfmm_setup_get(const hfmm_setup* s, const char* name, void* dst, size_t cap,
+                           size_t* nbytes) {
+  return guard([&] {
+    need(s, "hfmm_setup_get(setup)");
+    need(name, "hfmm_setup_get(name)");
+    auto v = hfmm_b200::setup_array(s->s, name);
+    if (nbytes) *nbytes = v.size();
+    if (dst && cap) std::memcpy(dst, v.data(), std::min(cap, v.size()));
+  });
+}
+
+hfmm_status hfmm_gpu_create(const hfmm_setup* s, int device, int rank, hfmm_gpu** out) {
+  return guard([&] {
+    need(s, "hfmm_gpu_create(setup)");
+    need(out, "hfmm_gpu_create(out)");
+    auto g = std::make_unique<hfmm_gpu>();
+    g->eng = std::make_unique<hfmm_b200::Engine>(s->s, device, rank);
+    *out = g.release();
+  });
+}
+
+void hfmm_gpu_destroy(hfmm_gpu* g) { delete g; }
+
+hfmm_status hfmm_gpu_evaluate(hfmm_gpu* g, const double* charges, double* pot_out,
+                              hfmm_gpu_timing* timing) {
+  return guard([&] {
+    need(g, "hfmm_gpu_evaluate(gpu)");
+    need(pot_out, "hfmm_gpu_evaluate(pot_out)");
+    double ms[8] = {0};
+    int64_t l0 = g->eng->launches();
+    g->eng->evaluate_host(charges, pot_out, ms);
+    if (timing) {
+      std::memcpy(timing->ms, ms, sizeof(ms));
+      timing->kernel_launches = g->eng->launches() - l0;
+    }
+  });
+}
+
+hfmm_status hfmm_gpu_evaluate_device(hfmm_gpu* g, const double* d_q, double* d_pot, void* stream) {
+  return guard([&] {
+    need(g, "hfmm_gpu_evaluate_device(gpu)");
+    g->eng->evaluate_device(d_q, d_pot, static_cast<cudaStream_t>(stream));
+  });
+}
+
+hfmm_status hfmm_gpu_set_charges(hfmm_gpu* g, const double* charges) {
+  return guard([&] {
+    need(g, "hfmm_gpu_set_charges(gpu)");
+    need(charges, "hfmm_gpu_set_charges(charges)");
+    g->eng->set_charges(charges);
+  });
+}
+
+hfmm_status hfmm_gpu_run_phase(hfmm_gpu* g, int phase) {
+  return guard([&] {
+    need(g, "hfmm_gpu_run_phase(gpu)");
+    g->eng->run_phase(phase);
+  });
+}
+
+hfmm_status hfmm_gpu_get_expansion(hfmm_gpu* g, int kind, int level, double* out, size_t cap) {
+  return guard([&] {
+    need(g, "hfmm_gpu_get_expansion(gpu)");
+    need(out, "hfmm_gpu_get_expansion(out)");
+    g->eng->get_expansion(kind, level, out, cap);
+  });
+}
+
+hfmm_status hfmm_gpu_get_potentials_sorted(hfmm_gpu* g, double* out, size_t cap) {
+  return guard([&] {
+    need(g, "hfmm_gpu_get_potentials_sorted(gpu)");
+    need(out, "hfmm_gpu_get_potentials_sorted(out)");
+    g->eng->get_potentials_sorted(out, cap);
+  });
+}
+
+hfmm_status hfmm_evaluate_potential(const double* positions, const double* charges, size_t n,
+                                    const hfmm_run_config* cfg, int device, double* pot_out) {
+  return guard([&] {
+    need(cfg, "hfmm_evaluate_potential(cfg)");
+    need(pot_out, "hfmm_evaluate_potential(pot_out)");
+    if (cfg->num_ranks != 1)
+      throw std::invalid_argument("hfmm_evaluate_potential: one device evaluates num_ranks == 1");
+    hfmm_b200::Setup s = hfmm_b200::build_setup(positions, charges, n, *cfg);
+    hfmm_b200::Engine e(s, device, 0);
+    e.evaluate_host(nullptr, pot_out, nullptr);
+  });
+}
+
+hfmm_status hfmm_gpu_direct(const double* positions, const double* charges, size_t n,
+                            const int64_t* obs, size_t m, double k, int device, double* pot_out) {
+  return guard([&] {
+    need(positions, "hfmm_gpu_direct(positions)");
+    need(charges, "hfmm_gpu_direct(charges)");
+    need(obs, "hfmm_gpu_direct(observers)");
+    need(pot_out, "hfmm_gpu_direct(pot_out)");
+    hfmm_b200::direct_sum(positions, charges, n, obs, m, k, device, pot_out);
+  });
+}
+
+void hfmm_generate_inputs(int shape, size_t n, double extent, uint64_t seed, double* positions,
+                          double* charges) {
+  hfmm_b200::generate_inputs(shape, n, extent, seed, positions, charges);
+}
+
+}  // extern "C"

@@ -1,0 +1,524 @@
+// Device engine host side: setup upload and per-phase launches.
+#include "engine.hpp"
+
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "interp.hpp"
+#include "kernels.cuh"
+
+namespace hfmm_b200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+inline int slot_of(long ox, long oy, long oz) {
+  return int((ox + 3) * 49 + (oy + 3) * 7 + (oz + 3));
+}
+
+inline uint32_t cell_axis(uint64_t code, int level, int axis) {
+  uint32_t v = 0;
+  for (int t = 0; t < level - 1; ++t) v |= uint32_t((code >> (3 * t + axis)) & 1) << t;
+  return v;
+}
+
+}  // namespace
+
+template <class T>
+T* Engine::alloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  allocs_.push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* Engine::upload_vec(const std::vector<T>& v) {
+  T* d = alloc<T>(v.size());
+  if (!v.empty()) ck(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st_), "upload");
+  return d;
+}
+
+Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank_(rank) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
+  if (device < 0 || device >= ndev) throw std::invalid_argument("hfmm_gpu_create: bad device");
+  if (rank < 0 || rank >= s.P) throw std::invalid_argument("hfmm_gpu_create: bad rank");
+  if (s.P != 1)
+    throw std::invalid_argument(
+        "hfmm_gpu_create: multi-rank device evaluation is driven by the distributed runner");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+  for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
+  upload();
+  ck(cudaStreamSynchronize(st_), "upload sync");
+}
+
+Engine::~Engine() {
+  cudaSetDevice(dev_);
+  if (st_) cudaStreamSynchronize(st_);
+  for (void* p : allocs_) cudaFree(p);
+  for (auto& e : ev_)
+    if (e) cudaEventDestroy(e);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void Engine::upload() {
+  const Setup& s = s_;
+  const int L = s.L;
+  const size_t n = s.n;
+  leaf_b_ = int64_t(s.rank_begin[size_t(rank_)]);
+  leaf_e_ = int64_t(s.rank_end[size_t(rank_)]);
+  part_b_ = int64_t(s.leaf_start[size_t(leaf_b_)]);
+  part_e_ = int64_t(s.leaf_start[size_t(leaf_e_)]);
+
+  std::vector<double> x(n), y(n), z(n);
+  for (size_t i = 0; i < n; ++i) {
+    x[i] = s.xyz[3 * i];
+    y[i] = s.xyz[3 * i + 1];
+    z[i] = s.xyz[3 * i + 2];
+  }
+  d_x = upload_vec(x);
+  d_y = upload_vec(y);
+  d_z = upload_vec(z);
+  d_q = alloc<double2>(n);
+  ck(cudaMemcpyAsync(d_q, s.q.data(), n * sizeof(double2), cudaMemcpyHostToDevice, st_), "q");
+  d_pot = alloc<double2>(n);
+  d_q_in = alloc<double2>(n);
+  d_pot_in = alloc<double2>(n);
+  std::vector<int64_t> orig(s.original_index.begin(), s.original_index.end());
+  d_orig = upload_vec(orig);
+  std::vector<int64_t> ls(s.leaf_start.begin(), s.leaf_start.end());
+  d_leaf_start = upload_vec(ls);
+  std::vector<int64_t> no(s.near_off.begin(), s.near_off.end());
+  d_near_off = upload_vec(no);
+  std::vector<int> nr(s.near.begin(), s.near.end());
+  d_near = upload_vec(nr);
+
+  lv_.assign(size_t(L + 1), DevLevel{});
+  std::vector<std::vector<double>> hdir(size_t(L + 1));
+  size_t tmp = 0;
+  for (int l = s.top; l <= L; ++l) {
+    const LevelData& t = s.levels[size_t(l)];
+    DevLevel& d = lv_[size_t(l)];
+    d.level = l;
+    d.nt = int(t.nt);
+    d.np = int(t.np);
+    d.trunc = t.trunc;
+    d.S = t.samples();
+    d.n_nodes = int(t.num_nodes());
+    d.side = t.side;
+    // Directions exactly as LevelSampling::direction (sphere_grid.cpp:25-37).
+    std::vector<double> dir(size_t(3 * d.S)), wq(size_t(d.S));
+    for (int64_t sidx = 0; sidx < d.S; ++sidx) {
+      const int64_t i = sidx / d.np, j = sidx % d.np;
+      const double th = (double(i) + 0.5) * M_PI / double(d.nt);
+      const double ph = double(j) * 2.0 * M_PI / double(d.np);
+      const double st = std::sin(th);
+      dir[size_t(3 * sidx)] = st * std::cos(ph);
+      dir[size_t(3 * sidx + 1)] = st * std::sin(ph);
+      dir[size_t(3 * sidx + 2)] = std::cos(th);
+      wq[size_t(sidx)] = t.theta_w[size_t(i)] * t.phi_w;
+    }
+    d.dir = upload_vec(dir);
+    hdir[size_t(l)] = dir;
+    d.wq = upload_vec(wq);
+    d.centers = upload_vec(t.centers);
+    d.mp = alloc<double2>(size_t(d.n_nodes) * size_t(d.S));
+    d.loc = alloc<double2>(size_t(d.n_nodes) * size_t(d.S));
+    // Far lists as (source, offset slot) and the used slots.
+    std::vector<int64_t> foff(t.far_off.begin(), t.far_off.end());
+    std::vector<int2> far(t.far.size());
+    std::vector<uint8_t> used(kSlots, 0);
+    for (size_t o = 0; o < t.num_nodes(); ++o)
+      for (uint64_t f = t.far_off[o]; f < t.far_off[o + 1]; ++f) {
+        const uint32_t src = t.far[f];
+        long ox = long(cell_axis(t.codes[o], l, 0)) - long(cell_axis(t.codes[src], l, 0));
+        long oy = long(cell_axis(t.codes[o], l, 1)) - long(cell_axis(t.codes[src], l, 1));
+        long oz = long(cell_axis(t.codes[o], l, 2)) - long(cell_axis(t.codes[src], l, 2));
+        const int sl = slot_of(ox, oy, oz);
+        far[f] = make_int2(int(src), sl);
+        used[size_t(sl)] = 1;
+      }
+    d.n_far = int64_t(far.size());
+    d.far_off = upload_vec(foff);
+    d.far = upload_vec(far);
+    d.slot_used = upload_vec(used);
+    // Translation-operator coefficients (operators.cpp:52-63), host libstdc++
+    // special functions exactly as the reference evaluates them.
+    std::vector<double2> coef(size_t(kSlots) * size_t(d.trunc + 1), make_double2(0, 0));
+    for (int sl = 0; sl < kSlots; ++sl) {
+      if (!used[size_t(sl)]) continue;
+      const double Dx = double(sl / 49 - 3) * t.side, Dy = double((sl / 7) % 7 - 3) * t.side,
+                   Dz = double(sl % 7 - 3) * t.side;
+      const double dist = std::sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+      if (dist < 2.0 * t.side * (1.0 - 1e-12))
+        throw std::invalid_argument("translation_operator: boxes not well separated (|D| < 2 * side)");
+      const double xk = s.k * dist;
+      std::complex<double> mj_pow(1.0, 0.0);
+      const std::complex<double> mj(0.0, -1.0);
+      for (int ll = 0; ll <= d.trunc; ++ll) {
+        std::complex<double> h2(std::sph_bessel(unsigned(ll), xk), -std::sph_neumann(unsigned(ll), xk));
+        std::complex<double> c = mj_pow * double(2 * ll + 1) * h2;
+        coef[size_t(sl * (d.trunc + 1) + ll)] = make_double2(c.real(), c.imag());
+        mj_pow *= mj;
+      }
+    }
+    d.tcoef = upload_vec(coef);
+    d.T = alloc<double2>(size_t(kSlots) * size_t(d.S));
+    // Child CSR, parent links and octants.
+    if (l < L) {
+      std::vector<int> coff(t.child_off.begin(), t.child_off.end());
+      std::vector<int> ch(t.children.begin(), t.children.end());
+      d.child_off = upload_vec(coff);
+      d.children = upload_vec(ch);
+    }
+    if (l > s.top) {
+      const LevelData& pt = s.levels[size_t(l - 1)];
+      std::vector<int> par(t.num_nodes(), -1);
+      for (size_t p = 0; p < pt.num_nodes(); ++p)
+        for (uint64_t z2 = pt.child_off[p]; z2 < pt.child_off[p + 1]; ++z2) par[pt.children[z2]] = int(p);
+      d.parent = upload_vec(par);
+    }
+  }
+  // Octant per node (child side of every parent/child pair).
+  std::vector<uint8_t*> octs(size_t(L + 1), nullptr);
+  for (int l = s.top; l <= L; ++l) {
+    const LevelData& t = s.levels[size_t(l)];
+    std::vector<uint8_t> oc(t.num_nodes());
+    for (size_t i = 0; i < t.num_nodes(); ++i) oc[i] = uint8_t(t.codes[i] & 7);
+    octs[size_t(l)] = upload_vec(oc);
+  }
+  oct_ = octs;
+  // Interpolation matrices and shift tables per parent level.
+  for (int l = s.top; l < L; ++l) {
+    DevLevel& P = lv_[size_t(l)];
+    const DevLevel& C = lv_[size_t(l + 1)];
+    const LevelData& tp = s.levels[size_t(l)];
+    const LevelData& tc = s.levels[size_t(l + 1)];
+    const int nc = C.nt, np = P.nt;
+    if (C.np != nc || P.np != np) throw std::logic_error("non-square sampling");
+    auto transpose = [](const std::vector<double>& M, int rows, int cols) {
+      std::vector<double2> T2(size_t(rows) * size_t(cols));
+      for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c)
+          T2[size_t(c) * rows + r] = make_double2(M[size_t(2 * (r * cols + c))], M[size_t(2 * (r * cols + c) + 1)]);
+      return T2;
+    };
+    P.PuT = upload_vec(transpose(resample_matrix(nc, 0.0, np, 0.0), np, nc));
+    P.TuT = upload_vec(transpose(resample_matrix(2 * nc, 0.5, 2 * np, 0.5), 2 * np, 2 * nc));
+    P.PdT = upload_vec(transpose(resample_matrix(np, 0.0, nc, 0.0), nc, np));
+    std::vector<double> Td = resample_matrix(2 * np, 0.5, 2 * nc, 0.5);  // 2nc x 2np
+    const double scale = (double(P.S) / double(C.S)) * tp.phi_w / tc.phi_w;
+    for (int j = 0; j < 2 * nc; ++j)
+      for (int i = 0; i < 2 * np; ++i) {
+        const double wp = tp.theta_w[size_t(i < np ? i : 2 * np - 1 - i)];
+        const double wc = tc.theta_w[size_t(j < nc ? j : 2 * nc - 1 - j)];
+        const double f = scale * wp / wc;
+        Td[size_t(2 * (j * 2 * np + i))] *= f;
+        Td[size_t(2 * (j * 2 * np + i) + 1)] *= f;
+      }
+    P.TdT = upload_vec(transpose(Td, 2 * nc, 2 * np));
+    // Shift tables on the parent grid: disp = c_child - c_parent = (b - 1/2) side_c.
+    const std::vector<double>& dir = hdir[size_t(l)];
+    std::vector<double2> up(size_t(8 * P.S)), dn(size_t(8 * P.S));
+    for (int o = 0; o < 8; ++o) {
+      const double dx = ((o & 1) ? 0.5 : -0.5) * C.side, dy = ((o & 2) ? 0.5 : -0.5) * C.side,
+                   dz = ((o & 4) ? 0.5 : -0.5) * C.side;
+      for (int64_t sidx = 0; sidx < P.S; ++sidx) {
+        const double a = s.k * (dir[size_t(3 * sidx)] * dx + dir[size_t(3 * sidx + 1)] * dy +
+                                dir[size_t(3 * sidx + 2)] * dz);
+        up[size_t(o * P.S + sidx)] = make_double2(std::cos(a), std::sin(a));
+        const double b = s.k * (dir[size_t(3 * sidx)] * (-dx) + dir[size_t(3 * sidx + 1)] * (-dy) +
+                                dir[size_t(3 * sidx + 2)] * (-dz));
+        dn[size_t(o * P.S + sidx)] = make_double2(std::cos(b), std::sin(b));
+      }
+    }
+    P.shift_up = upload_vec(up);
+    P.shift_dn = upload_vec(dn);
+    tmp = std::max(tmp, size_t(C.n_nodes) * size_t(nc) * size_t(np));
+  }
+  tmp_elems_ = tmp;
+  d_tmp = alloc<double2>(tmp);
+}
+
+void Engine::set_charges(const double* q_in) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  const int64_t n = int64_t(s_.n);
+  ck(cudaMemcpyAsync(d_q_in, q_in, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, st_), "H2D q");
+  k_gather_q<<<unsigned((n + 255) / 256), 256, 0, st_>>>(n, d_orig, d_q_in, d_q);
+  ++launches_;
+  ck(cudaGetLastError(), "k_gather_q");
+}
+
+void Engine::build_T() {
+  for (int l = s_.top; l <= s_.L; ++l) {
+    DevLevel& d = lv_[size_t(l)];
+    if (d.n_far == 0) continue;
+    dim3 grid(unsigned((d.S + 127) / 128), kSlots);
+    k_tbuild<<<grid, 128, size_t(d.trunc + 1) * sizeof(double2), st_>>>(d.S, d.trunc, d.dir, d.side,
+                                                                         d.tcoef, d.slot_used, d.T);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "k_tbuild");
+}
+
+void Engine::phase_c2m() {
+  const DevLevel& d = lv_[size_t(s_.L)];
+  const int64_t nl = leaf_e_ - leaf_b_;
+  k_c2m<<<unsigned(nl), 128, 0, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.S,
+                                       s_.k, d.mp);
+  ++launches_;
+  ck(cudaGetLastError(), "k_c2m");
+}
+
+namespace {
+int theta_chunk(int half, int outs_per_circle, int threads) {
+  int cp = std::max(1, (kThetaE * threads) / outs_per_circle);
+  return std::min(cp, half);
+}
+}  // namespace
+
+void Engine::phase_m2m() {
+  for (int l = s_.L - 1; l >= s_.top; --l) {
+    DevLevel& P = lv_[size_t(l)];
+    DevLevel& C = lv_[size_t(l + 1)];
+    const int nc = C.nt, np = P.nt;
+    k_m2m_phi<<<unsigned(C.n_nodes), 256, size_t(nc) * nc * sizeof(double2), st_>>>(nc, np, 0, C.mp, P.PuT,
+                                                                                   d_tmp);
+    ++launches_;
+    const int half = np / 2;
+    const int CP = theta_chunk(half, 2 * np, 256);
+    dim3 grid(unsigned(P.n_nodes), unsigned((half + CP - 1) / CP));
+    const size_t smem = size_t(CP) * 2 * nc * sizeof(double2);
+    if (smem > 48 * 1024)
+      ck(cudaFuncSetAttribute(k_m2m_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+    k_m2m_theta<<<grid, 256, smem, st_>>>(nc, np, CP, 0, 0, P.child_off, P.children, oct_[size_t(l + 1)], d_tmp,
+                                          P.TuT, P.shift_up, P.mp);
+    ++launches_;
+    ck(cudaGetLastError(), "m2m");
+  }
+}
+
+void Engine::phase_m2l() {
+  for (int l = s_.top; l <= s_.L; ++l) {
+    DevLevel& d = lv_[size_t(l)];
+    dim3 grid(unsigned(d.n_nodes), unsigned((d.S + 127) / 128));
+    k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, d.far_off, d.far, d.T, d.mp, d.loc);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "m2l");
+}
+
+void Engine::phase_l2l() {
+  for (int l = s_.top; l < s_.L; ++l) {
+    DevLevel& P = lv_[size_t(l)];
+    DevLevel& C = lv_[size_t(l + 1)];
+    const int nc = C.nt, np = P.nt;
+    const int half = np / 2;
+    const int CP = theta_chunk(half, 2 * nc, 256);
+    dim3 grid(unsigned(C.n_nodes), unsigned((half + CP - 1) / CP));
+    const size_t smem = size_t(CP) * 2 * np * sizeof(double2);
+    if (smem > 48 * 1024)
+      ck(cudaFuncSetAttribute(k_l2l_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+    k_l2l_theta<<<grid, 256, smem, st_>>>(nc, np, CP, 0, C.parent, oct_[size_t(l + 1)], P.loc, P.shift_dn, P.TdT,
+                                          d_tmp);
+    ++launches_;
+    const size_t smem2 = size_t(nc) * np * sizeof(double2);
+    if (smem2 > 48 * 1024)
+      ck(cudaFuncSetAttribute(k_l2l_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)), "attr");
+    k_l2l_phi<<<unsigned(C.n_nodes), 256, smem2, st_>>>(nc, np, 0, d_tmp, P.PdT, C.loc);
+    ++launches_;
+    ck(cudaGetLastError(), "l2l");
+  }
+}
+
+void Engine::phase_l2t() {
+  const DevLevel& d = lv_[size_t(s_.L)];
+  const int64_t nl = leaf_e_ - leaf_b_;
+  const size_t smem = size_t(d.S) * (sizeof(double2) + 3 * sizeof(double));
+  if (smem > 48 * 1024)
+    ck(cudaFuncSetAttribute(k_l2t, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+  k_l2t<<<unsigned(nl), 128, smem, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.S,
+                                          s_.k, d.loc, d_pot);
+  ++launches_;
+  ck(cudaGetLastError(), "k_l2t");
+}
+
+void Engine::phase_near() {
+  const int64_t nl = leaf_e_ - leaf_b_;
+  k_p2p<<<unsigned(nl), 128, 0, st_>>>(leaf_b_, d_leaf_start, d_near_off, d_near, d_x, d_y, d_z, d_q, s_.k,
+                                       d_pot);
+  ++launches_;
+  ck(cudaGetLastError(), "k_p2p");
+}
+
+void Engine::run_phase(int phase) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  switch (phase) {
+    case HFMM_PHASE_C2M:
+      phase_c2m();
+      break;
+    case HFMM_PHASE_M2M:
+      phase_m2m();
+      break;
+    case HFMM_PHASE_M2L:
+      build_T();
+      phase_m2l();
+      break;
+    case HFMM_PHASE_L2L:
+      phase_l2l();
+      break;
+    case HFMM_PHASE_L2T:
+      phase_l2t();
+      break;
+    case HFMM_PHASE_NEAR:
+      phase_near();
+      break;
+    default:
+      throw std::invalid_argument("hfmm_gpu_run_phase: unknown phase");
+  }
+  ck(cudaStreamSynchronize(st_), "phase sync");
+}
+
+void Engine::evaluate(double* ms) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  cudaEventRecord(ev_[0], st_);
+  build_T();
+  cudaEventRecord(ev_[1], st_);
+  phase_c2m();
+  cudaEventRecord(ev_[2], st_);
+  phase_m2m();
+  cudaEventRecord(ev_[3], st_);
+  phase_m2l();
+  cudaEventRecord(ev_[4], st_);
+  phase_l2l();
+  cudaEventRecord(ev_[5], st_);
+  phase_l2t();
+  cudaEventRecord(ev_[6], st_);
+  phase_near();
+  cudaEventRecord(ev_[7], st_);
+  ck(cudaStreamSynchronize(st_), "evaluate");
+  if (ms) {
+    float f = 0.f;
+    for (int i = 0; i < 7; ++i) {
+      cudaEventElapsedTime(&f, ev_[i], ev_[i + 1]);
+      ms[i] = f;
+    }
+    cudaEventElapsedTime(&f, ev_[0], ev_[7]);
+    ms[7] = f;
+  }
+}
+
+void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cudaStream_t st) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  cudaStream_t saved = st_;
+  if (st) st_ = st;
+  const int64_t n = int64_t(s_.n);
+  if (d_q_sorted && d_q_sorted != reinterpret_cast<const double*>(d_q))
+    ck(cudaMemcpyAsync(d_q, d_q_sorted, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "q");
+  build_T();
+  phase_c2m();
+  phase_m2m();
+  phase_m2l();
+  phase_l2l();
+  phase_l2t();
+  phase_near();
+  if (d_pot_sorted)
+    ck(cudaMemcpyAsync(d_pot_sorted, d_pot, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "pot");
+  st_ = saved;
+}
+
+void Engine::evaluate_host(const double* q_in, double* pot_out, double* ms) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  if (q_in) set_charges(q_in);
+  evaluate(ms);
+  const int64_t cnt = part_e_ - part_b_;
+  if (cnt > 0) {
+    k_scatter_pot<<<unsigned((cnt + 255) / 256), 256, 0, st_>>>(part_b_, part_e_, d_orig, d_pot, d_pot_in);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "scatter");
+  if (s_.P == 1) {
+    ck(cudaMemcpyAsync(pot_out, d_pot_in, s_.n * sizeof(double2), cudaMemcpyDeviceToHost, st_), "D2H pot");
+  } else {
+    throw std::logic_error("evaluate_host: multi-rank gather not supported here");
+  }
+  ck(cudaStreamSynchronize(st_), "evaluate_host");
+}
+
+void Engine::get_expansion(int kind, int level, double* out, size_t cap) {
+  if (level < s_.top || level > s_.L) throw std::out_of_range("get_expansion: level not computed");
+  const DevLevel& d = lv_[size_t(level)];
+  const size_t cnt = size_t(d.n_nodes) * size_t(d.S) * 2;
+  if (cap < cnt) throw std::invalid_argument("get_expansion: buffer too small");
+  ck(cudaMemcpy(out, kind == 0 ? d.mp : d.loc, cnt * sizeof(double), cudaMemcpyDeviceToHost), "D2H exp");
+}
+
+void Engine::get_potentials_sorted(double* out, size_t cap) {
+  if (cap < 2 * s_.n) throw std::invalid_argument("get_potentials_sorted: buffer too small");
+  ck(cudaMemcpy(out, d_pot, s_.n * sizeof(double2), cudaMemcpyDeviceToHost), "D2H pot");
+}
+
+
+void direct_sum(const double* positions, const double* charges, size_t n, const int64_t* obs,
+                size_t m, double k, int device, double* pot_out) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
+    auto ck = [](cudaError_t e, const char* w) {
+      if (e != cudaSuccess) throw std::runtime_error(std::string(w) + ": " + cudaGetErrorString(e));
+    };
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    for (size_t i = 0; i < m; ++i)
+      if (obs[i] < 0 || size_t(obs[i]) >= n) throw std::out_of_range("hfmm_gpu_direct: observer index");
+    std::vector<double> x(n), y(n), z(n);
+    for (size_t i = 0; i < n; ++i) {
+      x[i] = positions[3 * i];
+      y[i] = positions[3 * i + 1];
+      z[i] = positions[3 * i + 2];
+    }
+    double *dx, *dy, *dz;
+    double2 *dq, *dout;
+    int64_t* dobs;
+    int* derr;
+    ck(cudaMalloc(&dx, n * 8), "malloc");
+    ck(cudaMalloc(&dy, n * 8), "malloc");
+    ck(cudaMalloc(&dz, n * 8), "malloc");
+    ck(cudaMalloc(&dq, n * 16), "malloc");
+    ck(cudaMalloc(&dout, m * 16 + 16), "malloc");
+    ck(cudaMalloc(&dobs, m * 8 + 8), "malloc");
+    ck(cudaMalloc(&derr, sizeof(int)), "malloc");
+    cudaMemcpy(dx, x.data(), n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dy, y.data(), n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dz, z.data(), n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dq, charges, n * 16, cudaMemcpyHostToDevice);
+    cudaMemcpy(dobs, obs, m * 8, cudaMemcpyHostToDevice);
+    cudaMemset(derr, 0, sizeof(int));
+    if (m > 0) k_direct<<<unsigned(m), 256>>>(int64_t(n), dx, dy, dz, dq, dobs, k, dout, derr);
+    cudaError_t le = cudaGetLastError();
+    int err = 0;
+    cudaMemcpy(&err, derr, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaError_t e2 = cudaMemcpy(pot_out, dout, m * 16, cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dz);
+    cudaFree(dq);
+    cudaFree(dout);
+    cudaFree(dobs);
+    cudaFree(derr);
+    ck(le, "k_direct");
+    ck(e2, "k_direct D2H");
+    if (err) throw std::domain_error("direct_potential: coincident source and observer");
+}
+
+}  // namespace hfmm_b200

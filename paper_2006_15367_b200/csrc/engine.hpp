@@ -1,0 +1,113 @@
+// Device engine: one logical rank of the MLFMA evaluation on one B200.
+// Replaces RankEngine (/root/reference/proj/include/hfmm/traversal.hpp:125-156).
+#ifndef HFMM_B200_ENGINE_HPP
+#define HFMM_B200_ENGINE_HPP
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "setup.hpp"
+
+namespace hfmm_b200 {
+
+// Per-level device tables.  Expansions are dense [node][theta][phi]
+// complex128 in Morton order (the reference keeps one std::vector per node
+// in a hash map, traversal.hpp:151-152).
+struct DevLevel {
+  int level = 0, nt = 0, np = 0, trunc = 0;
+  int64_t S = 0;
+  int n_nodes = 0;
+  double side = 0.0;
+  double* dir = nullptr;      // S*3 sample directions (sphere_grid.cpp:31-37)
+  double* wq = nullptr;       // S quadrature weights theta_w[i]*phi_w
+  double* centers = nullptr;  // 3*n_nodes
+  double2* mp = nullptr;      // n_nodes*S multipole samples
+  double2* loc = nullptr;     // n_nodes*S local samples
+  int64_t* far_off = nullptr; // n_nodes+1
+  int2* far = nullptr;        // (source node, offset slot)
+  int64_t n_far = 0;
+  double2* T = nullptr;       // 343*S translation operator samples
+  double2* tcoef = nullptr;   // 343*(trunc+1) Legendre-series coefficients
+  uint8_t* slot_used = nullptr;
+  int* child_off = nullptr;   // n_nodes+1 (children at level+1)
+  int* children = nullptr;
+  int* parent = nullptr;      // n_nodes, parent index at level-1 (or -1)
+  // As a parent level of level+1:
+  double2* PuT = nullptr;  // phi upsample, transposed [n_c][n_p]
+  double2* TuT = nullptr;  // theta upsample (folded), transposed [2n_c][2n_p]
+  double2* PdT = nullptr;  // phi downsample, transposed [n_p][n_c]
+  double2* TdT = nullptr;  // theta downsample with weights folded, transposed [2n_p][2n_c]
+  double2* shift_up = nullptr;  // 8*S: exp(+i k khat.(c_child - c_parent)) on this grid
+  double2* shift_dn = nullptr;  // 8*S: exp(+i k khat.(c_parent - c_child))
+};
+
+class Engine {
+ public:
+  Engine(const Setup& s, int device, int rank);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // charges in input order (n*2) -> device sorted order
+  void set_charges(const double* q_input_order);
+  void run_phase(int phase);
+  // Full evaluation from the current device charges; fills ms[8].
+  void evaluate(double* ms);
+  // Device-resident: sorted charges in, sorted potentials out.
+  void evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cudaStream_t st);
+  // e2e: host charges (input order) -> host potentials (input order).
+  void evaluate_host(const double* q_in, double* pot_out, double* ms);
+
+  void get_expansion(int kind, int level, double* out, size_t cap_doubles);
+  void get_potentials_sorted(double* out, size_t cap_doubles);
+  int64_t launches() const { return launches_; }
+
+ private:
+  void upload();
+  void build_T();
+  void phase_c2m();
+  void phase_m2m();
+  void phase_m2l();
+  void phase_l2l();
+  void phase_l2t();
+  void phase_near();
+  template <class T>
+  T* alloc(size_t count);
+  template <class T>
+  T* upload_vec(const std::vector<T>& v);
+
+  const Setup& s_;
+  int dev_ = 0, rank_ = 0;
+  cudaStream_t st_ = nullptr;
+  std::vector<DevLevel> lv_;
+  std::vector<uint8_t*> oct_;  // per level: child octant (code & 7) of each node
+  std::vector<void*> allocs_;
+  int64_t launches_ = 0;
+  // particles (sorted)
+  double* d_x = nullptr;
+  double* d_y = nullptr;
+  double* d_z = nullptr;
+  double2* d_q = nullptr;
+  double2* d_pot = nullptr;      // sorted potentials
+  double2* d_q_in = nullptr;     // input-order staging
+  double2* d_pot_in = nullptr;   // input-order staging
+  int64_t* d_orig = nullptr;     // sorted -> input index
+  int64_t* d_leaf_start = nullptr;
+  int64_t* d_near_off = nullptr;
+  int* d_near = nullptr;
+  double2* d_tmp = nullptr;  // interpolation temporaries
+  size_t tmp_elems_ = 0;
+  int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range
+  int64_t part_b_ = 0, part_e_ = 0;  // owned particle range
+  cudaEvent_t ev_[8] = {};
+};
+
+// Device O(N M) direct sum (kernel.cpp:16-41) for the accuracy checks.
+void direct_sum(const double* positions, const double* charges, size_t n, const int64_t* obs,
+                size_t m, double k, int device, double* pot_out);
+
+}  // namespace hfmm_b200
+
+#endif
