@@ -131,6 +131,10 @@ hfmm_status hfmm_gpu_evaluate(hfmm_gpu* g, const double* charges,
 hfmm_status hfmm_gpu_evaluate_device(hfmm_gpu* g, const double* d_charges_sorted,
                                      double* d_pot_sorted, void* stream);
 
+/* Per-phase device ms and kernel count of the last evaluation on this handle
+ * (either entry point); events are recorded on the stream it ran on. */
+hfmm_status hfmm_gpu_last_timing(hfmm_gpu* g, hfmm_gpu_timing* timing);
+
 /* Runs a single phase (hfmm_phase) on the engine's current state, for
  * per-phase parity (RankEngine phase drivers, traversal.hpp:129-140).
  * HFMM_PHASE_C2M resets the state and uploads `charges` if given via
@@ -161,6 +165,14 @@ hfmm_status hfmm_evaluate_potential(const double* positions, const double* charg
 hfmm_status hfmm_gpu_direct(const double* positions, const double* charges, size_t n,
                             const int64_t* observer_index, size_t m, double k,
                             int device, double* pot_out);
+
+/* Dense complex matrix (n_out x n_in, row-major, re/im interleaved) of the
+ * linear map resample_circle(n_in, s_in -> n_out, s_out)
+ * (/root/reference/proj/src/sphere_grid.cpp:128-155) that the device M2M/L2L
+ * kernels apply per theta row (shift 0) and per folded great circle
+ * (shift 0.5).  out must hold 2*n_out*n_in doubles. */
+hfmm_status hfmm_resample_matrix(int64_t n_in, double s_in, int64_t n_out, double s_out,
+                                 double* out);
 
 /* Frozen seeded generator of the BASELINE inputs:
  * shape 0 = uniform cube of side `extent`, 1 = sphere surface of radius `extent`. */

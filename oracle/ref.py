@@ -72,6 +72,23 @@ def generate_inputs(shape: str, n: int, extent: float, seed: int):
     return pos, q
 
 
+def generate_geometry(kind: str, extent: float, spacing: float, lam: float = 1.0,
+                      random: bool = True, seed: int = 0):
+    """hfmm::generate_geometry (geometry.cpp:75-127): 'grid', 'sphere' or 'volume'."""
+    k = {"grid": 0, "sphere": 1, "volume": 2}[kind]
+    cnt = ctypes.c_size_t()
+    _check(lib().ref_generate_geometry(ctypes.c_int(k), ctypes.c_double(extent), ctypes.c_double(spacing),
+                                       ctypes.c_double(lam), ctypes.c_int(int(random)), ctypes.c_uint64(seed),
+                                       ctypes.c_size_t(0), None, None, ctypes.byref(cnt)))
+    n = cnt.value
+    pos = np.empty((n, 3))
+    q = np.empty((n, 2))
+    _check(lib().ref_generate_geometry(ctypes.c_int(k), ctypes.c_double(extent), ctypes.c_double(spacing),
+                                       ctypes.c_double(lam), ctypes.c_int(int(random)), ctypes.c_uint64(seed),
+                                       ctypes.c_size_t(n), _p(pos), _p(q), ctypes.byref(cnt)))
+    return pos, q
+
+
 class RefSetup:
     """hfmm::build_setup on the reference, with the flat dump accessors."""
 

@@ -238,6 +238,31 @@ void ref_generate_inputs(int shape, size_t n, double extent, uint64_t seed,
   hfmm_b200::generate_inputs(shape, n, extent, seed, xyz, q);
 }
 
+// generate_geometry (geometry.cpp:75-127): kind 0 planar grid, 1 sphere
+// (Fibonacci), 2 cubic volume; rule 0 unit, 1 seeded random intensities.
+// Returns the point count; xyz/q (if non-null) must hold cap particles.
+int ref_generate_geometry(int kind, double extent, double spacing, double lambda, int rule,
+                          uint64_t seed, size_t cap, double* xyz, double* q, size_t* count) {
+  return guard([&] {
+    GeometrySpec g;
+    g.kind = kind == 0 ? GeometryKind::PlanarGrid
+             : kind == 1 ? GeometryKind::SphereSurface
+                         : GeometryKind::CubicVolume;
+    g.extent = extent;
+    g.spacing = spacing;
+    auto p = generate_geometry(g, lambda, rule ? IntensityRule::RandomSeeded : IntensityRule::Unit, seed);
+    *count = p.size();
+    if (xyz && q)
+      for (size_t i = 0; i < std::min(cap, p.size()); ++i) {
+        xyz[3 * i] = p[i].position.x;
+        xyz[3 * i + 1] = p[i].position.y;
+        xyz[3 * i + 2] = p[i].position.z;
+        q[2 * i] = p[i].intensity.real();
+        q[2 * i + 1] = p[i].intensity.imag();
+      }
+  });
+}
+
 int ref_setup_build(const double* xyz, const double* q, size_t n,
                     const hfmm_run_config* cfg, void** out) {
   return guard([&] {

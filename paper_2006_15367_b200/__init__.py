@@ -2,13 +2,14 @@
 reference hfmm engine, arXiv 2006.15367).  See DESIGN.md."""
 from .hfmm import (AlignPolicy, EvalResult, GlobalSetup, Phase, RankEngine, RunConfig,
                    SchedulerKind, build_setup, direct_potential, evaluate_potential,
-                   evaluate_with_setup, generate_inputs)
+                   evaluate_with_setup, generate_inputs, resample_matrix)
 from ._native import (CudaError, DomainError, HfmmError, InvalidArgument, LengthError, LogicError,
                       NoDeviceError, OutOfRange)
 
 __all__ = [
     "AlignPolicy", "EvalResult", "GlobalSetup", "Phase", "RankEngine", "RunConfig", "SchedulerKind",
     "build_setup", "direct_potential", "evaluate_potential", "evaluate_with_setup", "generate_inputs",
+    "resample_matrix",
     "CudaError", "DomainError", "HfmmError", "InvalidArgument", "LengthError", "LogicError",
     "NoDeviceError", "OutOfRange",
 ]

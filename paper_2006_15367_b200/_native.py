@@ -90,6 +90,7 @@ _SIG = {
     "hfmm_gpu_destroy": (None, [_P]),
     "hfmm_gpu_evaluate": (ctypes.c_int, [_P, _P, _P, ctypes.POINTER(TimingC)]),
     "hfmm_gpu_evaluate_device": (ctypes.c_int, [_P, _P, _P, _P]),
+    "hfmm_gpu_last_timing": (ctypes.c_int, [_P, ctypes.POINTER(TimingC)]),
     "hfmm_gpu_set_charges": (ctypes.c_int, [_P, _P]),
     "hfmm_gpu_run_phase": (ctypes.c_int, [_P, ctypes.c_int]),
     "hfmm_gpu_get_expansion": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t]),
@@ -98,6 +99,8 @@ _SIG = {
                                                ctypes.c_int, _P]),
     "hfmm_gpu_direct": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.c_double,
                                        ctypes.c_int, _P]),
+    "hfmm_resample_matrix": (ctypes.c_int, [ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
+                                            ctypes.c_double, _P]),
     "hfmm_generate_inputs": (None, [ctypes.c_int, ctypes.c_size_t, ctypes.c_double, ctypes.c_uint64,
                                     _P, _P]),
 }

@@ -11,6 +11,7 @@
 #include "engine.hpp"
 #include "hfmm_gpu.h"
 #include "inputs.hpp"
+#include "interp.hpp"
 #include "setup.hpp"
 
 struct hfmm_setup {
@@ -147,6 +148,14 @@ hfmm_status hfmm_gpu_evaluate_device(hfmm_gpu* g, const double* d_q, double* d_p
   });
 }
 
+hfmm_status hfmm_gpu_last_timing(hfmm_gpu* g, hfmm_gpu_timing* timing) {
+  return guard([&] {
+    need(g, "hfmm_gpu_last_timing(gpu)");
+    need(timing, "hfmm_gpu_last_timing(timing)");
+    g->eng->last_timing(timing->ms, &timing->kernel_launches);
+  });
+}
+
 hfmm_status hfmm_gpu_set_charges(hfmm_gpu* g, const double* charges) {
   return guard([&] {
     need(g, "hfmm_gpu_set_charges(gpu)");
@@ -199,6 +208,16 @@ hfmm_status hfmm_gpu_direct(const double* positions, const double* charges, size
     need(obs, "hfmm_gpu_direct(observers)");
     need(pot_out, "hfmm_gpu_direct(pot_out)");
     hfmm_b200::direct_sum(positions, charges, n, obs, m, k, device, pot_out);
+  });
+}
+
+hfmm_status hfmm_resample_matrix(int64_t n_in, double s_in, int64_t n_out, double s_out,
+                                 double* out) {
+  return guard([&] {
+    need(out, "hfmm_resample_matrix(out)");
+    if (n_in <= 0 || n_out <= 0) throw std::invalid_argument("resample_circle: bad sizes");
+    auto m = hfmm_b200::resample_matrix(n_in, s_in, n_out, s_out);
+    std::memcpy(out, m.data(), m.size() * sizeof(double));
   });
 }
 

@@ -293,6 +293,9 @@ void Engine::phase_m2m() {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
+    const size_t smem0 = size_t(nc) * nc * sizeof(double2);
+    if (smem0 > 48 * 1024)
+      ck(cudaFuncSetAttribute(k_m2m_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem0)), "attr");
     k_m2m_phi<<<unsigned(C.n_nodes), 256, size_t(nc) * nc * sizeof(double2), st_>>>(nc, np, 0, C.mp, P.PuT,
                                                                                    d_tmp);
     ++launches_;
@@ -392,6 +395,32 @@ void Engine::run_phase(int phase) {
 
 void Engine::evaluate(double* ms) {
   ck(cudaSetDevice(dev_), "cudaSetDevice");
+  evaluate_device(nullptr, nullptr, nullptr);
+  ck(cudaStreamSynchronize(st_), "evaluate");
+  if (ms) last_timing(ms, nullptr);
+}
+
+void Engine::last_timing(double* ms, int64_t* launches) {
+  if (!timed_) throw std::logic_error("last_timing: no evaluation recorded");
+  ck(cudaEventSynchronize(ev_[7]), "event sync");
+  float f = 0.f;
+  for (int i = 0; i < 7; ++i) {
+    cudaEventElapsedTime(&f, ev_[i], ev_[i + 1]);
+    ms[i] = f;
+  }
+  cudaEventElapsedTime(&f, ev_[0], ev_[7]);
+  ms[7] = f;
+  if (launches) *launches = last_launches_;
+}
+
+void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cudaStream_t st) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  cudaStream_t saved = st_;
+  if (st) st_ = st;
+  const int64_t l0 = launches_;
+  const int64_t n = int64_t(s_.n);
+  if (d_q_sorted && d_q_sorted != reinterpret_cast<const double*>(d_q))
+    ck(cudaMemcpyAsync(d_q, d_q_sorted, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "q");
   cudaEventRecord(ev_[0], st_);
   build_T();
   cudaEventRecord(ev_[1], st_);
@@ -407,41 +436,17 @@ void Engine::evaluate(double* ms) {
   cudaEventRecord(ev_[6], st_);
   phase_near();
   cudaEventRecord(ev_[7], st_);
-  ck(cudaStreamSynchronize(st_), "evaluate");
-  if (ms) {
-    float f = 0.f;
-    for (int i = 0; i < 7; ++i) {
-      cudaEventElapsedTime(&f, ev_[i], ev_[i + 1]);
-      ms[i] = f;
-    }
-    cudaEventElapsedTime(&f, ev_[0], ev_[7]);
-    ms[7] = f;
-  }
-}
-
-void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cudaStream_t st) {
-  ck(cudaSetDevice(dev_), "cudaSetDevice");
-  cudaStream_t saved = st_;
-  if (st) st_ = st;
-  const int64_t n = int64_t(s_.n);
-  if (d_q_sorted && d_q_sorted != reinterpret_cast<const double*>(d_q))
-    ck(cudaMemcpyAsync(d_q, d_q_sorted, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "q");
-  build_T();
-  phase_c2m();
-  phase_m2m();
-  phase_m2l();
-  phase_l2l();
-  phase_l2t();
-  phase_near();
   if (d_pot_sorted)
     ck(cudaMemcpyAsync(d_pot_sorted, d_pot, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "pot");
+  last_launches_ = launches_ - l0;
+  timed_ = true;
   st_ = saved;
 }
 
 void Engine::evaluate_host(const double* q_in, double* pot_out, double* ms) {
   ck(cudaSetDevice(dev_), "cudaSetDevice");
   if (q_in) set_charges(q_in);
-  evaluate(ms);
+  evaluate_device(nullptr, nullptr, nullptr);
   const int64_t cnt = part_e_ - part_b_;
   if (cnt > 0) {
     k_scatter_pot<<<unsigned((cnt + 255) / 256), 256, 0, st_>>>(part_b_, part_e_, d_orig, d_pot, d_pot_in);
@@ -454,6 +459,7 @@ void Engine::evaluate_host(const double* q_in, double* pot_out, double* ms) {
     throw std::logic_error("evaluate_host: multi-rank gather not supported here");
   }
   ck(cudaStreamSynchronize(st_), "evaluate_host");
+  if (ms) last_timing(ms, nullptr);
 }
 
 void Engine::get_expansion(int kind, int level, double* out, size_t cap) {

@@ -63,6 +63,8 @@ class Engine {
   void get_expansion(int kind, int level, double* out, size_t cap_doubles);
   void get_potentials_sorted(double* out, size_t cap_doubles);
   int64_t launches() const { return launches_; }
+  // Per-phase ms of the last evaluation (events on its stream), [0] T build .. [7] total.
+  void last_timing(double* ms, int64_t* launches);
 
  private:
   void upload();
@@ -102,6 +104,8 @@ class Engine {
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range
   int64_t part_b_ = 0, part_e_ = 0;  // owned particle range
   cudaEvent_t ev_[8] = {};
+  int64_t last_launches_ = 0;
+  bool timed_ = false;
 };
 
 // Device O(N M) direct sum (kernel.cpp:16-41) for the accuracy checks.

@@ -218,6 +218,12 @@ class RankEngine:
                                              ctypes.c_void_p(d_pot_sorted_ptr),
                                              ctypes.c_void_p(stream_ptr)))
 
+    def last_timing(self) -> tuple[dict, int]:
+        """Per-phase device ms and kernel launches of the last evaluation."""
+        t = _native.TimingC()
+        check(lib().hfmm_gpu_last_timing(self._h, ctypes.byref(t)))
+        return {k: float(v) for k, v in zip(_PHASE_NAMES, t.ms)}, int(t.kernel_launches)
+
     def close(self):
         h, self._h = getattr(self, "_h", None), None
         if h and _native._lib is not None:
@@ -265,3 +271,11 @@ def generate_inputs(shape: str, n: int, extent: float, seed: int):
     q = np.empty((n, 2))
     lib().hfmm_generate_inputs(0 if shape == "cube" else 1, n, float(extent), int(seed), ptr(pos), ptr(q))
     return pos, q[:, 0] + 1j * q[:, 1]
+
+
+def resample_matrix(n_in: int, s_in: float, n_out: int, s_out: float) -> np.ndarray:
+    """Dense (n_out, n_in) complex matrix of resample_circle (sphere_grid.cpp:128-155)
+    as applied by the device M2M/L2L kernels."""
+    out = np.empty((n_out, n_in, 2))
+    check(lib().hfmm_resample_matrix(int(n_in), float(s_in), int(n_out), float(s_out), ptr(out)))
+    return out[..., 0] + 1j * out[..., 1]
