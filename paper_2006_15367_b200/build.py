@@ -19,7 +19,7 @@ LIB = os.path.join(OUT_DIR, "libhfmm_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["setup.cpp", "engine.cu", "capi.cu"]
-HEADERS = ["setup.hpp", "engine.hpp", "kernels.cuh", "interp.hpp", "inputs.hpp"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h")))
 
 
 def _nvcc() -> str:

@@ -3,12 +3,15 @@
 
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 
 #include "interp.hpp"
 #include "kernels.cuh"
+#include "m2l.cuh"
+#include "interp_tc.cuh"
 
 namespace hfmm_b200 {
 
@@ -70,6 +73,71 @@ Engine::~Engine() {
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (st_) cudaStreamDestroy(st_);
+}
+
+namespace {
+int lda_for(int K) { return (K % 8 == 4) ? K : K + 4; }  // row stride == 4 (mod 8) double2
+void set_dims(int* d, int K, int N, bool with_ldo) {
+  d[0] = K;
+  d[1] = N;
+  d[2] = lda_for(K);
+  d[3] = with_ldo ? N + 4 : 0;
+}
+PassDims to_dims(const int* d) { return PassDims{d[0], d[1], d[2], d[3]}; }
+}  // namespace
+
+// Real + rank-1 matrices for the fused tensor-core M2M / L2L of parent level P
+// over child level C, and the shared-memory plan (children per batch).
+void Engine::setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, const LevelData& tc) {
+  const int nc = C.nt, np = P.nt, half = np / 2;
+  // M2M: phi n_c -> n_p (shift 0), theta 2 n_c -> 2 n_p (shift 0.5)
+  RealRank1 uphi = real_rank1(nc, 0.0, np, 0.0);
+  RealRank1 uth = real_rank1(2 * nc, 0.5, 2 * np, 0.5);
+  set_dims(P.up_phi, uphi.K, uphi.N, false);
+  set_dims(P.up_th, uth.K, uth.N, true);
+  P.up_phi_B = upload_vec(uphi.B);
+  P.up_phi_v = upload_vec(uphi.v);
+  P.up_th_B = upload_vec(uth.B);
+  P.up_th_v = upload_vec(uth.v);
+  // L2L: theta 2 n_p -> 2 n_c with w_p (cols) and scale / w_c (rows); phi n_p -> n_c
+  std::vector<double> wp(size_t(2 * np)), wc(size_t(2 * nc));
+  const double scale = (double(P.S) / double(C.S)) * tp.phi_w / tc.phi_w;
+  for (int i = 0; i < 2 * np; ++i) wp[size_t(i)] = tp.theta_w[size_t(i < np ? i : 2 * np - 1 - i)];
+  for (int j = 0; j < 2 * nc; ++j) wc[size_t(j)] = scale / tc.theta_w[size_t(j < nc ? j : 2 * nc - 1 - j)];
+  RealRank1 dth = real_rank1(2 * np, 0.5, 2 * nc, 0.5, &wc, &wp);
+  RealRank1 dphi = real_rank1(np, 0.0, nc, 0.0);
+  set_dims(P.dn_th, dth.K, dth.N, false);
+  set_dims(P.dn_phi, dphi.K, dphi.N, false);
+  P.dn_th_B = upload_vec(dth.B);
+  P.dn_th_v = upload_vec(dth.v);
+  P.dn_phi_B = upload_vec(dphi.B);
+  P.dn_phi_v = upload_vec(dphi.v);
+  // Shared-memory plans (double2 counts), children per batch CB in {4, 2, 1}.
+  const size_t budget = 110 * 1024, hard = 227 * 1024;
+  const char* force_cb = std::getenv("HFMM_FUSED_CB");  // debugging aid
+  const int max_cb = force_cb ? std::atoi(force_cb) : 4;
+  for (int cb : {4, 2, 1}) {
+    if (cb > max_cb) continue;
+    const size_t xs = size_t(cb) * nc * P.up_phi[2], gs = size_t(cb) * half * P.up_th[3];
+    const size_t bytes = (std::max(xs, gs) + size_t(cb) * half * P.up_th[2]) * sizeof(double2);
+    if (bytes <= budget || (cb == 1 && bytes <= hard)) {
+      P.m2m_cb = cb;
+      P.m2m_smem = bytes;
+      P.m2m_fused = P.S <= int64_t(kFusedE) * kFusedThreads && !std::getenv("HFMM_NO_FUSED");
+      break;
+    }
+  }
+  for (int cb : {4, 2, 1}) {
+    if (cb > max_cb) continue;
+    const size_t bytes = (size_t(P.S) + size_t(cb) * half * P.dn_th[2] + size_t(cb) * nc * P.dn_phi[2]) *
+                         sizeof(double2);
+    if (bytes <= budget || (cb == 1 && bytes <= hard)) {
+      P.l2l_cb = cb;
+      P.l2l_smem = bytes;
+      P.l2l_fused = !std::getenv("HFMM_NO_FUSED");
+      break;
+    }
+  }
 }
 
 void Engine::upload() {
@@ -174,6 +242,19 @@ void Engine::upload() {
       }
     }
     d.tcoef = upload_vec(coef);
+    // Dense cell lookup for well-populated levels (stencil M2L).
+    d.G = 1 << (l - 1);
+    const double cells = double(d.G) * d.G * d.G;
+    if (d.n_far > 0 && d.G <= 512 && double(d.n_nodes) >= 0.25 * cells) {
+      std::vector<int> lk(size_t(cells), -1);
+      for (size_t i = 0; i < t.num_nodes(); ++i) {
+        const uint64_t c = t.codes[i];
+        const size_t gx = cell_axis(c, l, 0), gy = cell_axis(c, l, 1), gz = cell_axis(c, l, 2);
+        lk[(gz * size_t(d.G) + gy) * size_t(d.G) + gx] = int(i);
+      }
+      d.lookup = upload_vec(lk);
+      d.dense = true;
+    }
     d.T = alloc<double2>(size_t(kSlots) * size_t(d.S));
     // Child CSR, parent links and octants.
     if (l < L) {
@@ -245,6 +326,7 @@ void Engine::upload() {
     }
     P.shift_up = upload_vec(up);
     P.shift_dn = upload_vec(dn);
+    setup_fused(P, C, tp, tc);
     tmp = std::max(tmp, size_t(C.n_nodes) * size_t(nc) * size_t(np));
   }
   tmp_elems_ = tmp;
@@ -293,6 +375,15 @@ void Engine::phase_m2m() {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
+    if (P.m2m_fused) {
+      ck(cudaFuncSetAttribute(k_m2m_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.m2m_smem)), "attr");
+      k_m2m_fused<<<unsigned(P.n_nodes), kFusedThreads, P.m2m_smem, st_>>>(
+          nc, np, P.m2m_cb, to_dims(P.up_phi), to_dims(P.up_th), P.child_off, P.children, oct_[size_t(l + 1)],
+          C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up);
+      ++launches_;
+      ck(cudaGetLastError(), "k_m2m_fused");
+      continue;
+    }
     const size_t smem0 = size_t(nc) * nc * sizeof(double2);
     if (smem0 > 48 * 1024)
       ck(cudaFuncSetAttribute(k_m2m_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem0)), "attr");
@@ -313,10 +404,17 @@ void Engine::phase_m2m() {
 }
 
 void Engine::phase_m2l() {
+  ck(cudaFuncSetAttribute(k_m2l_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
   for (int l = s_.top; l <= s_.L; ++l) {
     DevLevel& d = lv_[size_t(l)];
-    dim3 grid(unsigned(d.n_nodes), unsigned((d.S + 127) / 128));
-    k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, d.far_off, d.far, d.T, d.mp, d.loc);
+    if (d.dense) {
+      const int nb = (d.G + m2l::MB - 1) / m2l::MB;
+      dim3 grid(unsigned(nb * nb * nb), unsigned(d.S / 2));
+      k_m2l_dense<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, d.lookup, d.T, d.mp, d.loc);
+    } else {
+      dim3 grid(unsigned(d.n_nodes), unsigned((d.S + 127) / 128));
+      k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, d.far_off, d.far, d.T, d.mp, d.loc);
+    }
     ++launches_;
   }
   ck(cudaGetLastError(), "m2l");
@@ -327,6 +425,15 @@ void Engine::phase_l2l() {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
+    if (P.l2l_fused) {
+      ck(cudaFuncSetAttribute(k_l2l_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.l2l_smem)), "attr");
+      k_l2l_fused<<<unsigned(P.n_nodes), kFusedThreads, P.l2l_smem, st_>>>(
+          nc, np, P.l2l_cb, to_dims(P.dn_th), to_dims(P.dn_phi), P.child_off, P.children, oct_[size_t(l + 1)],
+          P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn);
+      ++launches_;
+      ck(cudaGetLastError(), "k_l2l_fused");
+      continue;
+    }
     const int half = np / 2;
     const int CP = theta_chunk(half, 2 * nc, 256);
     dim3 grid(unsigned(C.n_nodes), unsigned((half + CP - 1) / CP));

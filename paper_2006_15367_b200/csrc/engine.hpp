@@ -31,6 +31,9 @@ struct DevLevel {
   double2* T = nullptr;       // 343*S translation operator samples
   double2* tcoef = nullptr;   // 343*(trunc+1) Legendre-series coefficients
   uint8_t* slot_used = nullptr;
+  int G = 0;                  // cells per axis = 2^(level-1)
+  int* lookup = nullptr;      // dense row-major cell -> node index (-1 empty), dense levels only
+  bool dense = false;         // M2L as a stencil over the cell grid (m2l.cuh)
   int* child_off = nullptr;   // n_nodes+1 (children at level+1)
   int* children = nullptr;
   int* parent = nullptr;      // n_nodes, parent index at level-1 (or -1)
@@ -41,6 +44,20 @@ struct DevLevel {
   double2* TdT = nullptr;  // theta downsample with weights folded, transposed [2n_p][2n_c]
   double2* shift_up = nullptr;  // 8*S: exp(+i k khat.(c_child - c_parent)) on this grid
   double2* shift_dn = nullptr;  // 8*S: exp(+i k khat.(c_parent - c_child))
+  // Fused tensor-core M2M / L2L (interp_tc.cuh): real matrices + rank-1 vectors.
+  bool m2m_fused = false, l2l_fused = false;
+  int m2m_cb = 1, l2l_cb = 1;
+  size_t m2m_smem = 0, l2l_smem = 0;
+  int up_phi[4] = {0, 0, 0, 0}, up_th[4] = {0, 0, 0, 0};  // PassDims {K, N, lda, ldo}
+  int dn_th[4] = {0, 0, 0, 0}, dn_phi[4] = {0, 0, 0, 0};
+  double* up_phi_B = nullptr;
+  double* up_phi_v = nullptr;
+  double* up_th_B = nullptr;
+  double* up_th_v = nullptr;
+  double* dn_th_B = nullptr;
+  double* dn_th_v = nullptr;
+  double* dn_phi_B = nullptr;
+  double* dn_phi_v = nullptr;
 };
 
 class Engine {
@@ -68,6 +85,7 @@ class Engine {
 
  private:
   void upload();
+  void setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, const LevelData& tc);
   void build_T();
   void phase_c2m();
   void phase_m2m();

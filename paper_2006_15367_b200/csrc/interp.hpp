@@ -13,8 +13,10 @@
 #ifndef HFMM_B200_INTERP_HPP
 #define HFMM_B200_INTERP_HPP
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <stdexcept>
 #include <vector>
 
 namespace hfmm_b200 {
@@ -57,6 +59,67 @@ inline std::vector<double> resample_matrix(int64_t n_in, double s_in, int64_t n_
       M[size_t(2 * (j * n_in + i) + 1)] = double(im / (long double)n_in);
     }
   return M;
+}
+
+// Real + rank-1 split of a resampling map, M = R + i u v^T, laid out as the
+// B operand of the fused tensor-core passes: B is (K x N) row-major with
+// B[k][n] = R[n][k] (k < n_in), B[n_in][n] = u[n], zero padding elsewhere;
+// K = round_up(n_in + 1, 4), N = round_up(n_out, 8).  row_scale / col_scale
+// (optional, length n_out / n_in) multiply M from the left / right.
+struct RealRank1 {
+  int K = 0, N = 0;
+  std::vector<double> B;  // K*N
+  std::vector<double> v;  // n_in
+};
+
+inline RealRank1 real_rank1(int64_t n_in, double s_in, int64_t n_out, double s_out,
+                            const std::vector<double>* row_scale = nullptr,
+                            const std::vector<double>* col_scale = nullptr) {
+  const std::vector<double> M = resample_matrix(n_in, s_in, n_out, s_out);
+  const int64_t Kw = std::min(n_in, n_out);
+  const long double pi = 3.141592653589793238462643383279503L;
+  // Im(M)[j][i] = -(1/n_in) sin(K pi (a_j - b_i)) = u1_j v1_i + u2_j v2_i
+  std::vector<long double> u1(static_cast<size_t>(n_out)), u2(static_cast<size_t>(n_out)), v1(static_cast<size_t>(n_in)), v2(static_cast<size_t>(n_in));
+  for (int64_t j = 0; j < n_out; ++j) {
+    const long double a = ((long double)j + s_out) / (long double)n_out;
+    u1[size_t(j)] = -sinl(Kw * pi * a) / (long double)n_in;
+    u2[size_t(j)] = cosl(Kw * pi * a) / (long double)n_in;
+  }
+  for (int64_t i = 0; i < n_in; ++i) {
+    const long double b = ((long double)i + s_in) / (long double)n_in;
+    v1[size_t(i)] = cosl(Kw * pi * b);
+    v2[size_t(i)] = sinl(Kw * pi * b);
+  }
+  auto amax = [](const std::vector<long double>& x) {
+    long double m = 0;
+    for (auto e : x) m = std::max(m, e < 0 ? -e : e);
+    return m;
+  };
+  const bool use1 = amax(u1) * amax(v1) >= amax(u2) * amax(v2);
+  const std::vector<long double>& u = use1 ? u1 : u2;
+  const std::vector<long double>& v = use1 ? v1 : v2;
+  if ((use1 ? amax(u2) * amax(v2) : amax(u1) * amax(v1)) > 1e-13L)
+    throw std::logic_error("real_rank1: imaginary part is not rank one");
+  RealRank1 out;
+  out.K = int((n_in + 1 + 3) / 4 * 4);
+  out.N = int((n_out + 7) / 8 * 8);
+  out.B.assign(size_t(out.K) * size_t(out.N), 0.0);
+  out.v.resize(size_t(n_in));
+  for (int64_t j = 0; j < n_out; ++j) {
+    const double rs = row_scale ? (*row_scale)[size_t(j)] : 1.0;
+    for (int64_t i = 0; i < n_in; ++i) {
+      const double cs = col_scale ? (*col_scale)[size_t(i)] : 1.0;
+      const double re = M[size_t(2 * (j * n_in + i))];
+      const double im = M[size_t(2 * (j * n_in + i) + 1)];
+      if (std::fabs(im - double(u[size_t(j)] * v[size_t(i)])) > 1e-14)
+        throw std::logic_error("real_rank1: rank-one factors do not reproduce the map");
+      out.B[size_t(i) * out.N + size_t(j)] = rs * re * cs;
+    }
+    out.B[size_t(n_in) * out.N + size_t(j)] = rs * double(u[size_t(j)]);
+  }
+  for (int64_t i = 0; i < n_in; ++i)
+    out.v[size_t(i)] = double(v[size_t(i)]) * (col_scale ? (*col_scale)[size_t(i)] : 1.0);
+  return out;
 }
 
 }  // namespace hfmm_b200

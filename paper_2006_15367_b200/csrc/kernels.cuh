@@ -22,6 +22,17 @@ __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
 
 constexpr int kSlots = 343;  // (ox, oy, oz) in [-3, 3]^3
 
+// cp.async (Ampere+ LDGSTS) 16-byte copy; src-size 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }  // (ox, oy, oz) in [-3, 3]^3
+
 // ---------------------------------------------------------------------------
 // Translation operators T[slot][s] (operators.cpp:39-80): Legendre series with
 // host-computed coefficients (-i)^l (2l+1) h_l^(2)(k|D|).

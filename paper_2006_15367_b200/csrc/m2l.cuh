@@ -1,0 +1,141 @@
+// M2L on densely populated levels as a per-sample 3-D stencil.
+//
+// For one sample s the far-field translation of a level (operators.cpp:82-87,
+// traversal.cpp:443-581) is a sparse convolution over the level's cell grid:
+//   L_o[s] = sum_d  T[d][s] * M_{o-d}[s],   d in [-3,3]^3,
+// restricted to far pairs: parents adjacent (Chebyshev <= 1) and the boxes
+// themselves not adjacent (interaction_lists.cpp:54-98).  Whether a pair is
+// far depends only on d and on the parities of o, so the mask is resolved at
+// compile time along x and is warp-uniform along y, z.
+//
+// Work decomposition (B200): one CTA = an 8x8x8 observer block x 2 samples.
+// The 14^3 source region (block + halo 3) for the 2 samples and the 343 T
+// taps are staged in shared memory (~100 KB, 2 CTAs/SM).  Each thread owns an
+// x-row of 8 observers for one sample; for every (dy, dz) tap row it loads the
+// 14 source values of its row once and the 7 taps (a warp broadcast) and
+// issues up to 48 complex FMAs from registers.  A warp holds 16 rows of one
+// (y, z) parity class x 2 samples, so every mask branch is warp-uniform and
+// the padded row stride makes the 16-byte loads bank-conflict free.
+#ifndef HFMM_B200_M2L_CUH
+#define HFMM_B200_M2L_CUH
+
+#include "kernels.cuh"
+
+namespace hfmm_b200 {
+
+namespace m2l {
+constexpr int MB = 8;               // observer block edge
+constexpr int MR = MB + 6;          // source region edge (halo 3)
+constexpr int ROW = MR * 2 + 1;     // double2 per region row (2 samples/cell + 16 B pad)
+constexpr int ZS = MR * ROW;        // double2 per region z-slice
+constexpr int REGION = MR * ZS;     // double2 in the region
+constexpr int SMEM_BYTES = (REGION + kSlots * 2) * 16;
+
+__host__ __device__ constexpr int fdiv2(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }
+__host__ __device__ constexpr int iabs(int v) { return v < 0 ? -v : v; }
+// parent of (2a + p) vs parent of (2a + p - d) are adjacent
+__host__ __device__ constexpr bool parent_near(int p, int d) { return iabs(fdiv2(p - d)) <= 1; }
+
+template <bool INNER>
+__device__ __forceinline__ void tap_row(double2 (&acc)[MB], const double2 (&m)[MR], const double2 (&t)[7]) {
+#pragma unroll
+  for (int k = 0; k < MB; ++k) {
+#pragma unroll
+    for (int dx = -3; dx <= 3; ++dx) {
+      // observer x = 8 bx + k: parent-adjacency along x depends on k and dx only
+      const bool xnear = iabs(fdiv2(k) - fdiv2(k - dx)) <= 1;
+      const bool adjacent = INNER && iabs(dx) <= 1;
+      if (xnear && !adjacent) cmac(acc[k], t[dx + 3], m[k - dx + 3]);
+    }
+  }
+}
+}  // namespace m2l
+
+__global__ void __launch_bounds__(128, 2) k_m2l_dense(int G, int nb, int64_t S,
+                                                      const int* __restrict__ lookup,
+                                                      const double2* __restrict__ T,
+                                                      const double2* __restrict__ mp,
+                                                      double2* __restrict__ loc) {
+  using namespace m2l;
+  extern __shared__ double2 smem[];
+  double2* Ms = smem;
+  double2* Ts = smem + REGION;
+  const int blk = blockIdx.x;
+  const int bx = (blk % nb) * MB, by = ((blk / nb) % nb) * MB, bz = (blk / (nb * nb)) * MB;
+  const int64_t s0 = int64_t(blockIdx.y) * 2;
+
+  // Stage T taps and the source region with cp.async (LDGSTS): every load is
+  // in flight at once; empty / out-of-grid cells are zero-filled by the copy.
+  for (int t = threadIdx.x; t < kSlots * 2; t += blockDim.x)
+    cp_async16(Ts + t, T + int64_t(t >> 1) * S + s0 + (t & 1), true);
+  constexpr int NCOPY = MR * MR * MR * 2;
+  constexpr int BATCH = 8;
+  for (int base = threadIdx.x; base < NCOPY; base += BATCH * 128) {
+    int node[BATCH];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int t = base + u * 128;
+      const int c = t >> 1;
+      const int cx = c % MR, cy = (c / MR) % MR, cz = c / (MR * MR);
+      const int gx = bx - 3 + cx, gy = by - 3 + cy, gz = bz - 3 + cz;
+      node[u] = -1;
+      if (t < NCOPY && gx >= 0 && gy >= 0 && gz >= 0 && gx < G && gy < G && gz < G)
+        node[u] = __ldg(lookup + (int64_t(gz) * G + gy) * G + gx);
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int t = base + u * 128;
+      if (t < NCOPY) {
+        const int sw = t & 1, c = t >> 1;
+        const int cx = c % MR, cy = (c / MR) % MR, cz = c / (MR * MR);
+        const bool ok = node[u] >= 0;
+        cp_async16(Ms + cz * ZS + cy * ROW + cx * 2 + sw, mp + (ok ? int64_t(node[u]) * S + s0 + sw : 0), ok);
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int py = warp & 1, pz = warp >> 1;
+  const int sw = lane & 1, r = lane >> 1;
+  const int oy = 2 * (r & 3) + py, oz = 2 * (r >> 2) + pz;
+  double2 acc[MB];
+#pragma unroll
+  for (int k = 0; k < MB; ++k) acc[k] = make_double2(0.0, 0.0);
+
+  for (int dz = -3; dz <= 3; ++dz) {
+    if (!parent_near(pz, dz)) continue;
+    for (int dy = -3; dy <= 3; ++dy) {
+      if (!parent_near(py, dy)) continue;
+      const double2* row = Ms + (oz - dz + 3) * ZS + (oy - dy + 3) * ROW + sw;
+      double2 m[MR];
+#pragma unroll
+      for (int i = 0; i < MR; ++i) m[i] = row[2 * i];
+      const double2* trow = Ts + ((dy + 3) * 7 + (dz + 3)) * 2 + sw;
+      double2 t[7];
+#pragma unroll
+      for (int j = 0; j < 7; ++j) t[j] = trow[j * 49 * 2];
+      if (iabs(dy) <= 1 && iabs(dz) <= 1)
+        tap_row<true>(acc, m, t);
+      else
+        tap_row<false>(acc, m, t);
+    }
+  }
+
+  const int gy = by + oy, gz = bz + oz;
+  if (gy < G && gz < G) {
+#pragma unroll
+    for (int k = 0; k < MB; ++k) {
+      const int gx = bx + k;
+      if (gx < G) {
+        const int node = lookup[(int64_t(gz) * G + gy) * G + gx];
+        if (node >= 0) loc[int64_t(node) * S + s0 + sw] = acc[k];
+      }
+    }
+  }
+}
+
+}  // namespace hfmm_b200
+
+#endif
