@@ -12,6 +12,7 @@
 #include "kernels.cuh"
 #include "m2l.cuh"
 #include "interp_tc.cuh"
+#include "interp_ct.cuh"
 
 namespace hfmm_b200 {
 
@@ -60,6 +61,7 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
     throw std::invalid_argument(
         "hfmm_gpu_create: multi-rank device evaluation is driven by the distributed runner");
   ck(cudaSetDevice(device), "cudaSetDevice");
+  use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;  // debugging aid: runtime-shaped kernels only
   ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
   upload();
@@ -112,31 +114,42 @@ void Engine::setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, co
   P.dn_th_v = upload_vec(dth.v);
   P.dn_phi_B = upload_vec(dphi.B);
   P.dn_phi_v = upload_vec(dphi.v);
-  // Shared-memory plans (double2 counts), children per batch CB in {4, 2, 1}.
-  const size_t budget = 110 * 1024, hard = 227 * 1024;
-  const char* force_cb = std::getenv("HFMM_FUSED_CB");  // debugging aid
+  // Shared-memory plans: children per batch CB and buffering; prefer two
+  // CTAs per SM, else one.  HFMM_FUSED_CB caps CB, HFMM_NO_FUSED disables
+  // the fused path (debugging aids).
+  const char* force_cb = std::getenv("HFMM_FUSED_CB");
   const int max_cb = force_cb ? std::atoi(force_cb) : 4;
-  for (int cb : {4, 2, 1}) {
-    if (cb > max_cb) continue;
-    const size_t xs = size_t(cb) * nc * P.up_phi[2], gs = size_t(cb) * half * P.up_th[3];
-    const size_t bytes = (std::max(xs, gs) + size_t(cb) * half * P.up_th[2]) * sizeof(double2);
-    if (bytes <= budget || (cb == 1 && bytes <= hard)) {
-      P.m2m_cb = cb;
-      P.m2m_smem = bytes;
-      P.m2m_fused = P.S <= int64_t(kFusedE) * kFusedThreads && !std::getenv("HFMM_NO_FUSED");
-      break;
-    }
+  const bool allow = std::getenv("HFMM_NO_FUSED") == nullptr;
+  const std::pair<int, int> order[] = {{4, 1}, {2, 1}, {4, 0}, {2, 0}, {1, 1}, {1, 0}};
+  auto m2m_bytes = [&](int cb, int db) {
+    return (size_t(db ? 2 : 1) * cb * nc * P.up_phi[2] + size_t(cb) * half * P.up_th[2] + size_t(P.S)) *
+           sizeof(double2);
+  };
+  auto l2l_bytes = [&](int cb, int db) {
+    return (size_t(db ? P.S : 0) + size_t(cb) * half * P.dn_th[2] + size_t(cb) * nc * P.dn_phi[2]) *
+           sizeof(double2);
+  };
+  for (size_t budget : {size_t(113 * 1024), size_t(227 * 1024)}) {
+    if (P.m2m_fused || !allow) break;
+    for (auto [cb, db] : order)
+      if (cb <= max_cb && m2m_bytes(cb, db) <= budget) {
+        P.m2m_plan[0] = cb;
+        P.m2m_plan[1] = db;
+        P.m2m_plan[2] = int(m2m_bytes(cb, db));
+        P.m2m_fused = true;
+        break;
+      }
   }
-  for (int cb : {4, 2, 1}) {
-    if (cb > max_cb) continue;
-    const size_t bytes = (size_t(P.S) + size_t(cb) * half * P.dn_th[2] + size_t(cb) * nc * P.dn_phi[2]) *
-                         sizeof(double2);
-    if (bytes <= budget || (cb == 1 && bytes <= hard)) {
-      P.l2l_cb = cb;
-      P.l2l_smem = bytes;
-      P.l2l_fused = !std::getenv("HFMM_NO_FUSED");
-      break;
-    }
+  for (size_t budget : {size_t(113 * 1024), size_t(227 * 1024)}) {
+    if (P.l2l_fused || !allow) break;
+    for (auto [cb, db] : order)
+      if (cb <= max_cb && l2l_bytes(cb, db) <= budget) {
+        P.l2l_plan[0] = cb;
+        P.l2l_plan[1] = db;
+        P.l2l_plan[2] = int(l2l_bytes(cb, db));
+        P.l2l_fused = true;
+        break;
+      }
   }
 }
 
@@ -375,10 +388,18 @@ void Engine::phase_m2m() {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
+    const CtLaunch cl{P.n_nodes, 0, P.child_off, P.children, oct_[size_t(l + 1)], st_};
+    if (use_ct_ && launch_m2m_ct(nc, np, cl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v,
+                                 P.shift_up)) {
+      ++launches_;
+      ck(cudaGetLastError(), "k_m2m_ct");
+      continue;
+    }
     if (P.m2m_fused) {
-      ck(cudaFuncSetAttribute(k_m2m_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.m2m_smem)), "attr");
-      k_m2m_fused<<<unsigned(P.n_nodes), kFusedThreads, P.m2m_smem, st_>>>(
-          nc, np, P.m2m_cb, to_dims(P.up_phi), to_dims(P.up_th), P.child_off, P.children, oct_[size_t(l + 1)],
+      const FusedPlan fp{P.m2m_plan[0], P.m2m_plan[1], P.m2m_plan[2]};
+      ck(cudaFuncSetAttribute(k_m2m_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
+      k_m2m_fused<<<unsigned(P.n_nodes), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
+          nc, np, fp, to_dims(P.up_phi), to_dims(P.up_th), P.child_off, P.children, oct_[size_t(l + 1)],
           C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up);
       ++launches_;
       ck(cudaGetLastError(), "k_m2m_fused");
@@ -425,10 +446,18 @@ void Engine::phase_l2l() {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
+    const CtLaunch cl{P.n_nodes, 0, P.child_off, P.children, oct_[size_t(l + 1)], st_};
+    if (use_ct_ && launch_l2l_ct(nc, np, cl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v,
+                                 P.shift_dn)) {
+      ++launches_;
+      ck(cudaGetLastError(), "k_l2l_ct");
+      continue;
+    }
     if (P.l2l_fused) {
-      ck(cudaFuncSetAttribute(k_l2l_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.l2l_smem)), "attr");
-      k_l2l_fused<<<unsigned(P.n_nodes), kFusedThreads, P.l2l_smem, st_>>>(
-          nc, np, P.l2l_cb, to_dims(P.dn_th), to_dims(P.dn_phi), P.child_off, P.children, oct_[size_t(l + 1)],
+      const FusedPlan fp{P.l2l_plan[0], P.l2l_plan[1], P.l2l_plan[2]};
+      ck(cudaFuncSetAttribute(k_l2l_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
+      k_l2l_fused<<<unsigned(P.n_nodes), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
+          nc, np, fp, to_dims(P.dn_th), to_dims(P.dn_phi), P.child_off, P.children, oct_[size_t(l + 1)],
           P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn);
       ++launches_;
       ck(cudaGetLastError(), "k_l2l_fused");

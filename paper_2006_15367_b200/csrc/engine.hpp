@@ -46,8 +46,7 @@ struct DevLevel {
   double2* shift_dn = nullptr;  // 8*S: exp(+i k khat.(c_parent - c_child))
   // Fused tensor-core M2M / L2L (interp_tc.cuh): real matrices + rank-1 vectors.
   bool m2m_fused = false, l2l_fused = false;
-  int m2m_cb = 1, l2l_cb = 1;
-  size_t m2m_smem = 0, l2l_smem = 0;
+  int m2m_plan[3] = {1, 0, 0}, l2l_plan[3] = {1, 0, 0};  // FusedPlan {CB, dbuf, smem bytes}
   int up_phi[4] = {0, 0, 0, 0}, up_th[4] = {0, 0, 0, 0};  // PassDims {K, N, lda, ldo}
   int dn_th[4] = {0, 0, 0, 0}, dn_phi[4] = {0, 0, 0, 0};
   double* up_phi_B = nullptr;
@@ -105,6 +104,7 @@ class Engine {
   std::vector<uint8_t*> oct_;  // per level: child octant (code & 7) of each node
   std::vector<void*> allocs_;
   int64_t launches_ = 0;
+  bool use_ct_ = true;
   // particles (sorted)
   double* d_x = nullptr;
   double* d_y = nullptr;

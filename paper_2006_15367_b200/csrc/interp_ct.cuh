@@ -1,0 +1,452 @@
+// Compile-time-shaped fused M2M / L2L (DMMA) for the level pairs of the
+// BASELINE configurations.  Same algorithm as interp_tc.cuh (see its header
+// for the real + rank-1 split and the row orderings); with (n_c, n_p) known
+// at compile time every index map folds to constants, the k-loops unroll,
+// padded 8x8 sub-tiles are skipped statically, the two real B matrices live
+// in shared memory for the CTA's lifetime, and CTAs are persistent over
+// parents so the B staging and the Sacc setup are amortised.
+#ifndef HFMM_B200_INTERP_CT_CUH
+#define HFMM_B200_INTERP_CT_CUH
+
+#include "interp_tc.cuh"
+
+namespace hfmm_b200 {
+namespace ct {
+
+__host__ __device__ constexpr int round4(int v) { return (v + 3) / 4 * 4; }
+__host__ __device__ constexpr int round8(int v) { return (v + 7) / 8 * 8; }
+__host__ __device__ constexpr int lda_for(int K) { return (K % 8 == 4) ? K : K + 4; }
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+template <int NC, int NP>
+struct Shape {
+  static constexpr int HALF = NP / 2, SC = NC * NC, SP = NP * NP;
+  // M2M passes
+  static constexpr int UPHI_K = round4(NC + 1), UPHI_N = round8(NP), UPHI_LDA = lda_for(UPHI_K);
+  static constexpr int UTH_K = round4(2 * NC + 1), UTH_N = round8(2 * NP), UTH_LDA = lda_for(UTH_K);
+  // L2L passes
+  static constexpr int DTH_K = round4(2 * NP + 1), DTH_N = round8(2 * NC), DTH_LDA = lda_for(DTH_K);
+  static constexpr int DPHI_K = round4(NP + 1), DPHI_N = round8(NC), DPHI_LDA = lda_for(DPHI_K);
+  // shared-memory footprints in bytes
+  static constexpr int m2m_bytes(int cb, int db) {
+    return ((db ? 2 : 1) * cb * NC * UPHI_LDA + cb * HALF * UTH_LDA + SP) * 16 +
+           (UPHI_K * UPHI_N + UTH_K * UTH_N) * 8;
+  }
+  static constexpr int l2l_bytes(int cb, int db) {
+    return ((db ? SP : 0) + cb * HALF * DTH_LDA + cb * NC * DPHI_LDA) * 16 + (DTH_K * DTH_N + DPHI_K * DPHI_N) * 8;
+  }
+  // plan: children per batch and buffering, two CTAs/SM if possible
+  static constexpr int kBudget2 = 113 * 1024, kBudget1 = 227 * 1024;
+  static constexpr int pick(bool m2m, int budget, int which) {
+    const int cbs[6] = {4, 2, 4, 2, 1, 1}, dbs[6] = {1, 1, 0, 0, 1, 0};
+    for (int i = 0; i < 6; ++i) {
+      const int b = m2m ? m2m_bytes(cbs[i], dbs[i]) : l2l_bytes(cbs[i], dbs[i]);
+      if (b <= budget) return which == 0 ? cbs[i] : which == 1 ? dbs[i] : b;
+    }
+    return -1;
+  }
+  static constexpr int M2M_CB = pick(true, kBudget2, 0) > 0 ? pick(true, kBudget2, 0) : pick(true, kBudget1, 0);
+  static constexpr int M2M_DB = pick(true, kBudget2, 0) > 0 ? pick(true, kBudget2, 1) : pick(true, kBudget1, 1);
+  static constexpr int M2M_BYTES = M2M_CB > 0 ? m2m_bytes(M2M_CB, M2M_DB) : 0;
+  static constexpr int L2L_CB = pick(false, kBudget2, 0) > 0 ? pick(false, kBudget2, 0) : pick(false, kBudget1, 0);
+  static constexpr int L2L_DB = pick(false, kBudget2, 0) > 0 ? pick(false, kBudget2, 1) : pick(false, kBudget1, 1);
+  static constexpr int L2L_BYTES = L2L_CB > 0 ? l2l_bytes(L2L_CB, L2L_DB) : 0;
+};
+
+// Warp-tiled DMMA GEMM with compile-time shape; B (K x N, row-major) in smem.
+// Warp tile = up to 2 x 2 8x8 sub-tiles; padded sub-tiles are skipped.
+// pre(m0, n0, valid) runs before the k-loop of every 8x8 sub-tile's owner
+// (all lanes), epi(m0, n0, c0, c1) after it (all lanes, may shuffle).
+template <int M, int N, int K, class RowPtr, class Epi>
+__device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ Bs, Epi epi) {
+  constexpr int MT8 = (M + 7) / 8, NT8 = N / 8;
+  constexpr int MT = (MT8 + 1) / 2, NT = (NT8 + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  for (int w = warp; w < MT * NT; w += kWarps) {
+    const int mt = w / NT, nt = w - mt * NT;
+    const int m0 = mt * 16, n0 = nt * 16;
+    const bool vm1 = 2 * mt + 1 < MT8, vn1 = 2 * nt + 1 < NT8;
+    const int r0 = m0 + g, r1 = m0 + 8 + g;
+    const bool ok0 = r0 < M, ok1 = r1 < M;
+    const double* a0p = reinterpret_cast<const double*>(rowp(ok0 ? r0 >> 1 : 0)) + (r0 & 1) + 2 * tq;
+    const double* a1p = reinterpret_cast<const double*>(rowp(ok1 ? r1 >> 1 : 0)) + (r1 & 1) + 2 * tq;
+    const double* bp = Bs + tq * N + n0 + g;
+    double c00a = 0, c00b = 0, c01a = 0, c01b = 0, c10a = 0, c10b = 0, c11a = 0, c11b = 0;
+#pragma unroll
+    for (int k = 0; k < K; k += 4) {
+      const double a0 = ok0 ? a0p[2 * k] : 0.0;
+      const double b0 = bp[k * N];
+      dmma884(c00a, c00b, a0, b0);
+      if (vn1) {
+        const double b1 = bp[k * N + 8];
+        dmma884(c01a, c01b, a0, b1);
+        if (vm1) {
+          const double a1 = ok1 ? a1p[2 * k] : 0.0;
+          dmma884(c10a, c10b, a1, b0);
+          dmma884(c11a, c11b, a1, b1);
+        }
+      } else if (vm1) {
+        const double a1 = ok1 ? a1p[2 * k] : 0.0;
+        dmma884(c10a, c10b, a1, b0);
+      }
+    }
+    epi(m0, n0, c00a, c00b);
+    if (vn1) epi(m0, n0 + 8, c01a, c01b);
+    if (vm1) {
+      epi(m0 + 8, n0, c10a, c10b);
+      if (vn1) epi(m0 + 8, n0 + 8, c11a, c11b);
+    }
+  }
+}
+
+template <int ROWS, int KIN, int LD>
+__device__ __forceinline__ void rank1_ct(double2* X, const double* __restrict__ v) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < ROWS; r += kWarps) {
+    double sr = 0.0, si = 0.0;
+    double2* x = X + r * LD;
+#pragma unroll
+    for (int k = lane; k < KIN; k += 32) {
+      const double vk = __ldg(v + k);
+      const double2 xv = x[k];
+      sr = fma(vk, xv.x, sr);
+      si = fma(vk, xv.y, si);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      sr += __shfl_xor_sync(0xffffffffu, sr, off);
+      si += __shfl_xor_sync(0xffffffffu, si, off);
+    }
+    if (lane == 0) x[KIN] = make_double2(-si, sr);
+  }
+}
+
+__device__ __forceinline__ void stage_doubles(double* dst, const double* __restrict__ src, int n) {
+  for (int t = threadIdx.x * 2; t < n; t += kThreads * 2) {
+    if (t + 1 < n)
+      cp_async16(dst + t, src + t, true);
+    else
+      dst[t] = src[t];
+  }
+}
+
+}  // namespace ct
+
+// ---------------------------------------------------------------------------
+template <int NC, int NP>
+__global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* __restrict__ child_off,
+                                                        const int* __restrict__ children,
+                                                        const uint8_t* __restrict__ oct_c,
+                                                        const double2* __restrict__ mp_c, double2* __restrict__ mp_p,
+                                                        const double* __restrict__ RphiT, const double* __restrict__ vphi,
+                                                        const double* __restrict__ RthT, const double* __restrict__ vth,
+                                                        const double2* __restrict__ shift_up) {
+  using S = ct::Shape<NC, NP>;
+  constexpr int CB = S::M2M_CB, DB = S::M2M_DB, HALF = S::HALF, SP = S::SP, SC = S::SC;
+  constexpr int XSZ = CB * NC * S::UPHI_LDA, R2 = 2 * CB;
+  extern __shared__ double2 sm[];
+  double2* Xb0 = sm;
+  double2* Xb1 = DB ? sm + XSZ : sm;
+  double2* Fs = sm + (DB ? 2 : 1) * XSZ;
+  double2* Sacc = Fs + CB * HALF * S::UTH_LDA;
+  double* Bphi = reinterpret_cast<double*>(Sacc + SP);
+  double* Bth = Bphi + S::UPHI_K * S::UPHI_N;
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+
+  ct::stage_doubles(Bphi, RphiT, S::UPHI_K * S::UPHI_N);
+  ct::stage_doubles(Bth, RthT, S::UTH_K * S::UTH_N);
+  cp_async_commit();
+  for (int t = threadIdx.x; t < CB * HALF * S::UTH_LDA; t += ct::kThreads) Fs[t] = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < SP; t += ct::kThreads) Sacc[t] = make_double2(0.0, 0.0);
+
+  // (parent, batch) sequence of this CTA
+  auto load = [&](double2* X, int par, int b0) {
+    const int ce = child_off[par + 1];
+    const int nb = min(CB, ce - b0);
+    for (int t = threadIdx.x; t < XSZ; t += ct::kThreads) {
+      const int row = t / S::UPHI_LDA, k = t - row * S::UPHI_LDA;
+      const int c = row / NC, i = row - c * NC;
+      const bool ok = c < nb && k < NC;
+      cp_async16(X + t, ok ? mp_c + int64_t(children[b0 + c]) * SC + i * NC + k : mp_c, ok);
+    }
+    cp_async_commit();
+  };
+  int par = blockIdx.x;
+  if (par >= n_par) return;
+  int b0 = child_off[par];
+  load(Xb0, par, b0);
+  int it = 0;
+  while (par < n_par) {
+    const int ce = child_off[par + 1];
+    const int nb = min(CB, ce - b0);
+    // next (parent, batch) of this CTA
+    int npar = par, nb0 = b0 + CB;
+    if (nb0 >= ce) {
+      npar = par + gridDim.x;
+      nb0 = npar < n_par ? child_off[npar] : 0;
+    }
+    double2* X = (it & 1) ? Xb1 : Xb0;
+    if (DB && npar < n_par) {
+      load((it & 1) ? Xb0 : Xb1, npar, nb0);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    ct::rank1_ct<CB * NC, NC, S::UPHI_LDA>(X, vphi);
+    __syncthreads();
+    // phi pass -> folded circles
+    ct::gemm_ct<CB * NC * 2, S::UPHI_N, S::UPHI_K>(
+        [&](int r) { return X + r * S::UPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1) {
+          const int r = m0 + g, ci = r >> 1, c = ci / NC, i = ci - c * NC;
+          if (c >= CB) return;
+          double2* base = Fs + c * HALF * S::UTH_LDA;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = n0 + 2 * tq + q;
+            if (n < NP) {
+              const int p = n < HALF ? n : n - HALF;
+              const int ii = n < HALF ? i : 2 * NC - 1 - i;
+              set_part(base + p * S::UTH_LDA + ii, r & 1, q ? v1 : v0);
+            }
+          }
+        });
+    __syncthreads();
+    if (!DB && npar < n_par) load(Xb0, npar, nb0);  // single buffer: overlap the next load with theta
+    ct::rank1_ct<CB * HALF, 2 * NC, S::UTH_LDA>(Fs, vth);
+    __syncthreads();
+    int octs[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) octs[c] = c < nb ? oct_c[children[b0 + c]] : 0;
+    // theta pass, rows (circle, child, re/im); children reduce in-warp
+    ct::gemm_ct<HALF * R2, S::UTH_N, S::UTH_K>(
+        [&](int row) {
+          const int p = row / CB, c = row - p * CB;
+          return Fs + (c * HALF + p) * S::UTH_LDA;
+        },
+        Bth, [&](int m0, int n0, double v0, double v1) {
+          const int r = m0 + g, part = r & 1, c = (r >> 1) % CB, p = r / R2;
+          const double o0 = __shfl_xor_sync(0xffffffffu, v0, 4);
+          const double o1 = __shfl_xor_sync(0xffffffffu, v1, 4);
+          const bool live = c < nb && p < HALF;
+          const double2* sh = shift_up + octs[c] * SP;
+          double cr[2], cim[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = n0 + 2 * tq + q;
+            const double re = part ? (q ? o1 : o0) : (q ? v1 : v0);
+            const double im = part ? (q ? v1 : v0) : (q ? o1 : o0);
+            const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
+            double2 f = make_double2(0.0, 0.0);
+            if (live && n < 2 * NP) f = __ldg(sh + s);
+            cr[q] = re * f.x - im * f.y;
+            cim[q] = re * f.y + im * f.x;
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (CB >= 2) {
+              cr[q] += __shfl_xor_sync(0xffffffffu, cr[q], 8);
+              cim[q] += __shfl_xor_sync(0xffffffffu, cim[q], 8);
+            }
+            if (CB >= 4) {
+              cr[q] += __shfl_xor_sync(0xffffffffu, cr[q], 16);
+              cim[q] += __shfl_xor_sync(0xffffffffu, cim[q], 16);
+            }
+          }
+          if (part == 0 && c == 0 && p < HALF) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int n = n0 + 2 * tq + q;
+              if (n < 2 * NP) {
+                const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
+                double2 a = Sacc[s];
+                a.x += cr[q];
+                a.y += cim[q];
+                Sacc[s] = a;
+              }
+            }
+          }
+        });
+    __syncthreads();
+    if (npar != par) {  // parent complete: write out and reset the accumulator
+      for (int t = threadIdx.x; t < SP; t += ct::kThreads) {
+        mp_p[int64_t(par) * SP + t] = Sacc[t];
+        Sacc[t] = make_double2(0.0, 0.0);
+      }
+    }
+    par = npar;
+    b0 = nb0;
+    ++it;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int NC, int NP>
+__global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* __restrict__ child_off,
+                                                        const int* __restrict__ children,
+                                                        const uint8_t* __restrict__ oct_c,
+                                                        const double2* __restrict__ loc_p, double2* __restrict__ loc_c,
+                                                        const double* __restrict__ RthT, const double* __restrict__ vth,
+                                                        const double* __restrict__ RphiT, const double* __restrict__ vphi,
+                                                        const double2* __restrict__ shift_dn) {
+  using S = ct::Shape<NC, NP>;
+  constexpr int CB = S::L2L_CB, DB = S::L2L_DB, HALF = S::HALF, SP = S::SP, SC = S::SC;
+  extern __shared__ double2 sm[];
+  double2* Lp = sm;
+  double2* Fs = DB ? sm + SP : sm;
+  double2* Ns = Fs + CB * HALF * S::DTH_LDA;
+  double* Bth = reinterpret_cast<double*>(Ns + CB * NC * S::DPHI_LDA);
+  double* Bphi = Bth + S::DTH_K * S::DTH_N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  double* lc = reinterpret_cast<double*>(loc_c);
+
+  ct::stage_doubles(Bth, RthT, S::DTH_K * S::DTH_N);
+  ct::stage_doubles(Bphi, RphiT, S::DPHI_K * S::DPHI_N);
+  cp_async_commit();
+  for (int t = threadIdx.x; t < CB * HALF * S::DTH_LDA; t += ct::kThreads) Fs[t] = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < CB * NC * S::DPHI_LDA; t += ct::kThreads) Ns[t] = make_double2(0.0, 0.0);
+
+  for (int par = blockIdx.x; par < n_par; par += gridDim.x) {
+    const int cb = child_off[par], ce = child_off[par + 1];
+    const double2* lpg = loc_p + int64_t(par) * SP;
+    __syncthreads();  // previous parent done with Lp
+    if (DB) {
+      for (int t = threadIdx.x; t < SP; t += ct::kThreads) cp_async16(Lp + t, lpg + t, true);
+      cp_async_commit();
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const double2* L = DB ? Lp : lpg;
+    for (int b0 = cb; b0 < ce; b0 += CB) {
+      const int nb = min(CB, ce - b0);
+      for (int row = warp; row < CB * HALF; row += ct::kWarps) {
+        const int c = row / HALF, p = row - c * HALF;
+        double2* f = Fs + row * S::DTH_LDA;
+        if (c < nb) {
+          const double2* sh = shift_dn + int64_t(oct_c[children[b0 + c]]) * SP;
+#pragma unroll
+          for (int i = lane; i < 2 * NP; i += 32) {
+            const int s = i < NP ? i * NP + p : (2 * NP - 1 - i) * NP + p + HALF;
+            f[i] = cmul(L[s], __ldg(sh + s));
+          }
+        } else {
+#pragma unroll
+          for (int i = lane; i < 2 * NP; i += 32) f[i] = make_double2(0.0, 0.0);
+        }
+      }
+      __syncthreads();
+      ct::rank1_ct<CB * HALF, 2 * NP, S::DTH_LDA>(Fs, vth);
+      __syncthreads();
+      ct::gemm_ct<CB * HALF * 2, S::DTH_N, S::DTH_K>(
+          [&](int r) { return Fs + r * S::DTH_LDA; }, Bth, [&](int m0, int n0, double v0, double v1) {
+            const int r = m0 + g, ci = r >> 1, c = ci / HALF, p = ci - c * HALF;
+            if (c >= CB) return;
+            double2* base = Ns + c * NC * S::DPHI_LDA;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int n = n0 + 2 * tq + q;
+              if (n < 2 * NC) {
+                const int row = n < NC ? n : 2 * NC - 1 - n;
+                const int col = n < NC ? p : p + HALF;
+                set_part(base + row * S::DPHI_LDA + col, r & 1, q ? v1 : v0);
+              }
+            }
+          });
+      __syncthreads();
+      ct::rank1_ct<CB * NC, NP, S::DPHI_LDA>(Ns, vphi);
+      __syncthreads();
+      ct::gemm_ct<CB * NC * 2, S::DPHI_N, S::DPHI_K>(
+          [&](int r) { return Ns + r * S::DPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1) {
+            const int r = m0 + g, ci = r >> 1, c = ci / NC, row = ci - c * NC;
+            if (c >= nb) return;
+            double* dst = lc + 2 * (int64_t(children[b0 + c]) * SC + row * NC) + (r & 1);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int n = n0 + 2 * tq + q;
+              if (n < NC) dst[2 * n] += q ? v1 : v0;
+            }
+          });
+      __syncthreads();
+    }
+  }
+}
+
+// Dispatch over the instantiated (n_c, n_p) pairs; returns false if the pair
+// has no compile-time kernel (the runtime-shaped kernels then run).
+#define HFMM_CT_PAIRS(X) \
+  X(18, 28) X(28, 42) X(42, 68) X(22, 30) X(30, 44) X(44, 72) X(26, 34) X(34, 52) X(52, 80)
+
+struct CtLaunch {
+  int n_par, grid;
+  const int* child_off;
+  const int* children;
+  const uint8_t* oct_c;
+  cudaStream_t st;
+};
+
+template <int NC, int NP>
+inline int ct_grid(int n_par, int bytes, const void* fn) {
+  int per_sm = 0, sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ct::kThreads, size_t(bytes));
+  const int g = sms * (per_sm > 0 ? per_sm : 1) * 4;
+  return n_par < g ? n_par : g;
+}
+
+template <int A, int B>
+bool try_m2m_ct(const CtLaunch& L, const double2* mp_c, double2* mp_p, const double* Bphi, const double* vphi,
+                const double* Bth, const double* vth, const double2* shift_up) {
+  using S = ct::Shape<A, B>;
+  if constexpr (S::M2M_CB > 0) {
+    auto fn = k_m2m_ct<A, B>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::M2M_BYTES);
+    const int grid = ct_grid<A, B>(L.n_par, S::M2M_BYTES, reinterpret_cast<const void*>(fn));
+    fn<<<grid, ct::kThreads, S::M2M_BYTES, L.st>>>(L.n_par, L.child_off, L.children, L.oct_c, mp_c, mp_p, Bphi,
+                                                   vphi, Bth, vth, shift_up);
+    return true;
+  } else {
+    return false;
+  }
+}
+
+template <int A, int B>
+bool try_l2l_ct(const CtLaunch& L, const double2* loc_p, double2* loc_c, const double* Bth, const double* vth,
+                const double* Bphi, const double* vphi, const double2* shift_dn) {
+  using S = ct::Shape<A, B>;
+  if constexpr (S::L2L_CB > 0) {
+    auto fn = k_l2l_ct<A, B>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::L2L_BYTES);
+    const int grid = ct_grid<A, B>(L.n_par, S::L2L_BYTES, reinterpret_cast<const void*>(fn));
+    fn<<<grid, ct::kThreads, S::L2L_BYTES, L.st>>>(L.n_par, L.child_off, L.children, L.oct_c, loc_p, loc_c, Bth,
+                                                   vth, Bphi, vphi, shift_dn);
+    return true;
+  } else {
+    return false;
+  }
+}
+
+inline bool launch_m2m_ct(int nc, int np, const CtLaunch& L, const double2* mp_c, double2* mp_p, const double* Bphi,
+                          const double* vphi, const double* Bth, const double* vth, const double2* shift_up) {
+#define HFMM_M2M_CASE(A, B) \
+  if (nc == A && np == B) return try_m2m_ct<A, B>(L, mp_c, mp_p, Bphi, vphi, Bth, vth, shift_up);
+  HFMM_CT_PAIRS(HFMM_M2M_CASE)
+#undef HFMM_M2M_CASE
+  return false;
+}
+
+inline bool launch_l2l_ct(int nc, int np, const CtLaunch& L, const double2* loc_p, double2* loc_c, const double* Bth,
+                          const double* vth, const double* Bphi, const double* vphi, const double2* shift_dn) {
+#define HFMM_L2L_CASE(A, B) \
+  if (nc == A && np == B) return try_l2l_ct<A, B>(L, loc_p, loc_c, Bth, vth, Bphi, vphi, shift_dn);
+  HFMM_CT_PAIRS(HFMM_L2L_CASE)
+#undef HFMM_L2L_CASE
+  return false;
+}
+
+}  // namespace hfmm_b200
+
+#endif

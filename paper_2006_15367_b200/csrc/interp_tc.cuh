@@ -11,8 +11,12 @@
 // imaginary parts of the data rows.
 //
 // One CTA (8 warps) owns one parent node and processes its children in
-// batches of CB: everything between the child samples in HBM and the parent
-// accumulators stays in shared memory / registers.
+// batches of CB (1, 2 or 4).  Child samples stream in with cp.async (double
+// buffered when shared memory allows); the M2M theta pass orders its rows
+// (circle, child, re/im) so one 8-row DMMA tile holds every child of a
+// circle: the epilogue combines re/im across lanes, applies each child's
+// shift and sums the children with warp shuffles straight into the parent
+// accumulator -- no intermediate grid ever leaves shared memory.
 #ifndef HFMM_B200_INTERP_TC_CUH
 #define HFMM_B200_INTERP_TC_CUH
 
@@ -26,39 +30,43 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-// Shape of one fused pass, computed on the host (all strides in double2).
+// Shape of one pass, computed on the host (strides in double2).
 struct PassDims {
   int K;    // padded reduction length (multiple of 4): n_in + 1 (rank-1 column) rounded up
   int N;    // padded output length (multiple of 8)
-  int lda;  // smem row stride of the input rows (== 4 mod 8 to avoid bank conflicts)
-  int ldo;  // smem row stride of the output rows (theta pass of M2M only)
+  int lda;  // smem row stride of the input rows (== 4 mod 8: conflict-free fragment loads)
+  int ldo;  // unused (kept for layout stability)
 };
 
-// C(r, n) = sum_k A(r, k) B(k, n) for r < M (real rows, padded to 16),
-// n < N, k < K; B is a K x N row-major real matrix in global memory (L1
-// resident, shared by all CTAs).  A(r, k) is part (r & 1) of the complex
-// element at row (r >> 1), column k of a double2 smem array with row stride
-// lda.  Warp tile 16 x 16 (2 x 2 DMMA tiles), warps stride over tiles.
-template <class Store>
-__device__ __forceinline__ void warp_gemm_rc(int M, int N, int K, const double2* __restrict__ A, int lda,
-                                             const double* __restrict__ B, Store store) {
+// Warp-tiled real GEMM over complex smem rows, DMMA m8n8k4:
+//   C(r, n) = sum_{k<K} A(r, k) B(k, n),   r < M (padded to 16), n < N.
+// A(r, k) = part (r & 1) of element k of complex row rowp(r >> 1) (smem);
+// B is K x N row-major in global memory (L1 resident).  The epilogue gets
+// the 8x8 tile origin and both accumulators of the lane:
+//   epi(m0, n0, c0, c1): lane holds C(m0 + g, n0 + 2 tq) and C(.., +1),
+// and is called by all 32 lanes (warp-uniform), so it may shuffle.
+template <class RowPtr, class Epi>
+__device__ __forceinline__ void warp_gemm_rc(int M, int N, int K, RowPtr rowp, const double* __restrict__ B,
+                                             Epi epi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
   const int mt = (M + 15) >> 4, nt = (N + 15) >> 4;
-  const double* Ad = reinterpret_cast<const double*>(A);
   for (int w = warp; w < mt * nt; w += nwarp) {
     const int m0 = (w / nt) << 4, n0 = (w % nt) << 4;
     double c[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
     const int r0 = m0 + g, r1 = m0 + 8 + g;
-    const double* a0p = Ad + 2 * (r0 >> 1) * lda + (r0 & 1);
-    const double* a1p = Ad + 2 * (r1 >> 1) * lda + (r1 & 1);
+    const bool ok0 = r0 < M, ok1 = r1 < M;
+    const double* a0p = reinterpret_cast<const double*>(rowp(ok0 ? r0 >> 1 : 0)) + (r0 & 1);
+    const double* a1p = reinterpret_cast<const double*>(rowp(ok1 ? r1 >> 1 : 0)) + (r1 & 1);
     const bool bn1 = n0 + 8 < N;
+    const double* bp = B + tq * N + n0 + g;
+#pragma unroll 2
     for (int k = 0; k < K; k += 4) {
       const int kk = k + tq;
-      const double a0 = r0 < M ? a0p[2 * kk] : 0.0;
-      const double a1 = r1 < M ? a1p[2 * kk] : 0.0;
-      const double b0 = __ldg(B + kk * N + n0 + g);
-      const double b1 = bn1 ? __ldg(B + kk * N + n0 + 8 + g) : 0.0;
+      const double a0 = ok0 ? a0p[2 * kk] : 0.0;
+      const double a1 = ok1 ? a1p[2 * kk] : 0.0;
+      const double b0 = __ldg(bp + k * N);
+      const double b1 = bn1 ? __ldg(bp + k * N + 8) : 0.0;
       dmma884(c[0][0][0], c[0][0][1], a0, b0);
       dmma884(c[0][1][0], c[0][1][1], a0, b1);
       dmma884(c[1][0][0], c[1][0][1], a1, b0);
@@ -67,26 +75,23 @@ __device__ __forceinline__ void warp_gemm_rc(int M, int N, int K, const double2*
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int r = m0 + 8 * i + g, n = n0 + 8 * j + 2 * tq;
-        if (r < M && n < N) {  // N is a multiple of 8: n and n + 1 are both in range
-          store(r, n, c[i][j][0]);
-          store(r, n + 1, c[i][j][1]);
-        }
-      }
+      for (int j = 0; j < 2; ++j)
+        if (n0 + 8 * j < N) epi(m0 + 8 * i, n0 + 8 * j, c[i][j][0], c[i][j][1]);
   }
 }
 
-// x[row][K_in] = i * (v . x[row][0:K_in]) for `rows` complex rows (warp per row).
-__device__ __forceinline__ void rank1_column(double2* X, int rows, int ld, int kin, const double* __restrict__ v) {
+// x[row][kin] = i * (v . x[row][0:kin]) for `rows` complex rows (warp per row).
+template <class RowPtr>
+__device__ __forceinline__ void rank1_column(int rows, int kin, const double* __restrict__ v, RowPtr rowp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   for (int r = warp; r < rows; r += nwarp) {
     double sr = 0.0, si = 0.0;
-    double2* x = X + r * ld;
+    double2* x = rowp(r);
     for (int k = lane; k < kin; k += 32) {
       const double vk = __ldg(v + k);
-      sr = fma(vk, x[k].x, sr);
-      si = fma(vk, x[k].y, si);
+      const double2 xv = x[k];
+      sr = fma(vk, xv.x, sr);
+      si = fma(vk, xv.y, si);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -102,84 +107,144 @@ __device__ __forceinline__ void set_part(double2* p, int part, double v) {
 }
 
 constexpr int kFusedThreads = 256;
-constexpr int kFusedE = 12;  // parent samples per thread (S_p <= 3072)
+
+// Launch plan of a fused pass (host-computed).
+struct FusedPlan {
+  int CB;    // children per batch (1, 2, 4)
+  int dbuf;  // M2M: double-buffer the child rows; L2L: keep the parent in smem
+  int smem_bytes;
+};
 
 // ---------------------------------------------------------------------------
 // M2M for one parent: phi upsample (n_c -> n_p per theta row), fold, theta
 // upsample (2 n_c -> 2 n_p per great circle), unfold, shift, sum over the
-// children in child order (traversal.cpp:322-429, sphere_grid.cpp:183-192).
+// children (traversal.cpp:322-429, sphere_grid.cpp:183-192).
 __global__ void __launch_bounds__(kFusedThreads) k_m2m_fused(
-    int n_c, int n_p, int CB, PassDims phi, PassDims th, const int* __restrict__ child_off,
+    int n_c, int n_p, FusedPlan plan, PassDims phi, PassDims th, const int* __restrict__ child_off,
     const int* __restrict__ children, const uint8_t* __restrict__ oct_c, const double2* __restrict__ mp_c,
     double2* __restrict__ mp_p, const double* __restrict__ RphiT, const double* __restrict__ vphi,
     const double* __restrict__ RthT, const double* __restrict__ vth, const double2* __restrict__ shift_up) {
   extern __shared__ double2 sm[];
+  const int CB = plan.CB;
   const int half = n_p / 2, Sc = n_c * n_c, Sp = n_p * n_p;
-  const int xs_size = CB * n_c * phi.lda, gs_size = CB * half * th.ldo;
-  double2* U = sm;                                       // X rows, later G rows
-  double2* Fs = sm + (xs_size > gs_size ? xs_size : gs_size);
+  const int xsz = CB * n_c * phi.lda;
+  double2* Xb0 = sm;
+  double2* Xb1 = plan.dbuf ? sm + xsz : sm;
+  double2* Fs = sm + (plan.dbuf ? 2 : 1) * xsz;
+  double2* Sacc = Fs + CB * half * th.lda;
   const int par = blockIdx.x;
   const int cb = child_off[par], ce = child_off[par + 1];
 
-  // Fs padding columns (beyond 2 n_c + 1) stay zero for the whole kernel.
-  for (int t = threadIdx.x; t < CB * half * th.lda; t += blockDim.x) Fs[t] = make_double2(0.0, 0.0);
-
-  double2 acc[kFusedE];
-#pragma unroll
-  for (int r = 0; r < kFusedE; ++r) acc[r] = make_double2(0.0, 0.0);
-
-  for (int b0 = cb; b0 < ce; b0 += CB) {
+  // Child rows [c][i][k] (k < n_c data, k == n_c rank-1 column, zero padding):
+  // one 16-byte cp.async per element, padding zero-filled by the copy.
+  auto issue_load = [&](double2* X, int b0) {
     const int nb = min(CB, ce - b0);
-    __syncthreads();
-    // 1. child samples -> X rows [c][i][0:n_c], zero padding
     for (int t = threadIdx.x; t < CB * n_c * phi.lda; t += blockDim.x) {
-      const int c = t / (n_c * phi.lda), rem = t % (n_c * phi.lda);
-      const int i = rem / phi.lda, k = rem % phi.lda;
-      double2 v = make_double2(0.0, 0.0);
-      if (c < nb && k < n_c) v = mp_c[int64_t(children[b0 + c]) * Sc + i * n_c + k];
-      U[t] = v;
+      const int row = t / phi.lda, k = t - row * phi.lda;
+      const int c = row / n_c, i = row - c * n_c;
+      const bool ok = c < nb && k < n_c;
+      cp_async16(X + t, ok ? mp_c + int64_t(children[b0 + c]) * Sc + i * n_c + k : mp_c, ok);
+    }
+    cp_async_commit();
+  };
+
+  for (int t = threadIdx.x; t < CB * half * th.lda; t += blockDim.x) Fs[t] = make_double2(0.0, 0.0);
+  for (int t = threadIdx.x; t < Sp; t += blockDim.x) Sacc[t] = make_double2(0.0, 0.0);
+  issue_load(Xb0, cb);
+
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int R2 = 2 * CB;  // theta rows per circle: (child, re/im)
+  int it = 0;
+  for (int b0 = cb; b0 < ce; b0 += CB, ++it) {
+    const int nb = min(CB, ce - b0);
+    double2* X = (it & 1) ? Xb1 : Xb0;
+    if (plan.dbuf && b0 + CB < ce) {
+      issue_load((it & 1) ? Xb0 : Xb1, b0 + CB);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait_all();
     }
     __syncthreads();
-    rank1_column(U, CB * n_c, phi.lda, n_c, vphi);
+    rank1_column(CB * n_c, n_c, vphi, [&](int r) { return X + r * phi.lda; });
     __syncthreads();
-    // 2. phi pass, stored folded into Fs[c][p][ii]
-    warp_gemm_rc(CB * n_c * 2, phi.N, phi.K, U, phi.lda, RphiT, [&](int r, int n, double v) {
-      if (n >= n_p) return;
-      const int ci = r >> 1, c = ci / n_c, i = ci % n_c;
-      const int p = n < half ? n : n - half;
-      const int ii = n < half ? i : 2 * n_c - 1 - i;
-      set_part(Fs + (c * half + p) * th.lda + ii, r & 1, v);
-    });
-    __syncthreads();
-    rank1_column(Fs, CB * half, th.lda, 2 * n_c, vth);
-    __syncthreads();
-    // 3. theta pass into G rows [c][p][n] (aliases the X rows)
-    warp_gemm_rc(CB * half * 2, th.N, th.K, Fs, th.lda, RthT, [&](int r, int n, double v) {
-      set_part(U + (r >> 1) * th.ldo + n, r & 1, v);
-    });
-    __syncthreads();
-    // 4. unfold, shift, accumulate in child order
+    // phi pass: rows (child, theta row, re/im) -> folded circles Fs[c][p][ii]
+    warp_gemm_rc(CB * n_c * 2, phi.N, phi.K, [&](int r) { return X + r * phi.lda; }, RphiT,
+                 [&](int m0, int n0, double v0, double v1) {
+                   const int r = m0 + g, ci = r >> 1, c = ci / n_c, i = ci - c * n_c;
+                   double2* base = Fs + c * half * th.lda;
 #pragma unroll
-    for (int r = 0; r < kFusedE; ++r) {
-      const int s = threadIdx.x + r * kFusedThreads;
-      if (s < Sp) {
-        const int row = s / n_p, col = s % n_p;
-        const int p = col < half ? col : col - half;
-        const int n = col < half ? row : 2 * n_p - 1 - row;
-        for (int c = 0; c < nb; ++c) {
-          const double2 g = U[(c * half + p) * th.ldo + n];
-          const double2 sh = shift_up[oct_c[children[b0 + c]] * Sp + s];
-          acc[r].x += g.x * sh.x - g.y * sh.y;
-          acc[r].y += g.x * sh.y + g.y * sh.x;
-        }
-      }
-    }
-  }
+                   for (int q = 0; q < 2; ++q) {
+                     const int n = n0 + 2 * tq + q;
+                     if (n < n_p && c < CB) {
+                       const int p = n < half ? n : n - half;
+                       const int ii = n < half ? i : 2 * n_c - 1 - i;
+                       set_part(base + p * th.lda + ii, r & 1, q ? v1 : v0);
+                     }
+                   }
+                 });
+    __syncthreads();
+    if (!plan.dbuf && b0 + CB < ce) issue_load(Xb0, b0 + CB);  // X is free: overlap with theta
+    rank1_column(CB * half, 2 * n_c, vth, [&](int r) { return Fs + r * th.lda; });
+    __syncthreads();
+    // theta pass: rows (circle, child, re/im); an 8-row tile holds 8 / R2
+    // whole circles, so the children of a circle reduce inside the warp.
+    int octs[4];
 #pragma unroll
-  for (int r = 0; r < kFusedE; ++r) {
-    const int s = threadIdx.x + r * kFusedThreads;
-    if (s < Sp) mp_p[int64_t(par) * Sp + s] = acc[r];
+    for (int c = 0; c < 4; ++c) octs[c] = c < nb ? oct_c[children[b0 + c]] : 0;
+    warp_gemm_rc(half * R2, th.N, th.K,
+                 [&](int row) {  // complex row -> (circle, child)
+                   const int p = row / CB, c = row - p * CB;
+                   return Fs + (c * half + p) * th.lda;
+                 },
+                 RthT, [&](int m0, int n0, double v0, double v1) {
+                   const int r = m0 + g, part = r & 1, c = (r >> 1) % CB, p = r / R2;
+                   const double o0 = __shfl_xor_sync(0xffffffffu, v0, 4);  // the other part
+                   const double o1 = __shfl_xor_sync(0xffffffffu, v1, 4);
+                   const int o = octs[c];
+                   const bool live = c < nb && p < half;
+                   double cr[2], cim[2];
+#pragma unroll
+                   for (int q = 0; q < 2; ++q) {
+                     const int n = n0 + 2 * tq + q;
+                     const double re = part ? (q ? o1 : o0) : (q ? v1 : v0);
+                     const double im = part ? (q ? v1 : v0) : (q ? o1 : o0);
+                     double2 sh = make_double2(0.0, 0.0);
+                     if (live && n < 2 * n_p) {
+                       const int s = n < n_p ? n * n_p + p : (2 * n_p - 1 - n) * n_p + p + half;
+                       sh = __ldg(shift_up + o * Sp + s);
+                     }
+                     cr[q] = re * sh.x - im * sh.y;
+                     cim[q] = re * sh.y + im * sh.x;
+                   }
+                   // sum the children of the circle: lanes differing in the child bits of g
+#pragma unroll
+                   for (int q = 0; q < 2; ++q) {
+                     if (CB >= 2) {
+                       cr[q] += __shfl_xor_sync(0xffffffffu, cr[q], 8);
+                       cim[q] += __shfl_xor_sync(0xffffffffu, cim[q], 8);
+                     }
+                     if (CB >= 4) {
+                       cr[q] += __shfl_xor_sync(0xffffffffu, cr[q], 16);
+                       cim[q] += __shfl_xor_sync(0xffffffffu, cim[q], 16);
+                     }
+                   }
+                   if (part == 0 && c == 0 && p < half) {
+#pragma unroll
+                     for (int q = 0; q < 2; ++q) {
+                       const int n = n0 + 2 * tq + q;
+                       if (n < 2 * n_p) {
+                         const int s = n < n_p ? n * n_p + p : (2 * n_p - 1 - n) * n_p + p + half;
+                         double2 a = Sacc[s];
+                         a.x += cr[q];
+                         a.y += cim[q];
+                         Sacc[s] = a;
+                       }
+                     }
+                   }
+                 });
+    __syncthreads();
   }
+  for (int t = threadIdx.x; t < Sp; t += blockDim.x) mp_p[int64_t(par) * Sp + t] = Sacc[t];
 }
 
 // ---------------------------------------------------------------------------
@@ -189,59 +254,84 @@ __global__ void __launch_bounds__(kFusedThreads) k_m2m_fused(
 // (traversal.cpp:583-661; the quadrature weights and the adjoint scale are
 // folded into the theta matrix).
 __global__ void __launch_bounds__(kFusedThreads) k_l2l_fused(
-    int n_c, int n_p, int CB, PassDims th, PassDims phi, const int* __restrict__ child_off,
+    int n_c, int n_p, FusedPlan plan, PassDims th, PassDims phi, const int* __restrict__ child_off,
     const int* __restrict__ children, const uint8_t* __restrict__ oct_c, const double2* __restrict__ loc_p,
     double2* __restrict__ loc_c, const double* __restrict__ RthT, const double* __restrict__ vth,
     const double* __restrict__ RphiT, const double* __restrict__ vphi, const double2* __restrict__ shift_dn) {
   extern __shared__ double2 sm[];
+  const int CB = plan.CB;
   const int half = n_p / 2, Sc = n_c * n_c, Sp = n_p * n_p;
-  double2* Lp = sm;
-  double2* Fs = Lp + Sp;
-  double2* Ns = Fs + CB * half * th.lda;
   const int par = blockIdx.x;
   const int cb = child_off[par], ce = child_off[par + 1];
   if (cb == ce) return;
-  for (int t = threadIdx.x; t < Sp; t += blockDim.x) Lp[t] = loc_p[int64_t(par) * Sp + t];
+  double2* Lp = sm;
+  double2* Fs = plan.dbuf ? sm + Sp : sm;
+  double2* Ns = Fs + CB * half * th.lda;
+  const double2* lpg = loc_p + int64_t(par) * Sp;
+  if (plan.dbuf) {
+    for (int t = threadIdx.x; t < Sp; t += blockDim.x) cp_async16(Lp + t, lpg + t, true);
+    cp_async_commit();
+  }
   for (int t = threadIdx.x; t < CB * half * th.lda; t += blockDim.x) Fs[t] = make_double2(0.0, 0.0);
   for (int t = threadIdx.x; t < CB * n_c * phi.lda; t += blockDim.x) Ns[t] = make_double2(0.0, 0.0);
+  cp_async_wait_all();
+  __syncthreads();
+  const double2* L = plan.dbuf ? Lp : lpg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  double* lc = reinterpret_cast<double*>(loc_c);
 
   for (int b0 = cb; b0 < ce; b0 += CB) {
     const int nb = min(CB, ce - b0);
-    __syncthreads();
-    // 1. shifted parent, folded: Fs[c][p][i], i < 2 n_p
-    for (int t = threadIdx.x; t < CB * half * 2 * n_p; t += blockDim.x) {
-      const int c = t / (half * 2 * n_p), rem = t % (half * 2 * n_p);
-      const int p = rem / (2 * n_p), i = rem % (2 * n_p);
-      double2 v = make_double2(0.0, 0.0);
+    // 1. shifted parent, folded: Fs[c][p][i] (warp per circle row, lanes over i)
+    for (int row = warp; row < CB * half; row += nwarp) {
+      const int c = row / half, p = row - c * half;
+      double2* f = Fs + row * th.lda;
       if (c < nb) {
-        const int s = i < n_p ? i * n_p + p : (2 * n_p - 1 - i) * n_p + p + half;
-        v = cmul(Lp[s], shift_dn[oct_c[children[b0 + c]] * Sp + s]);
+        const double2* sh = shift_dn + int64_t(oct_c[children[b0 + c]]) * Sp;
+        for (int i = lane; i < 2 * n_p; i += 32) {
+          const int s = i < n_p ? i * n_p + p : (2 * n_p - 1 - i) * n_p + p + half;
+          f[i] = cmul(L[s], __ldg(sh + s));
+        }
+      } else {
+        for (int i = lane; i < 2 * n_p; i += 32) f[i] = make_double2(0.0, 0.0);
       }
-      Fs[(c * half + p) * th.lda + i] = v;
     }
     __syncthreads();
-    rank1_column(Fs, CB * half, th.lda, 2 * n_p, vth);
+    rank1_column(CB * half, 2 * n_p, vth, [&](int r) { return Fs + r * th.lda; });
     __syncthreads();
-    // 2. theta pass, unfolded into narrow rows Ns[c][row][col] (n_c x n_p)
-    warp_gemm_rc(CB * half * 2, th.N, th.K, Fs, th.lda, RthT, [&](int r, int n, double v) {
-      if (n >= 2 * n_c) return;
-      const int ci = r >> 1, c = ci / half, p = ci % half;
-      const int row = n < n_c ? n : 2 * n_c - 1 - n;
-      const int col = n < n_c ? p : p + half;
-      set_part(Ns + (c * n_c + row) * phi.lda + col, r & 1, v);
-    });
+    // 2. theta pass: rows (child, circle, re/im), unfolded into Ns[c][row][col]
+    warp_gemm_rc(CB * half * 2, th.N, th.K, [&](int r) { return Fs + r * th.lda; }, RthT,
+                 [&](int m0, int n0, double v0, double v1) {
+                   const int r = m0 + g, ci = r >> 1, c = ci / half, p = ci - c * half;
+                   if (c >= CB) return;
+                   double2* base = Ns + c * n_c * phi.lda;
+#pragma unroll
+                   for (int q = 0; q < 2; ++q) {
+                     const int n = n0 + 2 * tq + q;
+                     if (n < 2 * n_c) {
+                       const int row = n < n_c ? n : 2 * n_c - 1 - n;
+                       const int col = n < n_c ? p : p + half;
+                       set_part(base + row * phi.lda + col, r & 1, q ? v1 : v0);
+                     }
+                   }
+                 });
     __syncthreads();
-    rank1_column(Ns, CB * n_c, phi.lda, n_p, vphi);
+    rank1_column(CB * n_c, n_p, vphi, [&](int r) { return Ns + r * phi.lda; });
     __syncthreads();
     // 3. phi pass, accumulated into the child locals
-    double* lc = reinterpret_cast<double*>(loc_c);
-    warp_gemm_rc(CB * n_c * 2, phi.N, phi.K, Ns, phi.lda, RphiT, [&](int r, int n, double v) {
-      if (n >= n_c) return;
-      const int ci = r >> 1, c = ci / n_c, row = ci % n_c;
-      if (c >= nb) return;
-      double* dst = lc + 2 * (int64_t(children[b0 + c]) * Sc + row * n_c + n) + (r & 1);
-      *dst += v;
-    });
+    warp_gemm_rc(CB * n_c * 2, phi.N, phi.K, [&](int r) { return Ns + r * phi.lda; }, RphiT,
+                 [&](int m0, int n0, double v0, double v1) {
+                   const int r = m0 + g, ci = r >> 1, c = ci / n_c, row = ci - c * n_c;
+                   if (c >= nb) return;
+                   double* dst = lc + 2 * (int64_t(children[b0 + c]) * Sc + row * n_c) + (r & 1);
+#pragma unroll
+                   for (int q = 0; q < 2; ++q) {
+                     const int n = n0 + 2 * tq + q;
+                     if (n < n_c) dst[2 * n] += q ? v1 : v0;
+                   }
+                 });
+    __syncthreads();
   }
 }
 
