@@ -153,6 +153,31 @@ hfmm_status hfmm_gpu_get_expansion(hfmm_gpu* g, int kind, int level, double* out
 hfmm_status hfmm_gpu_get_potentials_sorted(hfmm_gpu* g, double* out,
                                            size_t cap_doubles);
 
+/* ---------------- distributed mode (num_ranks > 1, one process per GPU) ----
+ * Rank r holds the nodes whose leaf range meets its Morton leaf range; the
+ * upward pass yields partial multipoles; one static exchange (kind 0) adds
+ * the partials of every far source a held observer needs; ghost particles
+ * of neighbouring ranks (kind 1, the reference near plan comm_plan.cpp:84-109)
+ * feed the near field.  The caller moves the buffers (e.g. NCCL); the
+ * engine packs / unpacks them on its stream.  Sequence per evaluation:
+ *   set_charges | load_charges_device; ghosts: pack(1,q) -> send/recv -> unpack(1,q);
+ *   run_phase(C2M), run_phase(M2M); exchange_begin(0); pack(0,q) -> send/recv ->
+ *   unpack(0,q) for q in rank order; run_phase(M2L..NEAR).
+ * In distributed mode hfmm_gpu_set_charges takes the full input-order array
+ * and keeps this rank's particles only. */
+hfmm_status hfmm_gpu_exchange_sizes(hfmm_gpu* g, int kind, int peer, int64_t* send_doubles,
+                                    int64_t* recv_doubles);
+hfmm_status hfmm_gpu_exchange_begin(hfmm_gpu* g, int kind);
+hfmm_status hfmm_gpu_pack(hfmm_gpu* g, int kind, int peer, double* d_send);
+hfmm_status hfmm_gpu_unpack(hfmm_gpu* g, int kind, int peer, const double* d_recv);
+/* All engine work goes to `stream` (cudaStream_t; NULL = a private stream). */
+hfmm_status hfmm_gpu_set_stream(hfmm_gpu* g, void* stream);
+hfmm_status hfmm_gpu_synchronize(hfmm_gpu* g);
+/* Copies this rank's particles' charges (sorted order, device pointer). */
+hfmm_status hfmm_gpu_load_charges_device(hfmm_gpu* g, const double* d_charges_sorted);
+/* This rank's sorted particle range [*begin, *end). */
+hfmm_status hfmm_gpu_particle_range(hfmm_gpu* g, int64_t* begin, int64_t* end);
+
 /* One-shot: build_setup + evaluate on one device (evaluate_potential,
  * traversal.cpp:819-823).  Requires cfg->num_ranks == 1. */
 hfmm_status hfmm_evaluate_potential(const double* positions, const double* charges,

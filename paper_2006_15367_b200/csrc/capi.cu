@@ -187,6 +187,66 @@ hfmm_status hfmm_gpu_get_potentials_sorted(hfmm_gpu* g, double* out, size_t cap)
   });
 }
 
+hfmm_status hfmm_gpu_exchange_sizes(hfmm_gpu* g, int kind, int peer, int64_t* send_d, int64_t* recv_d) {
+  return guard([&] {
+    need(g, "hfmm_gpu_exchange_sizes(gpu)");
+    need(send_d, "hfmm_gpu_exchange_sizes(send)");
+    need(recv_d, "hfmm_gpu_exchange_sizes(recv)");
+    g->eng->exchange_sizes(kind, peer, send_d, recv_d);
+  });
+}
+
+hfmm_status hfmm_gpu_exchange_begin(hfmm_gpu* g, int kind) {
+  return guard([&] {
+    need(g, "hfmm_gpu_exchange_begin(gpu)");
+    g->eng->exchange_begin(kind);
+  });
+}
+
+hfmm_status hfmm_gpu_pack(hfmm_gpu* g, int kind, int peer, double* d_send) {
+  return guard([&] {
+    need(g, "hfmm_gpu_pack(gpu)");
+    g->eng->pack(kind, peer, d_send);
+  });
+}
+
+hfmm_status hfmm_gpu_unpack(hfmm_gpu* g, int kind, int peer, const double* d_recv) {
+  return guard([&] {
+    need(g, "hfmm_gpu_unpack(gpu)");
+    g->eng->unpack(kind, peer, d_recv);
+  });
+}
+
+hfmm_status hfmm_gpu_set_stream(hfmm_gpu* g, void* stream) {
+  return guard([&] {
+    need(g, "hfmm_gpu_set_stream(gpu)");
+    g->eng->set_stream(static_cast<cudaStream_t>(stream));
+  });
+}
+
+hfmm_status hfmm_gpu_synchronize(hfmm_gpu* g) {
+  return guard([&] {
+    need(g, "hfmm_gpu_synchronize(gpu)");
+    g->eng->synchronize();
+  });
+}
+
+hfmm_status hfmm_gpu_load_charges_device(hfmm_gpu* g, const double* d_q) {
+  return guard([&] {
+    need(g, "hfmm_gpu_load_charges_device(gpu)");
+    need(d_q, "hfmm_gpu_load_charges_device(charges)");
+    g->eng->load_charges_device(d_q);
+  });
+}
+
+hfmm_status hfmm_gpu_particle_range(hfmm_gpu* g, int64_t* b, int64_t* e) {
+  return guard([&] {
+    need(g, "hfmm_gpu_particle_range(gpu)");
+    *b = g->eng->particle_begin();
+    *e = g->eng->particle_end();
+  });
+}
+
 hfmm_status hfmm_evaluate_potential(const double* positions, const double* charges, size_t n,
                                     const hfmm_run_config* cfg, int device, double* pot_out) {
   return guard([&] {

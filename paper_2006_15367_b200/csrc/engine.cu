@@ -57,14 +57,13 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
     throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
   if (device < 0 || device >= ndev) throw std::invalid_argument("hfmm_gpu_create: bad device");
   if (rank < 0 || rank >= s.P) throw std::invalid_argument("hfmm_gpu_create: bad rank");
-  if (s.P != 1)
-    throw std::invalid_argument(
-        "hfmm_gpu_create: multi-rank device evaluation is driven by the distributed runner");
+  dist_ = s.P > 1;
   ck(cudaSetDevice(device), "cudaSetDevice");
   use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;  // debugging aid: runtime-shaped kernels only
   ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
   upload();
+  if (dist_) upload_rank_plan();
   ck(cudaStreamSynchronize(st_), "upload sync");
 }
 
@@ -74,7 +73,7 @@ Engine::~Engine() {
   for (void* p : allocs_) cudaFree(p);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
-  if (st_) cudaStreamDestroy(st_);
+  if (st_ && owns_stream_) cudaStreamDestroy(st_);
 }
 
 namespace {
@@ -216,6 +215,8 @@ void Engine::upload() {
     d.centers = upload_vec(t.centers);
     d.mp = alloc<double2>(size_t(d.n_nodes) * size_t(d.S));
     d.loc = alloc<double2>(size_t(d.n_nodes) * size_t(d.S));
+    ck(cudaMemsetAsync(d.mp, 0, size_t(d.n_nodes) * size_t(d.S) * sizeof(double2), st_), "memset mp");
+    ck(cudaMemsetAsync(d.loc, 0, size_t(d.n_nodes) * size_t(d.S) * sizeof(double2), st_), "memset loc");
     // Far lists as (source, offset slot) and the used slots.
     std::vector<int64_t> foff(t.far_off.begin(), t.far_off.end());
     std::vector<int2> far(t.far.size());
@@ -350,7 +351,12 @@ void Engine::set_charges(const double* q_in) {
   ck(cudaSetDevice(dev_), "cudaSetDevice");
   const int64_t n = int64_t(s_.n);
   ck(cudaMemcpyAsync(d_q_in, q_in, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, st_), "H2D q");
-  k_gather_q<<<unsigned((n + 255) / 256), 256, 0, st_>>>(n, d_orig, d_q_in, d_q);
+  if (dist_) {
+    const int64_t cnt = part_e_ - part_b_;
+    if (cnt > 0) k_gather_q_range<<<unsigned((cnt + 255) / 256), 256, 0, st_>>>(part_b_, part_e_, d_orig, d_q_in, d_q);
+  } else {
+    k_gather_q<<<unsigned((n + 255) / 256), 256, 0, st_>>>(n, d_orig, d_q_in, d_q);
+  }
   ++launches_;
   ck(cudaGetLastError(), "k_gather_q");
 }
@@ -384,11 +390,17 @@ int theta_chunk(int half, int outs_per_circle, int threads) {
 }  // namespace
 
 void Engine::phase_m2m() {
+  // Distributed mode: halo rows still hold last evaluation's full multipoles;
+  // the upward pass must see zeros there (they are summed again after it).
+  if (dist_) exchange_begin(0);
   for (int l = s_.L - 1; l >= s_.top; --l) {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
-    const CtLaunch cl{P.n_nodes, 0, P.child_off, P.children, oct_[size_t(l + 1)], st_};
+    const RankLevel* R = dist_ ? &rl_[size_t(l)] : nullptr;
+    const CtLaunch cl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
+                      R ? R->children : P.children, oct_[size_t(l + 1)], st_};
+    if (cl.n_par == 0) continue;
     if (use_ct_ && launch_m2m_ct(nc, np, cl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v,
                                  P.shift_up)) {
       ++launches_;
@@ -398,8 +410,8 @@ void Engine::phase_m2m() {
     if (P.m2m_fused) {
       const FusedPlan fp{P.m2m_plan[0], P.m2m_plan[1], P.m2m_plan[2]};
       ck(cudaFuncSetAttribute(k_m2m_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
-      k_m2m_fused<<<unsigned(P.n_nodes), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
-          nc, np, fp, to_dims(P.up_phi), to_dims(P.up_th), P.child_off, P.children, oct_[size_t(l + 1)],
+      k_m2m_fused<<<unsigned(cl.n_par), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
+          nc, np, fp, cl.plist, to_dims(P.up_phi), to_dims(P.up_th), cl.child_off, cl.children, oct_[size_t(l + 1)],
           C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up);
       ++launches_;
       ck(cudaGetLastError(), "k_m2m_fused");
@@ -446,7 +458,10 @@ void Engine::phase_l2l() {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
-    const CtLaunch cl{P.n_nodes, 0, P.child_off, P.children, oct_[size_t(l + 1)], st_};
+    const RankLevel* R = dist_ ? &rl_[size_t(l)] : nullptr;
+    const CtLaunch cl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
+                      R ? R->children : P.children, oct_[size_t(l + 1)], st_};
+    if (cl.n_par == 0) continue;
     if (use_ct_ && launch_l2l_ct(nc, np, cl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v,
                                  P.shift_dn)) {
       ++launches_;
@@ -456,8 +471,8 @@ void Engine::phase_l2l() {
     if (P.l2l_fused) {
       const FusedPlan fp{P.l2l_plan[0], P.l2l_plan[1], P.l2l_plan[2]};
       ck(cudaFuncSetAttribute(k_l2l_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
-      k_l2l_fused<<<unsigned(P.n_nodes), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
-          nc, np, fp, to_dims(P.dn_th), to_dims(P.dn_phi), P.child_off, P.children, oct_[size_t(l + 1)],
+      k_l2l_fused<<<unsigned(cl.n_par), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
+          nc, np, fp, cl.plist, to_dims(P.dn_th), to_dims(P.dn_phi), cl.child_off, cl.children, oct_[size_t(l + 1)],
           P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn);
       ++launches_;
       ck(cudaGetLastError(), "k_l2l_fused");
@@ -526,7 +541,7 @@ void Engine::run_phase(int phase) {
     default:
       throw std::invalid_argument("hfmm_gpu_run_phase: unknown phase");
   }
-  ck(cudaStreamSynchronize(st_), "phase sync");
+  ck(cudaGetLastError(), "run_phase");
 }
 
 void Engine::evaluate(double* ms) {
@@ -551,6 +566,8 @@ void Engine::last_timing(double* ms, int64_t* launches) {
 
 void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cudaStream_t st) {
   ck(cudaSetDevice(dev_), "cudaSetDevice");
+  if (dist_)
+    throw std::logic_error("evaluate_device: num_ranks > 1 runs phase by phase with exchanges");
   cudaStream_t saved = st_;
   if (st) st_ = st;
   const int64_t l0 = launches_;
@@ -581,6 +598,10 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
 
 void Engine::evaluate_host(const double* q_in, double* pot_out, double* ms) {
   ck(cudaSetDevice(dev_), "cudaSetDevice");
+  if (dist_)
+    throw std::logic_error(
+        "evaluate: num_ranks > 1 needs the exchanges of the distributed driver "
+        "(paper_2006_15367_b200.distributed)");
   if (q_in) set_charges(q_in);
   evaluate_device(nullptr, nullptr, nullptr);
   const int64_t cnt = part_e_ - part_b_;
@@ -603,14 +624,170 @@ void Engine::get_expansion(int kind, int level, double* out, size_t cap) {
   const DevLevel& d = lv_[size_t(level)];
   const size_t cnt = size_t(d.n_nodes) * size_t(d.S) * 2;
   if (cap < cnt) throw std::invalid_argument("get_expansion: buffer too small");
+  ck(cudaStreamSynchronize(st_), "sync");
   ck(cudaMemcpy(out, kind == 0 ? d.mp : d.loc, cnt * sizeof(double), cudaMemcpyDeviceToHost), "D2H exp");
 }
 
 void Engine::get_potentials_sorted(double* out, size_t cap) {
   if (cap < 2 * s_.n) throw std::invalid_argument("get_potentials_sorted: buffer too small");
+  ck(cudaStreamSynchronize(st_), "sync");
   ck(cudaMemcpy(out, d_pot, s_.n * sizeof(double2), cudaMemcpyDeviceToHost), "D2H pot");
 }
 
+
+void Engine::upload_rank_plan() {
+  const Setup& s = s_;
+  const int L = s.L, P = s.P;
+  RankPlan rp = build_rank_plan(s, rank_);
+  rl_.assign(size_t(L + 1), RankLevel{});
+  for (int l = s.top; l < L; ++l) {
+    RankLevel& R = rl_[size_t(l)];
+    R.n_par = int(rp.held[size_t(l)].size());
+    R.plist = upload_vec(rp.held[size_t(l)]);
+    R.child_off = upload_vec(rp.child_off[size_t(l)]);
+    R.children = upload_vec(rp.children[size_t(l)]);
+  }
+  halo_nodes_.assign(size_t(L + 1), nullptr);
+  halo_cnt_.assign(size_t(L + 1), 0);
+  for (int l = s.top; l <= L; ++l) {
+    halo_cnt_[size_t(l)] = int(rp.halo[size_t(l)].size());
+    halo_nodes_[size_t(l)] = upload_vec(rp.halo[size_t(l)]);
+  }
+  peers_.assign(size_t(P), PeerPlan{});
+  for (int q = 0; q < P; ++q) {
+    if (q == rank_) continue;
+    PeerPlan& pp = peers_[size_t(q)];
+    pp.mp_send_nodes.assign(size_t(L + 1), nullptr);
+    pp.mp_recv_nodes.assign(size_t(L + 1), nullptr);
+    pp.mp_send_cnt.assign(size_t(L + 1), 0);
+    pp.mp_recv_cnt.assign(size_t(L + 1), 0);
+    for (int dir = 0; dir < 2; ++dir) {
+      const auto& items = dir == 0 ? rp.mp_send[size_t(q)] : rp.mp_recv[size_t(q)];
+      std::vector<std::vector<int>> per(size_t(L + 1));
+      for (auto [l, n] : items) per[size_t(l)].push_back(n);
+      int64_t total = 0;
+      for (int l = s.top; l <= L; ++l) {
+        (dir == 0 ? pp.mp_send_cnt : pp.mp_recv_cnt)[size_t(l)] = int(per[size_t(l)].size());
+        (dir == 0 ? pp.mp_send_nodes : pp.mp_recv_nodes)[size_t(l)] = upload_vec(per[size_t(l)]);
+        total += int64_t(per[size_t(l)].size()) * lv_[size_t(l)].S * 2;
+      }
+      (dir == 0 ? pp.mp_send : pp.mp_recv) = total;
+    }
+    // ghosts: leaves r owns that q needs, and leaves q owns that r needs (comm_plan.cpp:84-109)
+    for (int dir = 0; dir < 2; ++dir) {
+      const auto& leaves = dir == 0 ? s.near_send[size_t(rank_) * P + size_t(q)] : s.near_send[size_t(q) * P + size_t(rank_)];
+      std::vector<int64_t> idx;
+      for (uint64_t li : leaves)
+        for (uint64_t p = s.leaf_start[li]; p < s.leaf_start[li + 1]; ++p) idx.push_back(int64_t(p));
+      (dir == 0 ? pp.n_gh_send : pp.n_gh_recv) = int64_t(idx.size());
+      (dir == 0 ? pp.gh_send_idx : pp.gh_recv_idx) = upload_vec(idx);
+    }
+  }
+}
+
+void Engine::exchange_sizes(int kind, int peer, int64_t* send_d, int64_t* recv_d) const {
+  if (!dist_) throw std::logic_error("exchange: single-rank engine");
+  if (peer < 0 || peer >= s_.P) throw std::out_of_range("exchange: bad peer");
+  const PeerPlan& pp = peers_[size_t(peer)];
+  if (kind == 0) {
+    *send_d = pp.mp_send;
+    *recv_d = pp.mp_recv;
+  } else if (kind == 1) {
+    *send_d = 5 * pp.n_gh_send;
+    *recv_d = 5 * pp.n_gh_recv;
+  } else {
+    throw std::invalid_argument("exchange: bad kind");
+  }
+}
+
+void Engine::exchange_begin(int kind) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  if (!dist_) throw std::logic_error("exchange: single-rank engine");
+  if (kind != 0) return;
+  for (int l = s_.top; l <= s_.L; ++l) {  // halo sources start from zero before the partial sums
+    if (halo_cnt_[size_t(l)] == 0) continue;
+    const DevLevel& d = lv_[size_t(l)];
+    dim3 grid(unsigned(halo_cnt_[size_t(l)]), unsigned(std::min<int64_t>((d.S + 255) / 256, 64)));
+    k_zero_rows<<<grid, 256, 0, st_>>>(d.mp, halo_nodes_[size_t(l)], d.S);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "exchange_begin");
+}
+
+void Engine::pack(int kind, int peer, double* d_buf) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  int64_t sd = 0, rd = 0;
+  exchange_sizes(kind, peer, &sd, &rd);
+  const PeerPlan& pp = peers_[size_t(peer)];
+  if (kind == 0) {
+    int64_t off = 0;
+    for (int l = s_.top; l <= s_.L; ++l) {
+      const int cnt = pp.mp_send_cnt[size_t(l)];
+      if (cnt == 0) continue;
+      const DevLevel& d = lv_[size_t(l)];
+      dim3 grid(unsigned(cnt), unsigned(std::min<int64_t>((d.S + 255) / 256, 64)));
+      k_pack_rows<<<grid, 256, 0, st_>>>(d.mp, pp.mp_send_nodes[size_t(l)], d.S,
+                                         reinterpret_cast<double2*>(d_buf + off));
+      ++launches_;
+      off += int64_t(cnt) * d.S * 2;
+    }
+  } else if (pp.n_gh_send > 0) {
+    k_pack_particles<<<unsigned((pp.n_gh_send + 255) / 256), 256, 0, st_>>>(pp.n_gh_send, pp.gh_send_idx, d_x, d_y,
+                                                                           d_z, d_q, d_buf);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "pack");
+}
+
+void Engine::unpack(int kind, int peer, const double* d_buf) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  int64_t sd = 0, rd = 0;
+  exchange_sizes(kind, peer, &sd, &rd);
+  const PeerPlan& pp = peers_[size_t(peer)];
+  if (kind == 0) {
+    int64_t off = 0;
+    for (int l = s_.top; l <= s_.L; ++l) {
+      const int cnt = pp.mp_recv_cnt[size_t(l)];
+      if (cnt == 0) continue;
+      const DevLevel& d = lv_[size_t(l)];
+      dim3 grid(unsigned(cnt), unsigned(std::min<int64_t>((d.S + 255) / 256, 64)));
+      k_add_rows<<<grid, 256, 0, st_>>>(d.mp, pp.mp_recv_nodes[size_t(l)], d.S,
+                                        reinterpret_cast<const double2*>(d_buf + off));
+      ++launches_;
+      off += int64_t(cnt) * d.S * 2;
+    }
+  } else if (pp.n_gh_recv > 0) {
+    k_unpack_particles<<<unsigned((pp.n_gh_recv + 255) / 256), 256, 0, st_>>>(pp.n_gh_recv, pp.gh_recv_idx, d_buf,
+                                                                             d_x, d_y, d_z, d_q);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "unpack");
+}
+
+void Engine::set_stream(cudaStream_t st) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  ck(cudaStreamSynchronize(st_), "sync");
+  if (owns_stream_) cudaStreamDestroy(st_);
+  owns_stream_ = st == nullptr;
+  if (st == nullptr)
+    ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+  else
+    st_ = st;
+}
+
+void Engine::synchronize() {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  ck(cudaStreamSynchronize(st_), "sync");
+}
+
+void Engine::load_charges_device(const double* d_q_sorted) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  const int64_t b = dist_ ? part_b_ : 0, e = dist_ ? part_e_ : int64_t(s_.n);
+  if (e > b)
+    ck(cudaMemcpyAsync(d_q + b, reinterpret_cast<const double2*>(d_q_sorted) + b, size_t(e - b) * sizeof(double2),
+                       cudaMemcpyDeviceToDevice, st_),
+       "charges");
+}
 
 void direct_sum(const double* positions, const double* charges, size_t n, const int64_t* obs,
                 size_t m, double k, int device, double* pot_out) {

@@ -59,6 +59,26 @@ struct DevLevel {
   double* dn_phi_v = nullptr;
 };
 
+// Per-rank lists for one level acting as parent (distributed mode).
+struct RankLevel {
+  int n_par = 0;
+  int* plist = nullptr;      // held parents (global node indices)
+  int* child_off = nullptr;  // CSR over plist
+  int* children = nullptr;   // held children (global indices at level + 1)
+};
+
+// Static exchange plan with one peer (distributed mode).
+struct PeerPlan {
+  // multipole partials: per level, the node rows sent / received
+  std::vector<int*> mp_send_nodes, mp_recv_nodes;  // [level]
+  std::vector<int> mp_send_cnt, mp_recv_cnt;       // [level]
+  int64_t mp_send = 0, mp_recv = 0;                // doubles
+  // ghost particles (x, y, z, re, im) by sorted particle index
+  int64_t* gh_send_idx = nullptr;
+  int64_t* gh_recv_idx = nullptr;
+  int64_t n_gh_send = 0, n_gh_recv = 0;
+};
+
 class Engine {
  public:
   Engine(const Setup& s, int device, int rank);
@@ -77,6 +97,17 @@ class Engine {
   void evaluate_host(const double* q_in, double* pot_out, double* ms);
 
   void get_expansion(int kind, int level, double* out, size_t cap_doubles);
+  // Distributed mode (P > 1): exchange buffers are driven by the caller
+  // (torch.distributed over NCCL); kind 0 = multipole partials, 1 = ghosts.
+  void exchange_sizes(int kind, int peer, int64_t* send_doubles, int64_t* recv_doubles) const;
+  void exchange_begin(int kind);
+  void pack(int kind, int peer, double* d_buf);
+  void unpack(int kind, int peer, const double* d_buf);
+  void set_stream(cudaStream_t st);
+  void synchronize();
+  void load_charges_device(const double* d_q_sorted);
+  int64_t particle_begin() const { return part_b_; }
+  int64_t particle_end() const { return part_e_; }
   void get_potentials_sorted(double* out, size_t cap_doubles);
   int64_t launches() const { return launches_; }
   // Per-phase ms of the last evaluation (events on its stream), [0] T build .. [7] total.
@@ -100,6 +131,7 @@ class Engine {
   const Setup& s_;
   int dev_ = 0, rank_ = 0;
   cudaStream_t st_ = nullptr;
+  bool owns_stream_ = true;
   std::vector<DevLevel> lv_;
   std::vector<uint8_t*> oct_;  // per level: child octant (code & 7) of each node
   std::vector<void*> allocs_;
@@ -122,6 +154,13 @@ class Engine {
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range
   int64_t part_b_ = 0, part_e_ = 0;  // owned particle range
   cudaEvent_t ev_[8] = {};
+  // distributed mode
+  bool dist_ = false;
+  std::vector<RankLevel> rl_;               // [level as parent]
+  std::vector<PeerPlan> peers_;             // [peer]
+  std::vector<int*> halo_nodes_;            // [level]
+  std::vector<int> halo_cnt_;               // [level]
+  void upload_rank_plan();
   int64_t last_launches_ = 0;
   bool timed_ = false;
 };

@@ -136,7 +136,8 @@ __device__ __forceinline__ void stage_doubles(double* dst, const double* __restr
 
 // ---------------------------------------------------------------------------
 template <int NC, int NP>
-__global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* __restrict__ child_off,
+__global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* __restrict__ plist,
+                                                        const int* __restrict__ child_off,
                                                         const int* __restrict__ children,
                                                         const uint8_t* __restrict__ oct_c,
                                                         const double2* __restrict__ mp_c, double2* __restrict__ mp_p,
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* _
     __syncthreads();
     if (npar != par) {  // parent complete: write out and reset the accumulator
       for (int t = threadIdx.x; t < SP; t += ct::kThreads) {
-        mp_p[int64_t(par) * SP + t] = Sacc[t];
+        mp_p[int64_t(plist ? plist[par] : par) * SP + t] = Sacc[t];
         Sacc[t] = make_double2(0.0, 0.0);
       }
     }
@@ -284,7 +285,8 @@ __global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* _
 
 // ---------------------------------------------------------------------------
 template <int NC, int NP>
-__global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* __restrict__ child_off,
+__global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* __restrict__ plist,
+                                                        const int* __restrict__ child_off,
                                                         const int* __restrict__ children,
                                                         const uint8_t* __restrict__ oct_c,
                                                         const double2* __restrict__ loc_p, double2* __restrict__ loc_c,
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* _
 
   for (int par = blockIdx.x; par < n_par; par += gridDim.x) {
     const int cb = child_off[par], ce = child_off[par + 1];
-    const double2* lpg = loc_p + int64_t(par) * SP;
+    const double2* lpg = loc_p + int64_t(plist ? plist[par] : par) * SP;
     __syncthreads();  // previous parent done with Lp
     if (DB) {
       for (int t = threadIdx.x; t < SP; t += ct::kThreads) cp_async16(Lp + t, lpg + t, true);
@@ -380,7 +382,8 @@ __global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* _
   X(18, 28) X(28, 42) X(42, 68) X(22, 30) X(30, 44) X(44, 72) X(26, 34) X(34, 52) X(52, 80)
 
 struct CtLaunch {
-  int n_par, grid;
+  int n_par;
+  const int* plist;  // parent indices (nullptr: identity)
   const int* child_off;
   const int* children;
   const uint8_t* oct_c;
@@ -405,7 +408,7 @@ bool try_m2m_ct(const CtLaunch& L, const double2* mp_c, double2* mp_p, const dou
     auto fn = k_m2m_ct<A, B>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::M2M_BYTES);
     const int grid = ct_grid<A, B>(L.n_par, S::M2M_BYTES, reinterpret_cast<const void*>(fn));
-    fn<<<grid, ct::kThreads, S::M2M_BYTES, L.st>>>(L.n_par, L.child_off, L.children, L.oct_c, mp_c, mp_p, Bphi,
+    fn<<<grid, ct::kThreads, S::M2M_BYTES, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c, mp_c, mp_p, Bphi,
                                                    vphi, Bth, vth, shift_up);
     return true;
   } else {
@@ -421,7 +424,7 @@ bool try_l2l_ct(const CtLaunch& L, const double2* loc_p, double2* loc_c, const d
     auto fn = k_l2l_ct<A, B>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::L2L_BYTES);
     const int grid = ct_grid<A, B>(L.n_par, S::L2L_BYTES, reinterpret_cast<const void*>(fn));
-    fn<<<grid, ct::kThreads, S::L2L_BYTES, L.st>>>(L.n_par, L.child_off, L.children, L.oct_c, loc_p, loc_c, Bth,
+    fn<<<grid, ct::kThreads, S::L2L_BYTES, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c, loc_p, loc_c, Bth,
                                                    vth, Bphi, vphi, shift_dn);
     return true;
   } else {

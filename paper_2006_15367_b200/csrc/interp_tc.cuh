@@ -120,7 +120,7 @@ struct FusedPlan {
 // upsample (2 n_c -> 2 n_p per great circle), unfold, shift, sum over the
 // children (traversal.cpp:322-429, sphere_grid.cpp:183-192).
 __global__ void __launch_bounds__(kFusedThreads) k_m2m_fused(
-    int n_c, int n_p, FusedPlan plan, PassDims phi, PassDims th, const int* __restrict__ child_off,
+    int n_c, int n_p, FusedPlan plan, const int* __restrict__ plist, PassDims phi, PassDims th, const int* __restrict__ child_off,
     const int* __restrict__ children, const uint8_t* __restrict__ oct_c, const double2* __restrict__ mp_c,
     double2* __restrict__ mp_p, const double* __restrict__ RphiT, const double* __restrict__ vphi,
     const double* __restrict__ RthT, const double* __restrict__ vth, const double2* __restrict__ shift_up) {
@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(kFusedThreads) k_m2m_fused(
                  });
     __syncthreads();
   }
-  for (int t = threadIdx.x; t < Sp; t += blockDim.x) mp_p[int64_t(par) * Sp + t] = Sacc[t];
+  const int64_t gpar = plist ? plist[par] : par;
+  for (int t = threadIdx.x; t < Sp; t += blockDim.x) mp_p[gpar * Sp + t] = Sacc[t];
 }
 
 // ---------------------------------------------------------------------------
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_m2m_fused(
 // (traversal.cpp:583-661; the quadrature weights and the adjoint scale are
 // folded into the theta matrix).
 __global__ void __launch_bounds__(kFusedThreads) k_l2l_fused(
-    int n_c, int n_p, FusedPlan plan, PassDims th, PassDims phi, const int* __restrict__ child_off,
+    int n_c, int n_p, FusedPlan plan, const int* __restrict__ plist, PassDims th, PassDims phi, const int* __restrict__ child_off,
     const int* __restrict__ children, const uint8_t* __restrict__ oct_c, const double2* __restrict__ loc_p,
     double2* __restrict__ loc_c, const double* __restrict__ RthT, const double* __restrict__ vth,
     const double* __restrict__ RphiT, const double* __restrict__ vphi, const double2* __restrict__ shift_dn) {
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_l2l_fused(
   double2* Lp = sm;
   double2* Fs = plan.dbuf ? sm + Sp : sm;
   double2* Ns = Fs + CB * half * th.lda;
-  const double2* lpg = loc_p + int64_t(par) * Sp;
+  const double2* lpg = loc_p + int64_t(plist ? plist[par] : par) * Sp;
   if (plan.dbuf) {
     for (int t = threadIdx.x; t < Sp; t += blockDim.x) cp_async16(Lp + t, lpg + t, true);
     cp_async_commit();

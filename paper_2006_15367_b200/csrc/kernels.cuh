@@ -421,6 +421,61 @@ __global__ void k_scatter_pot(int64_t b, int64_t e, const int64_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// Exchange packing (distributed mode): whole expansion rows and ghost particles.
+__global__ void k_pack_rows(const double2* __restrict__ src, const int* __restrict__ nodes, int64_t S,
+                            double2* __restrict__ dst) {
+  const int64_t i = blockIdx.x;
+  const int64_t node = nodes[i];
+  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.y) * blockDim.x)
+    dst[i * S + s] = src[node * S + s];
+}
+__global__ void k_add_rows(double2* __restrict__ dst, const int* __restrict__ nodes, int64_t S,
+                           const double2* __restrict__ src) {
+  const int64_t i = blockIdx.x;
+  const int64_t node = nodes[i];
+  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.y) * blockDim.x) {
+    double2 a = dst[node * S + s];
+    const double2 b = src[i * S + s];
+    a.x += b.x;
+    a.y += b.y;
+    dst[node * S + s] = a;
+  }
+}
+__global__ void k_zero_rows(double2* __restrict__ dst, const int* __restrict__ nodes, int64_t S) {
+  const int64_t node = nodes[blockIdx.x];
+  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.y) * blockDim.x)
+    dst[node * S + s] = make_double2(0.0, 0.0);
+}
+__global__ void k_pack_particles(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ x,
+                                 const double* __restrict__ y, const double* __restrict__ z,
+                                 const double2* __restrict__ q, double* __restrict__ buf) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = idx[i];
+  buf[5 * i] = x[p];
+  buf[5 * i + 1] = y[p];
+  buf[5 * i + 2] = z[p];
+  buf[5 * i + 3] = q[p].x;
+  buf[5 * i + 4] = q[p].y;
+}
+__global__ void k_unpack_particles(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ buf,
+                                   double* __restrict__ x, double* __restrict__ y, double* __restrict__ z,
+                                   double2* __restrict__ q) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t p = idx[i];
+  x[p] = buf[5 * i];
+  y[p] = buf[5 * i + 1];
+  z[p] = buf[5 * i + 2];
+  q[p] = make_double2(buf[5 * i + 3], buf[5 * i + 4]);
+}
+__global__ void k_gather_q_range(int64_t b, int64_t e, const int64_t* __restrict__ orig,
+                                 const double2* __restrict__ q_in, double2* __restrict__ q_sorted) {
+  const int64_t i = b + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < e) q_sorted[i] = q_in[orig[i]];
+}
+
+// ---------------------------------------------------------------------------
 // Direct O(N M) sum (kernel.cpp:16-41): one CTA per observer; the first exact
 // coincidence is the self term; a second one flags an error.
 __global__ void k_direct(int64_t n, const double* __restrict__ x, const double* __restrict__ y,

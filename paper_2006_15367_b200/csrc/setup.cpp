@@ -539,6 +539,65 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
   return s;
 }
 
+RankPlan build_rank_plan(const Setup& s, int r) {
+  if (r < 0 || r >= s.P) throw std::out_of_range("build_rank_plan: bad rank");
+  const int L = s.L, P = s.P;
+  RankPlan rp;
+  rp.rank = r;
+  rp.held.assign(size_t(L + 1), {});
+  rp.child_off.assign(size_t(L + 1), {});
+  rp.children.assign(size_t(L + 1), {});
+  rp.halo.assign(size_t(L + 1), {});
+  std::vector<std::vector<uint8_t>> is_held(size_t(L + 1));
+  for (int l = s.top; l <= L; ++l) {
+    const LevelData& t = s.levels[size_t(l)];
+    is_held[size_t(l)].assign(t.num_nodes(), 0);
+    for (size_t i = 0; i < t.num_nodes(); ++i)
+      if (t.first_user[i] <= r && r <= t.last_user[i]) {
+        rp.held[size_t(l)].push_back(int(i));
+        is_held[size_t(l)][i] = 1;
+      }
+  }
+  for (int l = s.top; l < L; ++l) {
+    const LevelData& t = s.levels[size_t(l)];
+    auto& co = rp.child_off[size_t(l)];
+    auto& ch = rp.children[size_t(l)];
+    co.assign(1, 0);
+    for (int p : rp.held[size_t(l)]) {
+      for (uint64_t z = t.child_off[size_t(p)]; z < t.child_off[size_t(p) + 1]; ++z)
+        if (is_held[size_t(l + 1)][t.children[z]]) ch.push_back(int(t.children[z]));
+      co.push_back(int(ch.size()));
+    }
+  }
+  rp.child_off[size_t(L)].assign(rp.held[size_t(L)].size() + 1, 0);
+  // need[q][n]: far source n is needed by an observer rank q holds (one pass
+  // over the far lists, each observer visited once per user)
+  rp.mp_send.assign(size_t(P), {});
+  rp.mp_recv.assign(size_t(P), {});
+  for (int l = s.top; l <= L; ++l) {
+    const LevelData& t = s.levels[size_t(l)];
+    const size_t nn = t.num_nodes();
+    std::vector<std::vector<uint8_t>> need(static_cast<size_t>(P));
+    for (size_t o = 0; o < nn; ++o)
+      for (int q = t.first_user[o]; q <= t.last_user[o]; ++q) {
+        if (need[size_t(q)].empty()) need[size_t(q)].assign(nn, 0);
+        for (uint64_t f = t.far_off[o]; f < t.far_off[o + 1]; ++f) need[size_t(q)][t.far[f]] = 1;
+      }
+    for (size_t n = 0; n < nn; ++n) {
+      const bool mine = is_held[size_t(l)][n] != 0;
+      if (!need[size_t(r)].empty() && need[size_t(r)][n]) {
+        if (!mine) rp.halo[size_t(l)].push_back(int(n));
+        for (int q = t.first_user[n]; q <= t.last_user[n]; ++q)
+          if (q != r) rp.mp_recv[size_t(q)].push_back({l, int(n)});
+      }
+      if (mine)
+        for (int q = 0; q < P; ++q)
+          if (q != r && !need[size_t(q)].empty() && need[size_t(q)][n]) rp.mp_send[size_t(q)].push_back({l, int(n)});
+    }
+  }
+  return rp;
+}
+
 namespace {
 template <class T>
 std::vector<unsigned char> bytes_of(const std::vector<T>& v) {
@@ -607,6 +666,41 @@ std::vector<unsigned char> setup_array(const Setup& s, const std::string& name) 
       for (uint64_t li : lst) v.push_back(int64_t(li));
     }
     return bytes_of(v);
+  }
+  if (name.size() > 2 && name[0] == 'R') {
+    // R<r>.<field>[.L<l> | .<peer>]: per-rank plans (build_rank_plan)
+    const size_t d1 = name.find('.');
+    if (d1 != std::string::npos) {
+      const int r = std::atoi(name.substr(1, d1 - 1).c_str());
+      std::string rest = name.substr(d1 + 1);
+      const size_t d2 = rest.find('.');
+      const std::string field = rest.substr(0, d2);
+      const std::string arg = d2 == std::string::npos ? "" : rest.substr(d2 + 1);
+      RankPlan rp = build_rank_plan(s, r);
+      auto level_of = [&](const std::string& a) {
+        if (a.size() < 2 || a[0] != 'L') throw std::invalid_argument("hfmm_setup_get: bad level in " + name);
+        const int l = std::atoi(a.substr(1).c_str());
+        if (l < s.top || l > L) throw std::out_of_range("hfmm_setup_get: level not computed");
+        return size_t(l);
+      };
+      auto pairs = [&](const std::vector<std::pair<int, int>>& v) {
+        std::vector<int32_t> o;
+        for (auto& [l, n] : v) {
+          o.push_back(l);
+          o.push_back(n);
+        }
+        return bytes_of(o);
+      };
+      if (field == "held") return bytes_of(rp.held[level_of(arg)]);
+      if (field == "child_off") return bytes_of(rp.child_off[level_of(arg)]);
+      if (field == "children") return bytes_of(rp.children[level_of(arg)]);
+      if (field == "halo") return bytes_of(rp.halo[level_of(arg)]);
+      if (field == "mp_send" || field == "mp_recv") {
+        const int q = std::atoi(arg.c_str());
+        if (q < 0 || q >= s.P) throw std::out_of_range("hfmm_setup_get: bad peer");
+        return pairs(field == "mp_send" ? rp.mp_send[size_t(q)] : rp.mp_recv[size_t(q)]);
+      }
+    }
   }
   if (name.size() > 2 && name[0] == 'L') {
     size_t dot = name.find('.');

@@ -95,6 +95,26 @@ struct Setup {
   }
 };
 
+// Per-rank evaluation plan for one process per GPU.
+// Rank r "holds" every node whose leaf range meets its Morton leaf range
+// (first_user <= r <= last_user).  The upward pass runs on held nodes only
+// and yields PARTIAL multipoles (M2M is linear, so partials of a plural node
+// sum to the full one).  One static exchange then delivers, for every far
+// source a held observer needs, the partials of the source's other users;
+// the downward pass and L2T/P2P are rank-local except for ghost particles
+// (the reference's near plan, comm_plan.cpp:84-109).
+struct RankPlan {
+  int rank = 0;
+  std::vector<std::vector<int>> held;       // [level] held node indices, sorted
+  std::vector<std::vector<int>> child_off;  // [level] CSR over held[level] (held children only)
+  std::vector<std::vector<int>> children;   // [level] indices at level + 1
+  std::vector<std::vector<int>> halo;       // [level] needed far sources not held
+  // multipole exchange, per peer q: (level, node) items in (level, node) order
+  std::vector<std::vector<std::pair<int, int>>> mp_send;  // what r sends q
+  std::vector<std::vector<std::pair<int, int>>> mp_recv;  // what r receives from q
+};
+RankPlan build_rank_plan(const struct Setup& s, int r);
+
 // Replicates build_setup; throws the same std exception types.
 Setup build_setup(const double* xyz, const double* q, size_t n,
                   const hfmm_run_config& cfg);

@@ -218,6 +218,41 @@ class RankEngine:
                                              ctypes.c_void_p(d_pot_sorted_ptr),
                                              ctypes.c_void_p(stream_ptr)))
 
+    # distributed mode (paper_2006_15367_b200.distributed)
+    def run_phase(self, phase: int) -> None:
+        check(lib().hfmm_gpu_run_phase(self._h, int(phase)))
+
+    def exchange_sizes(self, kind: int, peer: int) -> tuple[int, int]:
+        s = ctypes.c_int64()
+        r = ctypes.c_int64()
+        check(lib().hfmm_gpu_exchange_sizes(self._h, kind, peer, ctypes.byref(s), ctypes.byref(r)))
+        return s.value, r.value
+
+    def exchange_begin(self, kind: int) -> None:
+        check(lib().hfmm_gpu_exchange_begin(self._h, kind))
+
+    def pack(self, kind: int, peer: int, buf) -> None:
+        """Packs this rank's outgoing data for `peer` into a device tensor (float64)."""
+        check(lib().hfmm_gpu_pack(self._h, kind, peer, ctypes.c_void_p(buf.data_ptr())))
+
+    def unpack(self, kind: int, peer: int, buf) -> None:
+        check(lib().hfmm_gpu_unpack(self._h, kind, peer, ctypes.c_void_p(buf.data_ptr())))
+
+    def set_stream(self, stream_ptr: int) -> None:
+        check(lib().hfmm_gpu_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
+
+    def synchronize(self) -> None:
+        check(lib().hfmm_gpu_synchronize(self._h))
+
+    def load_charges_device(self, d_q_sorted_ptr: int) -> None:
+        check(lib().hfmm_gpu_load_charges_device(self._h, ctypes.c_void_p(d_q_sorted_ptr)))
+
+    def particle_range(self) -> tuple[int, int]:
+        b = ctypes.c_int64()
+        e = ctypes.c_int64()
+        check(lib().hfmm_gpu_particle_range(self._h, ctypes.byref(b), ctypes.byref(e)))
+        return b.value, e.value
+
     def last_timing(self) -> tuple[dict, int]:
         """Per-phase device ms and kernel launches of the last evaluation."""
         t = _native.TimingC()
