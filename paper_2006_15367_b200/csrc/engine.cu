@@ -13,6 +13,7 @@
 #include "m2l.cuh"
 #include "interp_tc.cuh"
 #include "interp_ct.cuh"
+#include "interp_big.cuh"
 
 namespace hfmm_b200 {
 
@@ -60,6 +61,9 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   dist_ = s.P > 1;
   ck(cudaSetDevice(device), "cudaSetDevice");
   use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;  // debugging aid: runtime-shaped kernels only
+  // debugging aid: large-level path 0 = two-stage (default), 1 = fused runtime, 2 = legacy two-pass
+  if (const char* p = std::getenv("HFMM_BIG_PATH")) path_ = std::atoi(p);
+  l2l_ct_ = std::getenv("HFMM_L2L_CT") != nullptr;
   ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
   upload();
@@ -138,6 +142,20 @@ void Engine::setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, co
         P.m2m_fused = true;
         break;
       }
+  }
+  // Two-stage large-grid plans.
+  {
+    const int ldf = P.up_th[2];
+    const size_t per_circle = (size_t(kBigCB) * ldf + size_t(2 * np)) * sizeof(double2);
+    P.big_m2m_cp = int(std::max<size_t>(1, std::min<size_t>(size_t(half), (110 * 1024) / per_circle)));
+    P.big_smem[0] = size_t(nc) * P.up_phi[2] * sizeof(double2);
+    P.big_smem[1] = size_t(P.big_m2m_cp) * per_circle;
+    const size_t per_c2 = size_t(P.dn_th[2]) * sizeof(double2);
+    P.big_l2l_cp = int(std::max<size_t>(1, std::min<size_t>(size_t(half), (72 * 1024) / per_c2)));
+    P.big_smem[2] = size_t(P.big_l2l_cp) * per_c2;
+    P.big_smem[3] = size_t(nc) * P.dn_phi[2] * sizeof(double2);
+    P.big_ldn = P.dn_phi[2];
+    tmp_need_ = std::max(tmp_need_, std::max(size_t(C.n_nodes) * half * ldf, size_t(C.n_nodes) * nc * P.big_ldn));
   }
   for (size_t budget : {size_t(113 * 1024), size_t(227 * 1024)}) {
     if (P.l2l_fused || !allow) break;
@@ -260,11 +278,13 @@ void Engine::upload() {
     d.G = 1 << (l - 1);
     const double cells = double(d.G) * d.G * d.G;
     if (d.n_far > 0 && d.G <= 512 && double(d.n_nodes) >= 0.25 * cells) {
-      std::vector<int> lk(size_t(cells), -1);
+      // row-major cell -> node table padded by a 3-cell halo of -1 (m2l.cuh)
+      const size_t GP = size_t(std::max(d.G, m2l::MB)) + 6;
+      std::vector<int> lk(GP * GP * GP, -1);
       for (size_t i = 0; i < t.num_nodes(); ++i) {
         const uint64_t c = t.codes[i];
-        const size_t gx = cell_axis(c, l, 0), gy = cell_axis(c, l, 1), gz = cell_axis(c, l, 2);
-        lk[(gz * size_t(d.G) + gy) * size_t(d.G) + gx] = int(i);
+        const size_t gx = cell_axis(c, l, 0) + 3, gy = cell_axis(c, l, 1) + 3, gz = cell_axis(c, l, 2) + 3;
+        lk[(gz * GP + gy) * GP + gx] = int(i);
       }
       d.lookup = upload_vec(lk);
       d.dense = true;
@@ -343,8 +363,8 @@ void Engine::upload() {
     setup_fused(P, C, tp, tc);
     tmp = std::max(tmp, size_t(C.n_nodes) * size_t(nc) * size_t(np));
   }
-  tmp_elems_ = tmp;
-  d_tmp = alloc<double2>(tmp);
+  tmp_elems_ = std::max(tmp, tmp_need_);
+  d_tmp = alloc<double2>(tmp_elems_);
 }
 
 void Engine::set_charges(const double* q_in) {
@@ -407,7 +427,25 @@ void Engine::phase_m2m() {
       ck(cudaGetLastError(), "k_m2m_ct");
       continue;
     }
-    if (P.m2m_fused) {
+    if (path_ == 0) {  // two-stage large-grid kernels
+      const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
+      const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
+      ck(cudaFuncSetAttribute(k_m2m_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[0])), "attr");
+      ck(cudaFuncSetAttribute(k_m2m_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[1])), "attr");
+      if (ncl > 0) {
+        k_m2m_big_phi<<<unsigned(ncl), 256, P.big_smem[0], st_>>>(nc, np, to_dims(P.up_phi), P.up_th[2], clist, C.mp,
+                                                                 P.up_phi_B, P.up_phi_v, d_tmp);
+        ++launches_;
+      }
+      dim3 grid(unsigned(cl.n_par), unsigned((np / 2 + P.big_m2m_cp - 1) / P.big_m2m_cp));
+      k_m2m_big_theta<<<grid, 256, P.big_smem[1], st_>>>(nc, np, P.big_m2m_cp, to_dims(P.up_th), cl.plist, cl.child_off,
+                                                         cl.children, oct_[size_t(l + 1)], d_tmp, P.up_th_B,
+                                                         P.up_th_v, P.shift_up, P.mp);
+      ++launches_;
+      ck(cudaGetLastError(), "m2m big");
+      continue;
+    }
+    if (P.m2m_fused && path_ == 1) {
       const FusedPlan fp{P.m2m_plan[0], P.m2m_plan[1], P.m2m_plan[2]};
       ck(cudaFuncSetAttribute(k_m2m_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
       k_m2m_fused<<<unsigned(cl.n_par), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
@@ -462,13 +500,32 @@ void Engine::phase_l2l() {
     const CtLaunch cl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
                       R ? R->children : P.children, oct_[size_t(l + 1)], st_};
     if (cl.n_par == 0) continue;
-    if (use_ct_ && launch_l2l_ct(nc, np, cl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v,
+    // L2L: the two-stage kernels measured faster than the fused ones at every
+    // cfg-2 level (profiles/), so the compile-time fused L2L is opt-in.
+    if (use_ct_ && l2l_ct_ && launch_l2l_ct(nc, np, cl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v,
                                  P.shift_dn)) {
       ++launches_;
       ck(cudaGetLastError(), "k_l2l_ct");
       continue;
     }
-    if (P.l2l_fused) {
+    if (path_ == 0) {  // two-stage large-grid kernels
+      const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
+      const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
+      if (ncl == 0) continue;
+      ck(cudaFuncSetAttribute(k_l2l_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[2])), "attr");
+      ck(cudaFuncSetAttribute(k_l2l_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[3])), "attr");
+      dim3 grid(unsigned(ncl), unsigned((np / 2 + P.big_l2l_cp - 1) / P.big_l2l_cp));
+      k_l2l_big_theta<<<grid, 256, P.big_smem[2], st_>>>(nc, np, P.big_l2l_cp, to_dims(P.dn_th), P.big_ldn, clist,
+                                                         C.parent, oct_[size_t(l + 1)], P.loc, P.shift_dn, P.dn_th_B,
+                                                         P.dn_th_v, d_tmp);
+      ++launches_;
+      k_l2l_big_phi<<<unsigned(ncl), 256, P.big_smem[3], st_>>>(nc, np, to_dims(P.dn_phi), P.big_ldn, clist, d_tmp,
+                                                               P.dn_phi_B, P.dn_phi_v, C.loc);
+      ++launches_;
+      ck(cudaGetLastError(), "l2l big");
+      continue;
+    }
+    if (P.l2l_fused && path_ == 1) {
       const FusedPlan fp{P.l2l_plan[0], P.l2l_plan[1], P.l2l_plan[2]};
       ck(cudaFuncSetAttribute(k_l2l_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
       k_l2l_fused<<<unsigned(cl.n_par), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
@@ -646,6 +703,12 @@ void Engine::upload_rank_plan() {
     R.plist = upload_vec(rp.held[size_t(l)]);
     R.child_off = upload_vec(rp.child_off[size_t(l)]);
     R.children = upload_vec(rp.children[size_t(l)]);
+  }
+  held_.assign(size_t(L + 1), nullptr);
+  held_cnt_.assign(size_t(L + 1), 0);
+  for (int l = s.top; l <= L; ++l) {
+    held_cnt_[size_t(l)] = int(rp.held[size_t(l)].size());
+    held_[size_t(l)] = upload_vec(rp.held[size_t(l)]);
   }
   halo_nodes_.assign(size_t(L + 1), nullptr);
   halo_cnt_.assign(size_t(L + 1), 0);

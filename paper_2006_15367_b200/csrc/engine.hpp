@@ -46,6 +46,10 @@ struct DevLevel {
   double2* shift_dn = nullptr;  // 8*S: exp(+i k khat.(c_parent - c_child))
   // Fused tensor-core M2M / L2L (interp_tc.cuh): real matrices + rank-1 vectors.
   bool m2m_fused = false, l2l_fused = false;
+  // Two-stage large-grid kernels (interp_big.cuh): circles per CTA and smem bytes.
+  int big_m2m_cp = 1, big_l2l_cp = 1;
+  size_t big_smem[4] = {0, 0, 0, 0};  // m2m phi, m2m theta, l2l theta, l2l phi
+  int big_ldn = 0;                    // narrow-row stride of the L2L temp
   int m2m_plan[3] = {1, 0, 0}, l2l_plan[3] = {1, 0, 0};  // FusedPlan {CB, dbuf, smem bytes}
   int up_phi[4] = {0, 0, 0, 0}, up_th[4] = {0, 0, 0, 0};  // PassDims {K, N, lda, ldo}
   int dn_th[4] = {0, 0, 0, 0}, dn_phi[4] = {0, 0, 0, 0};
@@ -137,6 +141,9 @@ class Engine {
   std::vector<void*> allocs_;
   int64_t launches_ = 0;
   bool use_ct_ = true;
+  bool l2l_ct_ = false;
+  int path_ = 0;           // large-level M2M/L2L path (see constructor)
+  size_t tmp_need_ = 0;    // temp elements required by the large-level kernels
   // particles (sorted)
   double* d_x = nullptr;
   double* d_y = nullptr;
@@ -157,6 +164,8 @@ class Engine {
   // distributed mode
   bool dist_ = false;
   std::vector<RankLevel> rl_;               // [level as parent]
+  std::vector<int*> held_;                  // [level] held nodes (distributed mode)
+  std::vector<int> held_cnt_;
   std::vector<PeerPlan> peers_;             // [peer]
   std::vector<int*> halo_nodes_;            // [level]
   std::vector<int> halo_cnt_;               // [level]

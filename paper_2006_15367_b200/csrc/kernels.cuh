@@ -22,6 +22,41 @@ __device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b) {
 
 constexpr int kSlots = 343;  // (ox, oy, oz) in [-3, 3]^3
 
+// sin and cos of a moderate argument (|x| < 2^20): Cody-Waite reduction by
+// pi/2 with the round-to-nearest quadrant taken from a 1.5*2^52 magic add,
+// then Taylor polynomials on [-pi/4, pi/4] (truncation < 6e-17).  No slow
+// path: the arguments on this path are phases k |r| of a few radians.
+__device__ __forceinline__ void sincos_fast(double x, double* sp, double* cp) {
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(x, 0.63661977236758138, kMagic);
+  const int quad = __double2loint(t);
+  const double n = t - kMagic;
+  double y = fma(n, -1.5707963267948966, x);
+  y = fma(n, -6.123233995736766e-17, y);
+  const double y2 = y * y;
+  double ps = -7.6471637318198164759e-13;            // -1/15!
+  ps = fma(ps, y2, 1.6059043836821614599e-10);        //  1/13!
+  ps = fma(ps, y2, -2.5052108385441718775e-08);       // -1/11!
+  ps = fma(ps, y2, 2.7557319223985890653e-06);        //  1/9!
+  ps = fma(ps, y2, -1.9841269841269841270e-04);       // -1/7!
+  ps = fma(ps, y2, 8.3333333333333333333e-03);        //  1/5!
+  ps = fma(ps, y2, -1.6666666666666666667e-01);       // -1/3!
+  const double sn = fma(ps * y2, y, y);
+  double pc = 4.7794773323873852974e-14;              //  1/16!
+  pc = fma(pc, y2, -1.1470745597729724714e-11);       // -1/14!
+  pc = fma(pc, y2, 2.0876756987868098979e-09);        //  1/12!
+  pc = fma(pc, y2, -2.7557319223985890653e-07);       // -1/10!
+  pc = fma(pc, y2, 2.4801587301587301587e-05);        //  1/8!
+  pc = fma(pc, y2, -1.3888888888888888889e-03);       // -1/6!
+  pc = fma(pc, y2, 4.1666666666666666667e-02);        //  1/4!
+  pc = fma(pc, y2, -0.5);
+  const double cs = fma(pc, y2, 1.0);
+  const double s1 = (quad & 1) ? cs : sn;
+  const double c1 = (quad & 1) ? sn : cs;
+  *sp = (quad & 2) ? -s1 : s1;
+  *cp = ((quad + 1) & 2) ? -c1 : c1;
+}
+
 // cp.async (Ampere+ LDGSTS) 16-byte copy; src-size 0 zero-fills the destination.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -108,7 +143,7 @@ __global__ void __launch_bounds__(128) k_c2m(int64_t leaf_b, const int64_t* __re
 #pragma unroll
         for (int r = 0; r < kC2MR; ++r) {
           double sn, cs;
-          sincos(k * (kx[r] * dx + ky[r] * dy + kz[r] * dz), &sn, &cs);
+          sincos_fast(k * (kx[r] * dx + ky[r] * dy + kz[r] * dz), &sn, &cs);
           acc[r].x += qq.x * cs - qq.y * sn;
           acc[r].y += qq.x * sn + qq.y * cs;
         }
@@ -306,7 +341,7 @@ __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __re
     double ar = 0.0, ai = 0.0;
     for (int64_t s = lane; s < S; s += 32) {
       double sn, cs;
-      sincos(-k * (sd[3 * s] * dx + sd[3 * s + 1] * dy + sd[3 * s + 2] * dz), &sn, &cs);
+      sincos_fast(-k * (sd[3 * s] * dx + sd[3 * s + 1] * dy + sd[3 * s + 2] * dz), &sn, &cs);
       const double2 v = sL[s];
       ar += v.x * cs - v.y * sn;
       ai += v.x * sn + v.y * cs;
@@ -385,7 +420,7 @@ __global__ void __launch_bounds__(128) k_p2p(int64_t leaf_b, const int64_t* __re
           if (dx == 0.0 && dy == 0.0 && dz == 0.0) continue;  // self pair
           const double r = sqrt(dx * dx + dy * dy + dz * dz);
           double sn, cs;
-          sincos(-k * r, &sn, &cs);
+          sincos_fast(-k * r, &sn, &cs);
           const double w = inv4pi / r;
           const double gr = cs * w, gi = sn * w;
           const double2 qq = sq[t];

@@ -66,30 +66,32 @@ __global__ void __launch_bounds__(128, 2) k_m2l_dense(int G, int nb, int64_t S,
 
   // Stage T taps and the source region with cp.async (LDGSTS): every load is
   // in flight at once; empty / out-of-grid cells are zero-filled by the copy.
+  // The lookup is halo-padded by 3 cells (entries -1), so a region row is 14
+  // consecutive entries: one warp per row, lane = 2 * cx + sample.
   for (int t = threadIdx.x; t < kSlots * 2; t += blockDim.x)
     cp_async16(Ts + t, T + int64_t(t >> 1) * S + s0 + (t & 1), true);
-  constexpr int NCOPY = MR * MR * MR * 2;
-  constexpr int BATCH = 8;
-  for (int base = threadIdx.x; base < NCOPY; base += BATCH * 128) {
-    int node[BATCH];
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int GP = (G > MB ? G : MB) + 6;  // padded edge (host: same formula)
+    const int cx = lane >> 1, sw = lane & 1;
+    // 196 rows over 4 warps: 7 batches of 7 rows, lookups of a batch in flight together
+    constexpr int RB = 7;
+    for (int r0 = warp * RB; r0 < MR * MR; r0 += nwarp * RB) {
+      int node[RB];
 #pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int t = base + u * 128;
-      const int c = t >> 1;
-      const int cx = c % MR, cy = (c / MR) % MR, cz = c / (MR * MR);
-      const int gx = bx - 3 + cx, gy = by - 3 + cy, gz = bz - 3 + cz;
-      node[u] = -1;
-      if (t < NCOPY && gx >= 0 && gy >= 0 && gz >= 0 && gx < G && gy < G && gz < G)
-        node[u] = __ldg(lookup + (int64_t(gz) * G + gy) * G + gx);
-    }
+      for (int u = 0; u < RB; ++u) {
+        const int row = r0 + u, cz = row / MR, cy = row - cz * MR;
+        node[u] = (lane < 2 * MR && row < MR * MR)
+                      ? __ldg(lookup + (int64_t(bz + cz) * GP + (by + cy)) * GP + (bx + cx))
+                      : -1;
+      }
 #pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int t = base + u * 128;
-      if (t < NCOPY) {
-        const int sw = t & 1, c = t >> 1;
-        const int cx = c % MR, cy = (c / MR) % MR, cz = c / (MR * MR);
-        const bool ok = node[u] >= 0;
-        cp_async16(Ms + cz * ZS + cy * ROW + cx * 2 + sw, mp + (ok ? int64_t(node[u]) * S + s0 + sw : 0), ok);
+      for (int u = 0; u < RB; ++u) {
+        const int row = r0 + u, cz = row / MR, cy = row - cz * MR;
+        if (lane < 2 * MR && row < MR * MR) {
+          const bool ok = node[u] >= 0;
+          cp_async16(Ms + cz * ZS + cy * ROW + lane, mp + (ok ? int64_t(node[u]) * S + s0 + sw : 0), ok);
+        }
       }
     }
   }
@@ -129,7 +131,8 @@ __global__ void __launch_bounds__(128, 2) k_m2l_dense(int G, int nb, int64_t S,
     for (int k = 0; k < MB; ++k) {
       const int gx = bx + k;
       if (gx < G) {
-        const int node = lookup[(int64_t(gz) * G + gy) * G + gx];
+        const int GP = (G > MB ? G : MB) + 6;
+        const int node = lookup[(int64_t(gz + 3) * GP + (gy + 3)) * GP + (gx + 3)];
         if (node >= 0) loc[int64_t(node) * S + s0 + sw] = acc[k];
       }
     }
