@@ -148,12 +148,15 @@ void Engine::setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, co
     const int ldf = P.up_th[2];
     const size_t per_circle = (size_t(kBigCB) * ldf + size_t(2 * np)) * sizeof(double2);
     P.big_m2m_cp = int(std::max<size_t>(1, std::min<size_t>(size_t(half), (110 * 1024) / per_circle)));
-    P.big_smem[0] = size_t(nc) * P.up_phi[2] * sizeof(double2);
+    const size_t row_budget = 96 * 1024;
+    P.big_rc[0] = int(std::max<size_t>(1, std::min<size_t>(size_t(nc), row_budget / (size_t(P.up_phi[2]) * sizeof(double2)))));
+    P.big_smem[0] = size_t(P.big_rc[0]) * P.up_phi[2] * sizeof(double2);
     P.big_smem[1] = size_t(P.big_m2m_cp) * per_circle;
     const size_t per_c2 = size_t(P.dn_th[2]) * sizeof(double2);
     P.big_l2l_cp = int(std::max<size_t>(1, std::min<size_t>(size_t(half), (72 * 1024) / per_c2)));
     P.big_smem[2] = size_t(P.big_l2l_cp) * per_c2;
-    P.big_smem[3] = size_t(nc) * P.dn_phi[2] * sizeof(double2);
+    P.big_rc[1] = int(std::max<size_t>(1, std::min<size_t>(size_t(nc), row_budget / (size_t(P.dn_phi[2]) * sizeof(double2)))));
+    P.big_smem[3] = size_t(P.big_rc[1]) * P.dn_phi[2] * sizeof(double2);
     P.big_ldn = P.dn_phi[2];
     tmp_need_ = std::max(tmp_need_, std::max(size_t(C.n_nodes) * half * ldf, size_t(C.n_nodes) * nc * P.big_ldn));
   }
@@ -201,6 +204,16 @@ void Engine::upload() {
   d_near_off = upload_vec(no);
   std::vector<int> nr(s.near.begin(), s.near.end());
   d_near = upload_vec(nr);
+  // P2P launch lists: own leaves by population (k_p2p<false> / <true>)
+  {
+    std::vector<int> small, dense;
+    for (int64_t li = leaf_b_; li < leaf_e_; ++li)
+      (s.leaf_start[size_t(li) + 1] - s.leaf_start[size_t(li)] <= 32 ? small : dense).push_back(int(li));
+    n_small_ = int(small.size());
+    n_dense_ = int(dense.size());
+    d_small_leaves_ = upload_vec(small);
+    d_dense_leaves_ = upload_vec(dense);
+  }
 
   lv_.assign(size_t(L + 1), DevLevel{});
   std::vector<std::vector<double>> hdir(size_t(L + 1));
@@ -433,7 +446,8 @@ void Engine::phase_m2m() {
       ck(cudaFuncSetAttribute(k_m2m_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[0])), "attr");
       ck(cudaFuncSetAttribute(k_m2m_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[1])), "attr");
       if (ncl > 0) {
-        k_m2m_big_phi<<<unsigned(ncl), 256, P.big_smem[0], st_>>>(nc, np, to_dims(P.up_phi), P.up_th[2], clist, C.mp,
+        dim3 g0(unsigned(ncl), unsigned((nc + P.big_rc[0] - 1) / P.big_rc[0]));
+        k_m2m_big_phi<<<g0, 256, P.big_smem[0], st_>>>(nc, np, to_dims(P.up_phi), P.up_th[2], P.big_rc[0], clist, C.mp,
                                                                  P.up_phi_B, P.up_phi_v, d_tmp);
         ++launches_;
       }
@@ -519,7 +533,8 @@ void Engine::phase_l2l() {
                                                          C.parent, oct_[size_t(l + 1)], P.loc, P.shift_dn, P.dn_th_B,
                                                          P.dn_th_v, d_tmp);
       ++launches_;
-      k_l2l_big_phi<<<unsigned(ncl), 256, P.big_smem[3], st_>>>(nc, np, to_dims(P.dn_phi), P.big_ldn, clist, d_tmp,
+      dim3 g3(unsigned(ncl), unsigned((nc + P.big_rc[1] - 1) / P.big_rc[1]));
+      k_l2l_big_phi<<<g3, 256, P.big_smem[3], st_>>>(nc, np, to_dims(P.dn_phi), P.big_ldn, P.big_rc[1], clist, d_tmp,
                                                                P.dn_phi_B, P.dn_phi_v, C.loc);
       ++launches_;
       ck(cudaGetLastError(), "l2l big");
@@ -566,10 +581,17 @@ void Engine::phase_l2t() {
 }
 
 void Engine::phase_near() {
-  const int64_t nl = leaf_e_ - leaf_b_;
-  k_p2p<<<unsigned(nl), 128, 0, st_>>>(leaf_b_, d_leaf_start, d_near_off, d_near, d_x, d_y, d_z, d_q, s_.k,
-                                       d_pot);
-  ++launches_;
+  const DevLevel& d = lv_[size_t(s_.L)];
+  if (n_small_ > 0) {
+    k_p2p<false><<<unsigned(n_small_), 128, 0, st_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
+                                                      d_x, d_y, d_z, d_q, s_.k, d_pot);
+    ++launches_;
+  }
+  if (n_dense_ > 0) {
+    k_p2p<true><<<unsigned(n_dense_), 128, 0, st_>>>(d_dense_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
+                                                     d_x, d_y, d_z, d_q, s_.k, d_pot);
+    ++launches_;
+  }
   ck(cudaGetLastError(), "k_p2p");
 }
 

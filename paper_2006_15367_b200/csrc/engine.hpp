@@ -50,6 +50,7 @@ struct DevLevel {
   int big_m2m_cp = 1, big_l2l_cp = 1;
   size_t big_smem[4] = {0, 0, 0, 0};  // m2m phi, m2m theta, l2l theta, l2l phi
   int big_ldn = 0;                    // narrow-row stride of the L2L temp
+  int big_rc[2] = {1, 1};             // rows per CTA: m2m phi, l2l phi
   int m2m_plan[3] = {1, 0, 0}, l2l_plan[3] = {1, 0, 0};  // FusedPlan {CB, dbuf, smem bytes}
   int up_phi[4] = {0, 0, 0, 0}, up_th[4] = {0, 0, 0, 0};  // PassDims {K, N, lda, ldo}
   int dn_th[4] = {0, 0, 0, 0}, dn_phi[4] = {0, 0, 0, 0};
@@ -156,6 +157,9 @@ class Engine {
   int64_t* d_leaf_start = nullptr;
   int64_t* d_near_off = nullptr;
   int* d_near = nullptr;
+  int* d_small_leaves_ = nullptr;  // own leaves with <= 32 particles
+  int* d_dense_leaves_ = nullptr;
+  int n_small_ = 0, n_dense_ = 0;
   double2* d_tmp = nullptr;  // interpolation temporaries
   size_t tmp_elems_ = 0;
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range

@@ -20,7 +20,7 @@ namespace hfmm_b200 {
 // ---------------------------------------------------------------------------
 // M2M phi pass: X (n_c x n_c) of one child -> F rows [p][ii] (half rows of
 // stride ldf, columns 0 .. 2 n_c - 1; the rank-1 column is added later).
-__global__ void __launch_bounds__(256) k_m2m_big_phi(int n_c, int n_p, PassDims phi, int ldf,
+__global__ void __launch_bounds__(256) k_m2m_big_phi(int n_c, int n_p, PassDims phi, int ldf, int RC,
                                                      const int* __restrict__ clist,
                                                      const double2* __restrict__ mp_c,
                                                      const double* __restrict__ RphiT,
@@ -28,20 +28,21 @@ __global__ void __launch_bounds__(256) k_m2m_big_phi(int n_c, int n_p, PassDims 
   extern __shared__ double2 X[];
   const int half = n_p / 2, Sc = n_c * n_c;
   const int64_t child = clist ? clist[blockIdx.x] : blockIdx.x;
-  for (int t = threadIdx.x; t < n_c * phi.lda; t += blockDim.x) {
+  const int i0 = blockIdx.y * RC, nr = min(RC, n_c - i0);  // rows (theta) of this CTA
+  for (int t = threadIdx.x; t < nr * phi.lda; t += blockDim.x) {
     const int i = t / phi.lda, k = t - i * phi.lda;
-    cp_async16(X + t, k < n_c ? mp_c + child * Sc + i * n_c + k : mp_c, k < n_c);
+    cp_async16(X + t, k < n_c ? mp_c + child * Sc + (i0 + i) * n_c + k : mp_c, k < n_c);
   }
   cp_async_wait_all();
   __syncthreads();
-  rank1_column(n_c, n_c, vphi, [&](int r) { return X + r * phi.lda; });
+  rank1_column(nr, n_c, vphi, [&](int r) { return X + r * phi.lda; });
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   double2* Fc = F + child * half * ldf;
-  warp_gemm_rc(n_c * 2, phi.N, phi.K, [&](int r) { return X + r * phi.lda; }, RphiT,
+  warp_gemm_rc(nr * 2, phi.N, phi.K, [&](int r) { return X + r * phi.lda; }, RphiT,
                [&](int m0, int n0, double v0, double v1) {
-                 const int r = m0 + g, i = r >> 1;
-                 if (i >= n_c) return;
+                 const int r = m0 + g, i = i0 + (r >> 1);
+                 if ((r >> 1) >= nr) return;
 #pragma unroll
                  for (int q = 0; q < 2; ++q) {
                    const int n = n0 + 2 * tq + q;
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(256) k_l2l_big_theta(int n_c, int n_p, int CP,
 }
 
 // L2L phi pass of one child: narrow rows (n_c x n_p) -> += child local.
-__global__ void __launch_bounds__(256) k_l2l_big_phi(int n_c, int n_p, PassDims phi, int ldn,
+__global__ void __launch_bounds__(256) k_l2l_big_phi(int n_c, int n_p, PassDims phi, int ldn, int RC,
                                                      const int* __restrict__ clist,
                                                      const double2* __restrict__ Nb,
                                                      const double* __restrict__ RphiT,
@@ -212,21 +213,22 @@ __global__ void __launch_bounds__(256) k_l2l_big_phi(int n_c, int n_p, PassDims 
   extern __shared__ double2 Ns[];
   const int Sc = n_c * n_c;
   const int64_t child = clist ? clist[blockIdx.x] : blockIdx.x;
-  const double2* Nc = Nb + child * n_c * ldn;
-  for (int t = threadIdx.x; t < n_c * phi.lda; t += blockDim.x) {
+  const int i0 = blockIdx.y * RC, nr = min(RC, n_c - i0);  // narrow rows of this CTA
+  const double2* Nc = Nb + child * n_c * ldn + int64_t(i0) * ldn;
+  for (int t = threadIdx.x; t < nr * phi.lda; t += blockDim.x) {
     const int row = t / phi.lda, k = t - row * phi.lda;
     cp_async16(Ns + t, k < n_p ? Nc + row * ldn + k : Nc, k < n_p);
   }
   cp_async_wait_all();
   __syncthreads();
-  rank1_column(n_c, n_p, vphi, [&](int r) { return Ns + r * phi.lda; });
+  rank1_column(nr, n_p, vphi, [&](int r) { return Ns + r * phi.lda; });
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  double* lc = reinterpret_cast<double*>(loc_c) + 2 * child * Sc;
-  warp_gemm_rc(n_c * 2, phi.N, phi.K, [&](int r) { return Ns + r * phi.lda; }, RphiT,
+  double* lc = reinterpret_cast<double*>(loc_c) + 2 * (child * Sc + int64_t(i0) * n_c);
+  warp_gemm_rc(nr * 2, phi.N, phi.K, [&](int r) { return Ns + r * phi.lda; }, RphiT,
                [&](int m0, int n0, double v0, double v1) {
                  const int r = m0 + g, row = r >> 1;
-                 if (row >= n_c) return;
+                 if (row >= nr) return;
 #pragma unroll
                  for (int q = 0; q < 2; ++q) {
                    const int n = n0 + 2 * tq + q;

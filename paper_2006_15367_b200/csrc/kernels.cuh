@@ -24,33 +24,33 @@ constexpr int kSlots = 343;  // (ox, oy, oz) in [-3, 3]^3
 
 // sin and cos of a moderate argument (|x| < 2^20): Cody-Waite reduction by
 // pi/2 with the round-to-nearest quadrant taken from a 1.5*2^52 magic add,
-// then Taylor polynomials on [-pi/4, pi/4] (truncation < 6e-17).  No slow
-// path: the arguments on this path are phases k |r| of a few radians.
+// then the published minimax kernels of fdlibm (__kernel_sin / __kernel_cos,
+// degree 13 / 14 on [-pi/4, pi/4], error < 2^-58).  No slow path: the
+// arguments on this path are phases k |r| of a few radians.  Coefficients
+// live in the constant bank (64-bit immediates cannot be encoded in DFMA).
+__constant__ double kSinCos[14] = {
+    1.58969099521155010221e-10, -2.50507602534068634195e-08, 2.75573137070700676789e-06,
+    -1.98412698298579493134e-04, 8.33333333332248946124e-03, -1.66666666666666324348e-01,  // S6..S1
+    -1.13596475577881948265e-11, 2.08757232129817482790e-09, -2.75573143513906633035e-07,
+    2.48015872894767294178e-05, -1.38888888888741095749e-03, 4.16666666666666019037e-02,   // C6..C1
+    0.63661977236758138, -6.123233995736766e-17};  // 2/pi, -(pi/2)_lo
+
 __device__ __forceinline__ void sincos_fast(double x, double* sp, double* cp) {
   const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-  const double t = fma(x, 0.63661977236758138, kMagic);
+  const double t = fma(x, kSinCos[12], kMagic);
   const int quad = __double2loint(t);
   const double n = t - kMagic;
   double y = fma(n, -1.5707963267948966, x);
-  y = fma(n, -6.123233995736766e-17, y);
+  y = fma(n, kSinCos[13], y);
   const double y2 = y * y;
-  double ps = -7.6471637318198164759e-13;            // -1/15!
-  ps = fma(ps, y2, 1.6059043836821614599e-10);        //  1/13!
-  ps = fma(ps, y2, -2.5052108385441718775e-08);       // -1/11!
-  ps = fma(ps, y2, 2.7557319223985890653e-06);        //  1/9!
-  ps = fma(ps, y2, -1.9841269841269841270e-04);       // -1/7!
-  ps = fma(ps, y2, 8.3333333333333333333e-03);        //  1/5!
-  ps = fma(ps, y2, -1.6666666666666666667e-01);       // -1/3!
+  double ps = kSinCos[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) ps = fma(ps, y2, kSinCos[i]);
   const double sn = fma(ps * y2, y, y);
-  double pc = 4.7794773323873852974e-14;              //  1/16!
-  pc = fma(pc, y2, -1.1470745597729724714e-11);       // -1/14!
-  pc = fma(pc, y2, 2.0876756987868098979e-09);        //  1/12!
-  pc = fma(pc, y2, -2.7557319223985890653e-07);       // -1/10!
-  pc = fma(pc, y2, 2.4801587301587301587e-05);        //  1/8!
-  pc = fma(pc, y2, -1.3888888888888888889e-03);       // -1/6!
-  pc = fma(pc, y2, 4.1666666666666666667e-02);        //  1/4!
-  pc = fma(pc, y2, -0.5);
-  const double cs = fma(pc, y2, 1.0);
+  double pc = kSinCos[6];
+#pragma unroll
+  for (int i = 7; i < 12; ++i) pc = fma(pc, y2, kSinCos[i]);
+  const double cs = fma(pc, y2 * y2, fma(-0.5, y2, 1.0));
   const double s1 = (quad & 1) ? cs : sn;
   const double c1 = (quad & 1) ? sn : cs;
   *sp = (quad & 2) ? -s1 : s1;
@@ -358,76 +358,110 @@ __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __re
 // ---------------------------------------------------------------------------
 // Near-field P2P (operators.cpp:110-122 with green kernel.cpp:9-14, driver
 // traversal.cpp:768-786): one CTA per observer leaf; the near leaves'
-// particles are streamed through shared memory as one concatenated list; G
-// threads cooperate on one observer (G adapts to the leaf population) and
-// reduce by warp shuffles.
+// particles stream through shared memory as one concatenated list (a source
+// finds its leaf by binary search in the prefix sums).  Coordinates are
+// staged relative to the observer leaf centre and scaled by k, and the
+// charges by k / (4 pi), so a pair costs rsqrt + sincos + 4 FMA:
+//   g = exp(-i k r) / (4 pi r) = (k / 4 pi) exp(-i r') / r',  r' = k r.
+// The exact-zero separation (self pair, operators.cpp:118) is masked.
+// Two launch shapes over two leaf lists: SMALL leaves (<= 32 observers) let
+// G threads cooperate per observer; DENSE leaves give every warp all
+// observers of a pass (lane l holds l, l + 32, ...) and a quarter of each
+// staged chunk, so warps do equal work, then combine across warps.
 constexpr int kP2PChunk = 512;
-__global__ void __launch_bounds__(128) k_p2p(int64_t leaf_b, const int64_t* __restrict__ leaf_start,
-                                             const int64_t* __restrict__ near_off,
-                                             const int* __restrict__ near,
-                                             const double* __restrict__ x, const double* __restrict__ y,
-                                             const double* __restrict__ z,
-                                             const double2* __restrict__ q, double k,
-                                             double2* __restrict__ pot) {
-  __shared__ double sx[kP2PChunk], sy[kP2PChunk], sz[kP2PChunk];
-  __shared__ double2 sq[kP2PChunk];
-  __shared__ int64_t pref[28], nbeg[27];
-  const int64_t leaf = leaf_b + blockIdx.x;
-  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
-  const int n_o = int(p1 - p0);
-  const int64_t nb = near_off[leaf];
-  const int nn = int(near_off[leaf + 1] - nb);
+constexpr int kP2PObsPerLane = 8;  // dense leaves: up to 32 x 8 observers per pass
+
+__device__ __forceinline__ void p2p_pair(double xo, double yo, double zo, double sx, double sy, double sz,
+                                         double2 qq, double& ar, double& ai) {
+  const double dx = xo - sx, dy = yo - sy, dz = zo - sz;
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const bool self = r2 == 0.0;
+  const double ri = rsqrt(self ? 1.0 : r2);
+  double sn, cs;
+  sincos_fast(-(r2 * ri), &sn, &cs);  // exp(-i r')
+  const double gr = self ? 0.0 : cs * ri, gi = self ? 0.0 : sn * ri;
+  ar = fma(gr, qq.x, fma(-gi, qq.y, ar));
+  ai = fma(gr, qq.y, fma(gi, qq.x, ai));
+}
+
+struct P2PShared {
+  double sx[kP2PChunk], sy[kP2PChunk], sz[kP2PChunk];
+  double2 sq[kP2PChunk];
+  int64_t pref[28], nbeg[28];
+  int nn;
+};
+
+// Prefix sums of the near leaves of `leaf` into smem; returns the total.
+__device__ __forceinline__ int64_t p2p_prepare(P2PShared& sh, int64_t leaf, const int64_t* __restrict__ leaf_start,
+                                               const int64_t* __restrict__ near_off, const int* __restrict__ near) {
   if (threadIdx.x == 0) {
+    const int64_t nb = near_off[leaf];
+    const int nn = int(near_off[leaf + 1] - nb);
     int64_t run = 0;
     for (int j = 0; j < nn; ++j) {
       const int lf = near[nb + j];
-      pref[j] = run;
-      nbeg[j] = leaf_start[lf];
+      sh.pref[j] = run;
+      sh.nbeg[j] = leaf_start[lf];
       run += leaf_start[lf + 1] - leaf_start[lf];
     }
-    pref[nn] = run;
+    sh.pref[nn] = run;
+    sh.nn = nn;
   }
   __syncthreads();
-  const int64_t total = pref[nn];
-  int G = 32;
-  while (G > 1 && G * n_o > int(blockDim.x)) G >>= 1;
-  const int groups = blockDim.x / G;
-  const int j = threadIdx.x % G;
-  const double inv4pi = 1.0 / (4.0 * M_PI);
-  for (int ob = 0; ob < n_o; ob += groups) {
-    const int o = ob + threadIdx.x / G;
+  return sh.pref[sh.nn];
+}
+
+// Stage concatenated sources [cb, cb + n): relative to (cx, cy, cz), scaled.
+__device__ __forceinline__ void p2p_stage(P2PShared& sh, int64_t cb, int n, const double* __restrict__ x,
+                                          const double* __restrict__ y, const double* __restrict__ z,
+                                          const double2* __restrict__ q, double cx, double cy, double cz, double k,
+                                          double qs) {
+  const int nn = sh.nn;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const int64_t v = cb + t;
+    int lo = 0, hi = nn;  // largest j with pref[j] <= v
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (sh.pref[mid] <= v) lo = mid; else hi = mid;
+    }
+    const int64_t src = sh.nbeg[lo] + (v - sh.pref[lo]);
+    sh.sx[t] = k * (x[src] - cx);
+    sh.sy[t] = k * (y[src] - cy);
+    sh.sz[t] = k * (z[src] - cz);
+    const double2 qq = q[src];
+    sh.sq[t] = make_double2(qs * qq.x, qs * qq.y);
+  }
+}
+
+template <bool DENSE>
+__global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
+                                             const int64_t* __restrict__ near_off, const int* __restrict__ near,
+                                             const double* __restrict__ centers, const double* __restrict__ x,
+                                             const double* __restrict__ y, const double* __restrict__ z,
+                                             const double2* __restrict__ q, double k, double2* __restrict__ pot) {
+  __shared__ P2PShared sh;
+  const int64_t leaf = leaves[blockIdx.x];
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const int n_o = int(p1 - p0);
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
+  const int64_t total = p2p_prepare(sh, leaf, leaf_start, near_off, near);
+  if (!DENSE) {
+    int G = 32;
+    while (G > 1 && G * n_o > int(blockDim.x)) G >>= 1;
+    const int o = threadIdx.x / G, j = threadIdx.x % G;
     const bool valid = o < n_o;
-    const double xo = valid ? x[p0 + o] : 0.0, yo = valid ? y[p0 + o] : 0.0,
-                 zo = valid ? z[p0 + o] : 0.0;
+    const double xo = valid ? k * (x[p0 + o] - cx) : 1e300;
+    const double yo = valid ? k * (y[p0 + o] - cy) : 0.0;
+    const double zo = valid ? k * (z[p0 + o] - cz) : 0.0;
     double ar = 0.0, ai = 0.0;
     for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
       const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
       __syncthreads();
-      for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        const int64_t v = cb + t;
-        int jj = 0;
-        while (pref[jj + 1] <= v) ++jj;
-        const int64_t src = nbeg[jj] + (v - pref[jj]);
-        sx[t] = x[src];
-        sy[t] = y[src];
-        sz[t] = z[src];
-        sq[t] = q[src];
-      }
+      p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
       __syncthreads();
-      if (valid) {
-        for (int t = j; t < n; t += G) {
-          const double dx = xo - sx[t], dy = yo - sy[t], dz = zo - sz[t];
-          if (dx == 0.0 && dy == 0.0 && dz == 0.0) continue;  // self pair
-          const double r = sqrt(dx * dx + dy * dy + dz * dz);
-          double sn, cs;
-          sincos_fast(-k * r, &sn, &cs);
-          const double w = inv4pi / r;
-          const double gr = cs * w, gi = sn * w;
-          const double2 qq = sq[t];
-          ar += gr * qq.x - gi * qq.y;
-          ai += gr * qq.y + gi * qq.x;
-        }
-      }
+      if (valid)
+        for (int t = j; t < n; t += G) p2p_pair(xo, yo, zo, sh.sx[t], sh.sy[t], sh.sz[t], sh.sq[t], ar, ai);
     }
     for (int off = G >> 1; off > 0; off >>= 1) {
       ar += __shfl_down_sync(0xffffffffu, ar, off, G);
@@ -439,6 +473,53 @@ __global__ void __launch_bounds__(128) k_p2p(int64_t leaf_b, const int64_t* __re
       cur.y += ai;
       pot[p0 + o] = cur;
     }
+    return;
+  }
+  __shared__ double2 red[4][32 * kP2PObsPerLane];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  for (int ob = 0; ob < n_o; ob += 32 * kP2PObsPerLane) {
+    const int no = min(n_o - ob, 32 * kP2PObsPerLane);
+    const int nc = (no + 31) >> 5;  // observer slots of this pass
+    double xo[kP2PObsPerLane], yo[kP2PObsPerLane], zo[kP2PObsPerLane];
+    double ar[kP2PObsPerLane], ai[kP2PObsPerLane];
+#pragma unroll
+    for (int c = 0; c < kP2PObsPerLane; ++c) {
+      const int o = lane + 32 * c;
+      const bool v = c < nc && o < no;
+      xo[c] = v ? k * (x[p0 + ob + o] - cx) : 1e300;
+      yo[c] = v ? k * (y[p0 + ob + o] - cy) : 0.0;
+      zo[c] = v ? k * (z[p0 + ob + o] - cz) : 0.0;
+      ar[c] = 0.0;
+      ai[c] = 0.0;
+    }
+    for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
+      const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
+      __syncthreads();
+      p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
+      __syncthreads();
+      for (int t = warp; t < n; t += nwarp) {
+        const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
+        const double2 qq = sh.sq[t];
+#pragma unroll
+        for (int c = 0; c < kP2PObsPerLane; ++c)
+          if (c < nc) p2p_pair(xo[c], yo[c], zo[c], px, py, pz, qq, ar[c], ai[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kP2PObsPerLane; ++c) red[warp][lane + 32 * c] = make_double2(ar[c], ai[c]);
+    __syncthreads();
+    for (int o = threadIdx.x; o < no; o += blockDim.x) {
+      double2 sum = red[0][o];
+      for (int w = 1; w < nwarp; ++w) {
+        sum.x += red[w][o].x;
+        sum.y += red[w][o].y;
+      }
+      double2 cur = pot[p0 + ob + o];
+      cur.x += sum.x;
+      cur.y += sum.y;
+      pot[p0 + ob + o] = cur;
+    }
+    __syncthreads();
   }
 }
 
