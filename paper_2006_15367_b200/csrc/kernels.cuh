@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __re
 // observers of a pass (lane l holds l, l + 32, ...) and a quarter of each
 // staged chunk, so warps do equal work, then combine across warps.
 constexpr int kP2PChunk = 512;
-constexpr int kP2PObsPerLane = 8;  // dense leaves: up to 32 x 8 observers per pass
+constexpr int kP2PObsPerLane = 4;  // dense leaves: 32 x 4 observers per pass (measured best of 2..8)
 
 __device__ __forceinline__ void p2p_pair(double xo, double yo, double zo, double sx, double sy, double sz,
                                          double2 qq, double& ar, double& ai) {
