@@ -213,6 +213,45 @@ void Engine::upload() {
     n_dense_ = int(dense.size());
     d_small_leaves_ = upload_vec(small);
     d_dense_leaves_ = upload_vec(dense);
+    // symmetric pair lists among own dense leaves (k_p2p_sym / k_p2p_gather)
+    std::vector<int> pos(s.num_leaves(), -1);
+    for (size_t i = 0; i < dense.size(); ++i) pos[size_t(dense[i])] = int(i);
+    std::vector<int> poff{0}, pl, soff{0}, sl;
+    std::vector<int64_t> sscr;
+    std::vector<std::vector<std::pair<int, int64_t>>> incoming(dense.size());
+    int64_t scr = 0;
+    for (size_t i = 0; i < dense.size(); ++i) {
+      const int a = dense[i];
+      for (uint64_t z2 = s.near_off[size_t(a)]; z2 < s.near_off[size_t(a) + 1]; ++z2) {
+        const int b = int(s.near[z2]);
+        if (b > a && pos[size_t(b)] >= 0) {
+          sl.push_back(b);
+          sscr.push_back(scr);
+          incoming[size_t(pos[size_t(b)])].push_back({a, scr});
+          scr += int64_t(s.leaf_start[size_t(b) + 1] - s.leaf_start[size_t(b)]);
+        } else if (b == a || pos[size_t(b)] < 0) {
+          pl.push_back(b);
+        }
+      }
+      poff.push_back(int(pl.size()));
+      soff.push_back(int(sl.size()));
+    }
+    std::vector<int> ioff{0};
+    std::vector<int64_t> iscr;
+    for (auto& v : incoming) {  // senders in ascending leaf order: deterministic sums
+      std::sort(v.begin(), v.end());
+      for (auto& e : v) iscr.push_back(e.second);
+      ioff.push_back(int(iscr.size()));
+    }
+    d_plain_off_ = upload_vec(poff);
+    d_plain_ = upload_vec(pl);
+    d_sym_off_ = upload_vec(soff);
+    d_sym_ = upload_vec(sl);
+    d_sym_scr_ = upload_vec(sscr);
+    d_in_off_ = upload_vec(ioff);
+    d_in_scr_ = upload_vec(iscr);
+    d_p2p_scratch_ = alloc<double2>(size_t(std::max<int64_t>(scr, 1)));
+    use_sym_ = std::getenv("HFMM_P2P_NOSYM") == nullptr;
   }
 
   lv_.assign(size_t(L + 1), DevLevel{});
@@ -587,7 +626,14 @@ void Engine::phase_near() {
                                                       d_x, d_y, d_z, d_q, s_.k, d_pot);
     ++launches_;
   }
-  if (n_dense_ > 0) {
+  if (n_dense_ > 0 && use_sym_) {
+    k_p2p_sym<<<unsigned(n_dense_), 128, 0, st_>>>(d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_, d_sym_off_,
+                                                   d_sym_, d_sym_scr_, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot,
+                                                   d_p2p_scratch_);
+    k_p2p_gather<<<unsigned(n_dense_), 128, 0, st_>>>(d_dense_leaves_, d_leaf_start, d_in_off_, d_in_scr_,
+                                                      d_p2p_scratch_, d_pot);
+    launches_ += 2;
+  } else if (n_dense_ > 0) {
     k_p2p<true><<<unsigned(n_dense_), 128, 0, st_>>>(d_dense_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
                                                      d_x, d_y, d_z, d_q, s_.k, d_pot);
     ++launches_;

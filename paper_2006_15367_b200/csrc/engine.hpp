@@ -160,6 +160,15 @@ class Engine {
   int* d_small_leaves_ = nullptr;  // own leaves with <= 32 particles
   int* d_dense_leaves_ = nullptr;
   int n_small_ = 0, n_dense_ = 0;
+  int* d_plain_off_ = nullptr;  // symmetric P2P lists over dense own leaves
+  int* d_plain_ = nullptr;
+  int* d_sym_off_ = nullptr;
+  int* d_sym_ = nullptr;
+  int64_t* d_sym_scr_ = nullptr;
+  int* d_in_off_ = nullptr;
+  int64_t* d_in_scr_ = nullptr;
+  double2* d_p2p_scratch_ = nullptr;
+  bool use_sym_ = true;
   double2* d_tmp = nullptr;  // interpolation temporaries
   size_t tmp_elems_ = 0;
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range

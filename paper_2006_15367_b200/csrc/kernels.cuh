@@ -524,6 +524,170 @@ __global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, con
 }
 
 // ---------------------------------------------------------------------------
+// Symmetric near field for dense leaves: g(r) is the same for (m <- n) and
+// (n <- m), so every unordered pair of dense own leaves (A, B), A < B, is
+// evaluated once by A's CTA: A's observers accumulate in registers, B's in a
+// per-pair scratch row (warp-reduced over A's observers), which
+// k_p2p_gather adds to B in a fixed order (deterministic).  The self leaf
+// and neighbours that are small or ghost leaves go through the one-sided
+// path (`plain` list).
+__global__ void __launch_bounds__(128) k_p2p_sym(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
+                                                 const int* __restrict__ plain_off, const int* __restrict__ plain,
+                                                 const int* __restrict__ sym_off, const int* __restrict__ sym,
+                                                 const int64_t* __restrict__ sym_scr,
+                                                 const double* __restrict__ centers, const double* __restrict__ x,
+                                                 const double* __restrict__ y, const double* __restrict__ z,
+                                                 const double2* __restrict__ q, double k, double2* __restrict__ pot,
+                                                 double2* __restrict__ scratch) {
+  __shared__ P2PShared sh;
+  __shared__ double2 red[4][32 * kP2PObsPerLane];
+  const int i = blockIdx.x;
+  const int64_t leaf = leaves[i];
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const int n_o = int(p1 - p0);
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  // plain list as a concatenated source list (prefix sums as in p2p_prepare)
+  if (threadIdx.x == 0) {
+    const int b = plain_off[i], nn = plain_off[i + 1] - b;
+    int64_t run = 0;
+    for (int j = 0; j < nn; ++j) {
+      const int lf = plain[b + j];
+      sh.pref[j] = run;
+      sh.nbeg[j] = leaf_start[lf];
+      run += leaf_start[lf + 1] - leaf_start[lf];
+    }
+    sh.pref[nn] = run;
+    sh.nn = nn;
+  }
+  __syncthreads();
+  const int64_t total = sh.pref[sh.nn];
+  for (int ob = 0, pass = 0; ob < n_o; ob += 32 * kP2PObsPerLane, ++pass) {
+    const int no = min(n_o - ob, 32 * kP2PObsPerLane);
+    const int nc = (no + 31) >> 5;
+    double xo[kP2PObsPerLane], yo[kP2PObsPerLane], zo[kP2PObsPerLane];
+    double2 qo[kP2PObsPerLane];
+    double ar[kP2PObsPerLane], ai[kP2PObsPerLane];
+#pragma unroll
+    for (int c = 0; c < kP2PObsPerLane; ++c) {
+      const int o = lane + 32 * c;
+      const bool v = c < nc && o < no;
+      // invalid slots: far away but finite (zero charge, finite kernel value),
+      // so their terms in the partner leaf's reduction are exact zeros
+      xo[c] = v ? k * (x[p0 + ob + o] - cx) : 1.0e4;
+      yo[c] = v ? k * (y[p0 + ob + o] - cy) : 0.0;
+      zo[c] = v ? k * (z[p0 + ob + o] - cz) : 0.0;
+      const double2 qq = v ? q[p0 + ob + o] : make_double2(0.0, 0.0);
+      qo[c] = make_double2(qs * qq.x, qs * qq.y);
+      ar[c] = 0.0;
+      ai[c] = 0.0;
+    }
+    // one-sided part: self leaf + small / ghost neighbours
+    for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
+      const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
+      __syncthreads();
+      p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
+      __syncthreads();
+      for (int t = warp; t < n; t += nwarp) {
+        const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
+        const double2 qq = sh.sq[t];
+#pragma unroll
+        for (int c = 0; c < kP2PObsPerLane; ++c)
+          if (c < nc) p2p_pair(xo[c], yo[c], zo[c], px, py, pz, qq, ar[c], ai[c]);
+      }
+    }
+    // symmetric part: dense partners B > A
+    for (int j = sym_off[i]; j < sym_off[i + 1]; ++j) {
+      const int lb = sym[j];
+      const int64_t b0 = leaf_start[lb], nbp = leaf_start[lb + 1] - b0;
+      double2* scr = scratch + sym_scr[j];
+      for (int64_t cb = 0; cb < nbp; cb += kP2PChunk) {
+        const int n = int(nbp - cb < kP2PChunk ? nbp - cb : kP2PChunk);
+        __syncthreads();
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+          const int64_t src = b0 + cb + t;
+          sh.sx[t] = k * (x[src] - cx);
+          sh.sy[t] = k * (y[src] - cy);
+          sh.sz[t] = k * (z[src] - cz);
+          const double2 qq = q[src];
+          sh.sq[t] = make_double2(qs * qq.x, qs * qq.y);
+        }
+        __syncthreads();
+        for (int t = warp; t < n; t += nwarp) {
+          const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
+          const double2 qq = sh.sq[t];
+          double br = 0.0, bi = 0.0;
+#pragma unroll
+          for (int c = 0; c < kP2PObsPerLane; ++c) {
+            if (c < nc) {
+              const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
+              const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+              const bool self = r2 == 0.0;  // coincident particles in different leaves cannot occur
+              const double ri = rsqrt(self ? 1.0 : r2);
+              double sn, cs;
+              sincos_fast(-(r2 * ri), &sn, &cs);
+              const double gr = self ? 0.0 : cs * ri, gi = self ? 0.0 : sn * ri;
+              ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
+              ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
+              br = fma(gr, qo[c].x, fma(-gi, qo[c].y, br));
+              bi = fma(gr, qo[c].y, fma(gi, qo[c].x, bi));
+            }
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            br += __shfl_xor_sync(0xffffffffu, br, off);
+            bi += __shfl_xor_sync(0xffffffffu, bi, off);
+          }
+          if (lane == 0) {
+            double2 v = make_double2(br, bi);
+            if (pass > 0) {
+              const double2 old = scr[cb + t];
+              v.x += old.x;
+              v.y += old.y;
+            }
+            scr[cb + t] = v;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kP2PObsPerLane; ++c) red[warp][lane + 32 * c] = make_double2(ar[c], ai[c]);
+    __syncthreads();
+    for (int o = threadIdx.x; o < no; o += blockDim.x) {
+      double2 sum = red[0][o];
+      for (int w = 1; w < nwarp; ++w) {
+        sum.x += red[w][o].x;
+        sum.y += red[w][o].y;
+      }
+      double2 cur = pot[p0 + ob + o];
+      cur.x += sum.x;
+      cur.y += sum.y;
+      pot[p0 + ob + o] = cur;
+    }
+    __syncthreads();
+  }
+}
+
+// Adds the scratch rows other dense leaves wrote for leaf B (fixed order).
+__global__ void k_p2p_gather(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
+                             const int* __restrict__ in_off, const int64_t* __restrict__ in_scr,
+                             const double2* __restrict__ scratch, double2* __restrict__ pot) {
+  const int i = blockIdx.x;
+  const int64_t leaf = leaves[i];
+  const int64_t p0 = leaf_start[leaf], n = leaf_start[leaf + 1] - p0;
+  for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+    double2 acc = pot[p0 + t];
+    for (int j = in_off[i]; j < in_off[i + 1]; ++j) {
+      const double2 v = scratch[in_scr[j] + t];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    pot[p0 + t] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Permutations between input order and Morton order (traversal.cpp:108-110, :809-815).
 __global__ void k_gather_q(int64_t n, const int64_t* __restrict__ orig, const double2* __restrict__ q_in,
                            double2* __restrict__ q_sorted) {

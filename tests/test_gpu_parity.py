@@ -90,6 +90,19 @@ def test_config1_full_and_direct(hb, refo):
     assert rel_l2(res3.potentials, 2.0 * res.potentials) < 1e-14
 
 
+def test_dense_leaves_symmetric_near_field(hb, refo):
+    """Sphere with ~250 particles per leaf: the symmetric dense-leaf P2P path."""
+    pos, q = hb.generate_inputs("sphere", 200_000, 2.0, 45)
+    q2 = np.stack([q.real, q.imag], -1)
+    setup = hb.build_setup(pos, q)
+    counts = np.diff(setup.array("leaf_start", np.uint64).astype(np.int64))
+    assert (counts > 32).sum() > 100 and counts.max() > 128  # several observer passes
+    res = hb.RankEngine(setup).evaluate()
+    assert np.all(np.isfinite(res.potentials))
+    want, _, _ = refo.RefSetup(pos, q2, refo.config(num_ranks=os.cpu_count() or 1, scheduler=2)).evaluate()
+    assert rel_l2(res.potentials, want) < TOL
+
+
 def test_zero_and_linearity(hb):
     pos, q = hb.generate_inputs("sphere", 20_000, 1.5, 41)
     setup = hb.build_setup(pos, q)
