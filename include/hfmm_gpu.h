@@ -98,12 +98,15 @@ typedef enum hfmm_phase {
   HFMM_PHASE_M2L = 3, /* RankEngine::m2l_pass    traversal.cpp:443 */
   HFMM_PHASE_L2L = 4, /* RankEngine::l2l_pass    traversal.cpp:583 */
   HFMM_PHASE_L2T = 5, /* l2o part of l2o_near_phase traversal.cpp:717-728 */
-  HFMM_PHASE_NEAR = 6 /* near part of l2o_near_phase traversal.cpp:768-786 */
+  HFMM_PHASE_NEAR = 6, /* near part of l2o_near_phase traversal.cpp:768-786: joins it into
+                          the potentials (launching it first if not started) */
+  HFMM_PHASE_NEAR_START = 7 /* launches the near field on the engine's side stream
+                               (overlaps the far-field phases; needs charges/ghosts) */
 } hfmm_phase;
 
 /* Per-phase device milliseconds of the last hfmm_gpu_evaluate (CUDA events
  * on the engine stream), indexed by hfmm_phase; [0] = T-operator build,
- * [7] = whole evaluation. */
+ * [6] = near field (side stream, overlapped), [7] = whole evaluation. */
 typedef struct hfmm_gpu_timing {
   double ms[8];
   int64_t kernel_launches;

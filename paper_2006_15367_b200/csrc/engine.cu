@@ -64,8 +64,16 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   // debugging aid: large-level path 0 = two-stage (default), 1 = fused runtime, 2 = legacy two-pass
   if (const char* p = std::getenv("HFMM_BIG_PATH")) path_ = std::atoi(p);
   l2l_ct_ = std::getenv("HFMM_L2L_CT") != nullptr;
+  if (const char* p = std::getenv("HFMM_BIG_THREADS")) big_threads_ = std::atoi(p);
   ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
+  // Side stream for the near field.  (Giving the far-field chain a higher
+  // stream priority measured slower on cfg 2 and cfg 3: equal priorities.)
+  ck(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream2");
+  ck(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreate(&ev_near0_), "event");
+  ck(cudaEventCreate(&ev_near1_), "event");
   upload();
   if (dist_) upload_rank_plan();
   ck(cudaStreamSynchronize(st_), "upload sync");
@@ -78,6 +86,12 @@ Engine::~Engine() {
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (st_ && owns_stream_) cudaStreamDestroy(st_);
+  if (st2_) {
+    cudaStreamSynchronize(st2_);
+    cudaStreamDestroy(st2_);
+  }
+  for (cudaEvent_t e : {ev_fork_, ev_join_, ev_near0_, ev_near1_})
+    if (e) cudaEventDestroy(e);
 }
 
 namespace {
@@ -194,6 +208,7 @@ void Engine::upload() {
   d_q = alloc<double2>(n);
   ck(cudaMemcpyAsync(d_q, s.q.data(), n * sizeof(double2), cudaMemcpyHostToDevice, st_), "q");
   d_pot = alloc<double2>(n);
+  d_pot_near = alloc<double2>(n);
   d_q_in = alloc<double2>(n);
   d_pot_in = alloc<double2>(n);
   std::vector<int64_t> orig(s.original_index.begin(), s.original_index.end());
@@ -486,12 +501,12 @@ void Engine::phase_m2m() {
       ck(cudaFuncSetAttribute(k_m2m_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[1])), "attr");
       if (ncl > 0) {
         dim3 g0(unsigned(ncl), unsigned((nc + P.big_rc[0] - 1) / P.big_rc[0]));
-        k_m2m_big_phi<<<g0, 256, P.big_smem[0], st_>>>(nc, np, to_dims(P.up_phi), P.up_th[2], P.big_rc[0], clist, C.mp,
+        k_m2m_big_phi<<<g0, big_threads_, P.big_smem[0], st_>>>(nc, np, to_dims(P.up_phi), P.up_th[2], P.big_rc[0], clist, C.mp,
                                                                  P.up_phi_B, P.up_phi_v, d_tmp);
         ++launches_;
       }
       dim3 grid(unsigned(cl.n_par), unsigned((np / 2 + P.big_m2m_cp - 1) / P.big_m2m_cp));
-      k_m2m_big_theta<<<grid, 256, P.big_smem[1], st_>>>(nc, np, P.big_m2m_cp, to_dims(P.up_th), cl.plist, cl.child_off,
+      k_m2m_big_theta<<<grid, big_threads_, P.big_smem[1], st_>>>(nc, np, P.big_m2m_cp, to_dims(P.up_th), cl.plist, cl.child_off,
                                                          cl.children, oct_[size_t(l + 1)], d_tmp, P.up_th_B,
                                                          P.up_th_v, P.shift_up, P.mp);
       ++launches_;
@@ -568,12 +583,12 @@ void Engine::phase_l2l() {
       ck(cudaFuncSetAttribute(k_l2l_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[2])), "attr");
       ck(cudaFuncSetAttribute(k_l2l_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[3])), "attr");
       dim3 grid(unsigned(ncl), unsigned((np / 2 + P.big_l2l_cp - 1) / P.big_l2l_cp));
-      k_l2l_big_theta<<<grid, 256, P.big_smem[2], st_>>>(nc, np, P.big_l2l_cp, to_dims(P.dn_th), P.big_ldn, clist,
+      k_l2l_big_theta<<<grid, big_threads_, P.big_smem[2], st_>>>(nc, np, P.big_l2l_cp, to_dims(P.dn_th), P.big_ldn, clist,
                                                          C.parent, oct_[size_t(l + 1)], P.loc, P.shift_dn, P.dn_th_B,
                                                          P.dn_th_v, d_tmp);
       ++launches_;
       dim3 g3(unsigned(ncl), unsigned((nc + P.big_rc[1] - 1) / P.big_rc[1]));
-      k_l2l_big_phi<<<g3, 256, P.big_smem[3], st_>>>(nc, np, to_dims(P.dn_phi), P.big_ldn, P.big_rc[1], clist, d_tmp,
+      k_l2l_big_phi<<<g3, big_threads_, P.big_smem[3], st_>>>(nc, np, to_dims(P.dn_phi), P.big_ldn, P.big_rc[1], clist, d_tmp,
                                                                P.dn_phi_B, P.dn_phi_v, C.loc);
       ++launches_;
       ck(cudaGetLastError(), "l2l big");
@@ -619,26 +634,50 @@ void Engine::phase_l2t() {
   ck(cudaGetLastError(), "k_l2t");
 }
 
-void Engine::phase_near() {
+// Near field on the side stream: waits for everything issued so far on the
+// main stream (charges, ghosts), accumulates into d_pot_near.
+void Engine::near_start() {
   const DevLevel& d = lv_[size_t(s_.L)];
+  ck(cudaEventRecord(ev_fork_, st_), "fork");
+  ck(cudaStreamWaitEvent(st2_, ev_fork_, 0), "fork wait");
+  cudaEventRecord(ev_near0_, st2_);
+  const int64_t cnt = part_e_ - part_b_;
+  if (cnt > 0)
+    ck(cudaMemsetAsync(d_pot_near + part_b_, 0, size_t(cnt) * sizeof(double2), st2_), "memset near");
   if (n_small_ > 0) {
-    k_p2p<false><<<unsigned(n_small_), 128, 0, st_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
-                                                      d_x, d_y, d_z, d_q, s_.k, d_pot);
+    k_p2p<false><<<unsigned(n_small_), 128, 0, st2_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
+                                                       d_x, d_y, d_z, d_q, s_.k, d_pot_near);
     ++launches_;
   }
   if (n_dense_ > 0 && use_sym_) {
-    k_p2p_sym<<<unsigned(n_dense_), 128, 0, st_>>>(d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_, d_sym_off_,
-                                                   d_sym_, d_sym_scr_, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot,
-                                                   d_p2p_scratch_);
-    k_p2p_gather<<<unsigned(n_dense_), 128, 0, st_>>>(d_dense_leaves_, d_leaf_start, d_in_off_, d_in_scr_,
-                                                      d_p2p_scratch_, d_pot);
+    k_p2p_sym<<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_, d_sym_off_,
+                                                    d_sym_, d_sym_scr_, d.centers, d_x, d_y, d_z, d_q, s_.k,
+                                                    d_pot_near, d_p2p_scratch_);
+    k_p2p_gather<<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_in_off_, d_in_scr_,
+                                                       d_p2p_scratch_, d_pot_near);
     launches_ += 2;
   } else if (n_dense_ > 0) {
-    k_p2p<true><<<unsigned(n_dense_), 128, 0, st_>>>(d_dense_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
-                                                     d_x, d_y, d_z, d_q, s_.k, d_pot);
+    k_p2p<true><<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
+                                                      d_x, d_y, d_z, d_q, s_.k, d_pot_near);
     ++launches_;
   }
   ck(cudaGetLastError(), "k_p2p");
+  cudaEventRecord(ev_near1_, st2_);
+  ck(cudaEventRecord(ev_join_, st2_), "join");
+  near_started_ = true;
+}
+
+// Joins the near field into the potentials (after L2T wrote the far field).
+void Engine::phase_near() {
+  if (!near_started_) near_start();
+  ck(cudaStreamWaitEvent(st_, ev_join_, 0), "join wait");
+  const int64_t cnt = part_e_ - part_b_;
+  if (cnt > 0) {
+    k_add_pot<<<unsigned((cnt + 255) / 256), 256, 0, st_>>>(part_b_, part_e_, d_pot_near, d_pot);
+    ++launches_;
+  }
+  ck(cudaGetLastError(), "k_add_pot");
+  near_started_ = false;
 }
 
 void Engine::run_phase(int phase) {
@@ -663,6 +702,9 @@ void Engine::run_phase(int phase) {
     case HFMM_PHASE_NEAR:
       phase_near();
       break;
+    case HFMM_PHASE_NEAR_START:
+      near_start();
+      break;
     default:
       throw std::invalid_argument("hfmm_gpu_run_phase: unknown phase");
   }
@@ -684,6 +726,7 @@ void Engine::last_timing(double* ms, int64_t* launches) {
     cudaEventElapsedTime(&f, ev_[i], ev_[i + 1]);
     ms[i] = f;
   }
+  if (cudaEventElapsedTime(&f, ev_near0_, ev_near1_) == cudaSuccess) ms[6] = f;  // side stream
   cudaEventElapsedTime(&f, ev_[0], ev_[7]);
   ms[7] = f;
   if (launches) *launches = last_launches_;
@@ -700,6 +743,7 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
   if (d_q_sorted && d_q_sorted != reinterpret_cast<const double*>(d_q))
     ck(cudaMemcpyAsync(d_q, d_q_sorted, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "q");
   cudaEventRecord(ev_[0], st_);
+  near_start();  // side stream, overlapped with the far-field chain
   build_T();
   cudaEventRecord(ev_[1], st_);
   phase_c2m();

@@ -143,6 +143,7 @@ class Engine {
   int64_t launches_ = 0;
   bool use_ct_ = true;
   bool l2l_ct_ = false;
+  int big_threads_ = 256;  // block size of the two-stage large-grid kernels
   int path_ = 0;           // large-level M2M/L2L path (see constructor)
   size_t tmp_need_ = 0;    // temp elements required by the large-level kernels
   // particles (sorted)
@@ -174,6 +175,12 @@ class Engine {
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range
   int64_t part_b_ = 0, part_e_ = 0;  // owned particle range
   cudaEvent_t ev_[8] = {};
+  // near field on a side stream, overlapped with the far-field chain
+  cudaStream_t st2_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_near0_ = nullptr, ev_near1_ = nullptr;
+  double2* d_pot_near = nullptr;
+  bool near_started_ = false;
+  void near_start();
   // distributed mode
   bool dist_ = false;
   std::vector<RankLevel> rl_;               // [level as parent]

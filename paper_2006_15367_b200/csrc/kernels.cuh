@@ -694,6 +694,16 @@ __global__ void k_gather_q(int64_t n, const int64_t* __restrict__ orig, const do
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) q_sorted[i] = q_in[orig[i]];
 }
+__global__ void k_add_pot(int64_t b, int64_t e, const double2* __restrict__ add, double2* __restrict__ pot) {
+  const int64_t i = b + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < e) {
+    double2 a = pot[i];
+    const double2 v = add[i];
+    a.x += v.x;
+    a.y += v.y;
+    pot[i] = a;
+  }
+}
 __global__ void k_scatter_pot(int64_t b, int64_t e, const int64_t* __restrict__ orig,
                               const double2* __restrict__ pot_sorted, double2* __restrict__ pot_in) {
   const int64_t i = b + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

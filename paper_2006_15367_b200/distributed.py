@@ -82,6 +82,7 @@ class DistributedEvaluator:
     def step(self) -> None:
         """One evaluation from the charges already loaded into the engine."""
         self.exchange(KIND_GHOST)
+        self.eng.run_phase(Phase.NearStart)  # near field overlaps the far-field chain
         self.eng.run_phase(Phase.C2M)
         self.eng.run_phase(Phase.M2M)
         self.exchange(KIND_MULTIPOLE)

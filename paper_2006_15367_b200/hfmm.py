@@ -43,6 +43,7 @@ class Phase(enum.IntEnum):
     L2L = 4
     L2T = 5
     Near = 6
+    NearStart = 7
 
 
 @dataclass
