@@ -9,10 +9,10 @@
 // compile time along x and is warp-uniform along y, z.
 //
 // Work decomposition (B200): one CTA = an 8x8x8 observer block x 2 samples.
-// The 14^3 source region (block + halo 3) for the 2 samples and the 343 T
-// taps are staged in shared memory (~100 KB, 2 CTAs/SM).  Each thread owns an
-// x-row of 8 observers for one sample; for every (dy, dz) tap row it loads the
-// 14 source values of its row once and the 7 taps (a warp broadcast) and
+// The 12^3 source region (block + one parent group) for the 2 samples and the
+// 343 T taps are staged in shared memory (~69 KB, 3 CTAs/SM).  Each thread owns
+// an x-row of 8 observers for one sample; for every (dy, dz) tap row it loads
+// the 12 source values of its row once and the 7 taps (a warp broadcast) and
 // issues up to 48 complex FMAs from registers.  A warp holds 16 rows of one
 // (y, z) parity class x 2 samples, so every mask branch is warp-uniform and
 // the padded row stride makes the 16-byte loads bank-conflict free.
@@ -25,9 +25,14 @@ namespace hfmm_b200 {
 
 namespace m2l {
 constexpr int MB = 8;               // observer block edge
-constexpr int MR = MB + 6;          // source region edge (halo 3)
-constexpr int ROW = MR * 2 + 1;     // double2 per region row (2 samples/cell + 16 B pad)
-constexpr int ZS = MR * ROW;        // double2 per region z-slice
+// Far sources have adjacent PARENTS, so the halo is exactly one parent group:
+// cells [b - 2, b + MB + 2) per axis (a tap at distance 3 only reaches an
+// adjacent parent from the block's interior).
+constexpr int HALO = 2;
+constexpr int MR = MB + 2 * HALO;   // source region edge (12)
+constexpr int ROW = MR * 2 + 1;     // double2 per region row (2 samples/cell + 16 B pad, odd)
+constexpr int ZS = MR * ROW + 2;    // double2 per z-slice: 2 ZS == 4 (mod 8) keeps the
+                                    // 16-byte row loads of a warp bank-conflict free
 constexpr int REGION = MR * ZS;     // double2 in the region
 constexpr int SMEM_BYTES = (REGION + kSlots * 2) * 16;
 
@@ -45,13 +50,13 @@ __device__ __forceinline__ void tap_row(double2 (&acc)[MB], const double2 (&m)[M
       // observer x = 8 bx + k: parent-adjacency along x depends on k and dx only
       const bool xnear = iabs(fdiv2(k) - fdiv2(k - dx)) <= 1;
       const bool adjacent = INNER && iabs(dx) <= 1;
-      if (xnear && !adjacent) cmac(acc[k], t[dx + 3], m[k - dx + 3]);
+      if (xnear && !adjacent) cmac(acc[k], t[dx + 3], m[k - dx + HALO]);
     }
   }
 }
 }  // namespace m2l
 
-__global__ void __launch_bounds__(128, 2) k_m2l_dense(int G, int nb, int64_t S,
+__global__ void __launch_bounds__(128, 3) k_m2l_dense(int G, int nb, int64_t S,
                                                       const int* __restrict__ lookup,
                                                       const double2* __restrict__ T,
                                                       const double2* __restrict__ mp,
@@ -72,17 +77,18 @@ __global__ void __launch_bounds__(128, 2) k_m2l_dense(int G, int nb, int64_t S,
     cp_async16(Ts + t, T + int64_t(t >> 1) * S + s0 + (t & 1), true);
   {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-    const int GP = (G > MB ? G : MB) + 6;  // padded edge (host: same formula)
+    const int GP = (G > MB ? G : MB) + 6;  // padded edge (host: same formula, halo 3)
     const int cx = lane >> 1, sw = lane & 1;
-    // 196 rows over 4 warps: 7 batches of 7 rows, lookups of a batch in flight together
-    constexpr int RB = 7;
+    // 144 rows over 4 warps: batches of 6 rows, lookups of a batch in flight together
+    constexpr int RB = 6;
     for (int r0 = warp * RB; r0 < MR * MR; r0 += nwarp * RB) {
       int node[RB];
 #pragma unroll
       for (int u = 0; u < RB; ++u) {
         const int row = r0 + u, cz = row / MR, cy = row - cz * MR;
         node[u] = (lane < 2 * MR && row < MR * MR)
-                      ? __ldg(lookup + (int64_t(bz + cz) * GP + (by + cy)) * GP + (bx + cx))
+                      ? __ldg(lookup + (int64_t(bz + cz + 3 - HALO) * GP + (by + cy + 3 - HALO)) * GP +
+                              (bx + cx + 3 - HALO))
                       : -1;
       }
 #pragma unroll
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(128, 2) k_m2l_dense(int G, int nb, int64_t S,
     if (!parent_near(pz, dz)) continue;
     for (int dy = -3; dy <= 3; ++dy) {
       if (!parent_near(py, dy)) continue;
-      const double2* row = Ms + (oz - dz + 3) * ZS + (oy - dy + 3) * ROW + sw;
+      const double2* row = Ms + (oz - dz + HALO) * ZS + (oy - dy + HALO) * ROW + sw;
       double2 m[MR];
 #pragma unroll
       for (int i = 0; i < MR; ++i) m[i] = row[2 * i];
