@@ -52,14 +52,25 @@ struct Shape {
   static constexpr int L2L_CB = pick(false, kBudget2, 0) > 0 ? pick(false, kBudget2, 0) : pick(false, kBudget1, 0);
   static constexpr int L2L_DB = pick(false, kBudget2, 0) > 0 ? pick(false, kBudget2, 1) : pick(false, kBudget1, 1);
   static constexpr int L2L_BYTES = L2L_CB > 0 ? l2l_bytes(L2L_CB, L2L_DB) : 0;
+  // resident CTAs per SM the plan is sized for (the register cap follows it)
+  static constexpr int M2M_MINB = M2M_BYTES > 0 && M2M_BYTES <= kBudget2 ? 2 : 1;
+  static constexpr int L2L_MINB = L2L_BYTES > 0 && L2L_BYTES <= kBudget2 ? 2 : 1;
 };
 
 // Warp-tiled DMMA GEMM with compile-time shape; B (K x N, row-major) in smem.
 // Warp tile = up to 2 x 2 8x8 sub-tiles; padded sub-tiles are skipped.
-// pre(m0, n0, valid) runs before the k-loop of every 8x8 sub-tile's owner
-// (all lanes), epi(m0, n0, c0, c1) after it (all lanes, may shuffle).
-template <int M, int N, int K, class RowPtr, class Epi>
-__device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ Bs, Epi epi) {
+// pre(m0, n0) runs for every live 8x8 sub-tile BEFORE the k-loop (all lanes;
+// its result -- e.g. prefetched epilogue operands -- is handed to epi, so
+// their latency hides behind the DMMAs); epi(m0, n0, c0, c1, pre) after it.
+struct F2x2 {
+  double2 v[2];
+};
+struct NoPre {
+  __device__ __forceinline__ int operator()(int, int) const { return 0; }
+};
+
+template <int M, int N, int K, class RowPtr, class Epi, class Pre = NoPre>
+__device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ Bs, Epi epi, Pre pre = Pre()) {
   constexpr int MT8 = (M + 7) / 8, NT8 = N / 8;
   constexpr int MT = (MT8 + 1) / 2, NT = (NT8 + 1) / 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -68,6 +79,10 @@ __device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ 
     const int mt = w / NT, nt = w - mt * NT;
     const int m0 = mt * 16, n0 = nt * 16;
     const bool vm1 = 2 * mt + 1 < MT8, vn1 = 2 * nt + 1 < NT8;
+    const auto p00 = pre(m0, n0);
+    const auto p01 = pre(m0, vn1 ? n0 + 8 : n0);
+    const auto p10 = pre(vm1 ? m0 + 8 : m0, n0);
+    const auto p11 = pre(vm1 ? m0 + 8 : m0, vn1 ? n0 + 8 : n0);
     const int r0 = m0 + g, r1 = m0 + 8 + g;
     const bool ok0 = r0 < M, ok1 = r1 < M;
     const double* a0p = reinterpret_cast<const double*>(rowp(ok0 ? r0 >> 1 : 0)) + (r0 & 1) + 2 * tq;
@@ -92,34 +107,39 @@ __device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ 
         dmma884(c10a, c10b, a1, b0);
       }
     }
-    epi(m0, n0, c00a, c00b);
-    if (vn1) epi(m0, n0 + 8, c01a, c01b);
+    epi(m0, n0, c00a, c00b, p00);
+    if (vn1) epi(m0, n0 + 8, c01a, c01b, p01);
     if (vm1) {
-      epi(m0 + 8, n0, c10a, c10b);
-      if (vn1) epi(m0 + 8, n0 + 8, c11a, c11b);
+      epi(m0 + 8, n0, c10a, c10b, p10);
+      if (vn1) epi(m0 + 8, n0 + 8, c11a, c11b, p11);
     }
   }
 }
 
+// x[KIN] = i (v . x) for ROWS complex rows (the rank-1 imaginary part of the
+// resampling map, interp_tc.cuh).  Four lanes per row, eight rows per warp
+// pass: two shuffle levels instead of five.
 template <int ROWS, int KIN, int LD>
 __device__ __forceinline__ void rank1_ct(double2* X, const double* __restrict__ v) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < ROWS; r += kWarps) {
+  const int sub = lane & 3;
+  constexpr int RUP = (ROWS + 7) / 8 * 8;  // whole warps iterate together (shuffles)
+  for (int r = warp * 8 + (lane >> 2); r < RUP; r += kWarps * 8) {
+    const bool live = r < ROWS;
     double sr = 0.0, si = 0.0;
-    double2* x = X + r * LD;
+    double2* x = X + (live ? r : 0) * LD;
 #pragma unroll
-    for (int k = lane; k < KIN; k += 32) {
+    for (int k = sub; k < KIN; k += 4) {
       const double vk = __ldg(v + k);
       const double2 xv = x[k];
       sr = fma(vk, xv.x, sr);
       si = fma(vk, xv.y, si);
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      sr += __shfl_xor_sync(0xffffffffu, sr, off);
-      si += __shfl_xor_sync(0xffffffffu, si, off);
-    }
-    if (lane == 0) x[KIN] = make_double2(-si, sr);
+    sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+    si += __shfl_xor_sync(0xffffffffu, si, 1);
+    sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+    si += __shfl_xor_sync(0xffffffffu, si, 2);
+    if (live && sub == 0) x[KIN] = make_double2(-si, sr);
   }
 }
 
@@ -136,7 +156,7 @@ __device__ __forceinline__ void stage_doubles(double* dst, const double* __restr
 
 // ---------------------------------------------------------------------------
 template <int NC, int NP>
-__global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* __restrict__ plist,
+__global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::M2M_MINB)) k_m2m_ct(int n_par, const int* __restrict__ plist,
                                                         const int* __restrict__ child_off,
                                                         const int* __restrict__ children,
                                                         const uint8_t* __restrict__ oct_c,
@@ -200,7 +220,7 @@ __global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* _
     __syncthreads();
     // phi pass -> folded circles
     ct::gemm_ct<CB * NC * 2, S::UPHI_N, S::UPHI_K>(
-        [&](int r) { return X + r * S::UPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1) {
+        [&](int r) { return X + r * S::UPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1, int) {
           const int r = m0 + g, ci = r >> 1, c = ci / NC, i = ci - c * NC;
           if (c >= CB) return;
           double2* base = Fs + c * HALF * S::UTH_LDA;
@@ -227,23 +247,18 @@ __global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* _
           const int p = row / CB, c = row - p * CB;
           return Fs + (c * HALF + p) * S::UTH_LDA;
         },
-        Bth, [&](int m0, int n0, double v0, double v1) {
+        Bth,
+        [&](int m0, int n0, double v0, double v1, const ct::F2x2& f) {
           const int r = m0 + g, part = r & 1, c = (r >> 1) % CB, p = r / R2;
           const double o0 = __shfl_xor_sync(0xffffffffu, v0, 4);
           const double o1 = __shfl_xor_sync(0xffffffffu, v1, 4);
-          const bool live = c < nb && p < HALF;
-          const double2* sh = shift_up + octs[c] * SP;
           double cr[2], cim[2];
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const int n = n0 + 2 * tq + q;
             const double re = part ? (q ? o1 : o0) : (q ? v1 : v0);
             const double im = part ? (q ? v1 : v0) : (q ? o1 : o0);
-            const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
-            double2 f = make_double2(0.0, 0.0);
-            if (live && n < 2 * NP) f = __ldg(sh + s);
-            cr[q] = re * f.x - im * f.y;
-            cim[q] = re * f.y + im * f.x;
+            cr[q] = re * f.v[q].x - im * f.v[q].y;
+            cim[q] = re * f.v[q].y + im * f.v[q].x;
           }
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
@@ -269,6 +284,19 @@ __global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* _
               }
             }
           }
+        },
+        [&](int m0, int n0) {  // shift factors of this lane's two outputs, loaded ahead of the k-loop
+          const int r = m0 + g, c = (r >> 1) % CB, p = r / R2;
+          const bool live = c < nb && p < HALF;
+          const double2* sh = shift_up + octs[c] * SP;
+          ct::F2x2 f;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = n0 + 2 * tq + q;
+            const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
+            f.v[q] = (live && n < 2 * NP) ? __ldg(sh + s) : make_double2(0.0, 0.0);
+          }
+          return f;
         });
     __syncthreads();
     if (npar != par) {  // parent complete: write out and reset the accumulator
@@ -285,7 +313,7 @@ __global__ void __launch_bounds__(ct::kThreads) k_m2m_ct(int n_par, const int* _
 
 // ---------------------------------------------------------------------------
 template <int NC, int NP>
-__global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* __restrict__ plist,
+__global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::L2L_MINB)) k_l2l_ct(int n_par, const int* __restrict__ plist,
                                                         const int* __restrict__ child_off,
                                                         const int* __restrict__ children,
                                                         const uint8_t* __restrict__ oct_c,
@@ -343,7 +371,7 @@ __global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* _
       ct::rank1_ct<CB * HALF, 2 * NP, S::DTH_LDA>(Fs, vth);
       __syncthreads();
       ct::gemm_ct<CB * HALF * 2, S::DTH_N, S::DTH_K>(
-          [&](int r) { return Fs + r * S::DTH_LDA; }, Bth, [&](int m0, int n0, double v0, double v1) {
+          [&](int r) { return Fs + r * S::DTH_LDA; }, Bth, [&](int m0, int n0, double v0, double v1, int) {
             const int r = m0 + g, ci = r >> 1, c = ci / HALF, p = ci - c * HALF;
             if (c >= CB) return;
             double2* base = Ns + c * NC * S::DPHI_LDA;
@@ -361,7 +389,7 @@ __global__ void __launch_bounds__(ct::kThreads) k_l2l_ct(int n_par, const int* _
       ct::rank1_ct<CB * NC, NP, S::DPHI_LDA>(Ns, vphi);
       __syncthreads();
       ct::gemm_ct<CB * NC * 2, S::DPHI_N, S::DPHI_K>(
-          [&](int r) { return Ns + r * S::DPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1) {
+          [&](int r) { return Ns + r * S::DPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1, int) {
             const int r = m0 + g, ci = r >> 1, c = ci / NC, row = ci - c * NC;
             if (c >= nb) return;
             double* dst = lc + 2 * (int64_t(children[b0 + c]) * SC + row * NC) + (r & 1);
