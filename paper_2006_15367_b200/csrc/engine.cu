@@ -60,6 +60,7 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   if (rank < 0 || rank >= s.P) throw std::invalid_argument("hfmm_gpu_create: bad rank");
   dist_ = s.P > 1;
   ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
   use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;  // debugging aid: runtime-shaped kernels only
   // debugging aid: large-level path 0 = two-stage (default), 1 = fused runtime, 2 = legacy two-pass
   if (const char* p = std::getenv("HFMM_BIG_PATH")) path_ = std::atoi(p);
@@ -548,8 +549,9 @@ void Engine::phase_m2l() {
     DevLevel& d = lv_[size_t(l)];
     if (d.dense) {
       const int nb = (d.G + m2l::MB - 1) / m2l::MB;
-      dim3 grid(unsigned(nb * nb * nb), unsigned(d.S / 2));
-      k_m2l_dense<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, d.lookup, d.T, d.mp, d.loc);
+      const int ppc = m2l_pairs_per_cta(nb * nb * nb, d.S, sms_);
+      dim3 grid(unsigned(nb * nb * nb), unsigned((d.S / 2 + ppc - 1) / ppc));
+      k_m2l_dense<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, d.lookup, d.T, d.mp, d.loc);
     } else {
       dim3 grid(unsigned(d.n_nodes), unsigned((d.S + 127) / 128));
       k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, d.far_off, d.far, d.T, d.mp, d.loc);

@@ -135,6 +135,7 @@ class Engine {
 
   const Setup& s_;
   int dev_ = 0, rank_ = 0;
+  int sms_ = 148;  // multiprocessors of dev_
   cudaStream_t st_ = nullptr;
   bool owns_stream_ = true;
   std::vector<DevLevel> lv_;

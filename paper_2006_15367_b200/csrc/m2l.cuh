@@ -8,9 +8,11 @@
 // far depends only on d and on the parities of o, so the mask is resolved at
 // compile time along x and is warp-uniform along y, z.
 //
-// Work decomposition (B200): one CTA = an 8x8x8 observer block x 2 samples.
-// The 12^3 source region (block + one parent group) for the 2 samples and the
-// 343 T taps are staged in shared memory (~69 KB, 3 CTAs/SM).  Each thread owns
+// Work decomposition (B200): one CTA = an 8x8x8 observer block x a chunk of
+// sample pairs.  The node indices of the 12^3 source region (block + one
+// parent group) are resolved once into shared memory; then, per pair, the
+// region's 2 samples and the 343 T taps are staged in shared memory (~76 KB
+// with the index table, 3 CTAs/SM).  Each thread owns
 // an x-row of 8 observers for one sample; for every (dy, dz) tap row it loads
 // the 12 source values of its row once and the 7 taps (a warp broadcast) and
 // issues up to 48 complex FMAs from registers.  A warp holds 16 rows of one
@@ -34,7 +36,8 @@ constexpr int ROW = MR * 2 + 1;     // double2 per region row (2 samples/cell + 
 constexpr int ZS = MR * ROW + 2;    // double2 per z-slice: 2 ZS == 4 (mod 8) keeps the
                                     // 16-byte row loads of a warp bank-conflict free
 constexpr int REGION = MR * ZS;     // double2 in the region
-constexpr int SMEM_BYTES = (REGION + kSlots * 2) * 16;
+constexpr int CELLS = MR * MR * MR;  // region cells (node index table)
+constexpr int SMEM_BYTES = (REGION + kSlots * 2) * 16 + CELLS * 4;
 
 __host__ __device__ constexpr int fdiv2(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }
 __host__ __device__ constexpr int iabs(int v) { return v < 0 ? -v : v; }
@@ -56,7 +59,7 @@ __device__ __forceinline__ void tap_row(double2 (&acc)[MB], const double2 (&m)[M
 }
 }  // namespace m2l
 
-__global__ void __launch_bounds__(128, 3) k_m2l_dense(int G, int nb, int64_t S,
+__global__ void __launch_bounds__(128, 3) k_m2l_dense(int G, int nb, int64_t S, int ppc,
                                                       const int* __restrict__ lookup,
                                                       const double2* __restrict__ T,
                                                       const double2* __restrict__ mp,
@@ -65,84 +68,80 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dense(int G, int nb, int64_t S,
   extern __shared__ double2 smem[];
   double2* Ms = smem;
   double2* Ts = smem + REGION;
+  int* nodes = reinterpret_cast<int*>(Ts + kSlots * 2);  // region cell -> node (-1: empty)
   const int blk = blockIdx.x;
   const int bx = (blk % nb) * MB, by = ((blk / nb) % nb) * MB, bz = (blk / (nb * nb)) * MB;
-  const int64_t s0 = int64_t(blockIdx.y) * 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // Stage T taps and the source region with cp.async (LDGSTS): every load is
-  // in flight at once; empty / out-of-grid cells are zero-filled by the copy.
-  // The lookup is halo-padded by 3 cells (entries -1), so a region row is 14
-  // consecutive entries: one warp per row, lane = 2 * cx + sample.
-  for (int t = threadIdx.x; t < kSlots * 2; t += blockDim.x)
-    cp_async16(Ts + t, T + int64_t(t >> 1) * S + s0 + (t & 1), true);
+  // Node indices of the region, once per CTA.  The lookup is halo-padded by 3
+  // cells (entries -1), so every region cell has an entry.
   {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
     const int GP = (G > MB ? G : MB) + 6;  // padded edge (host: same formula, halo 3)
-    const int cx = lane >> 1, sw = lane & 1;
-    // 144 rows over 4 warps: batches of 6 rows, lookups of a batch in flight together
-    constexpr int RB = 6;
-    for (int r0 = warp * RB; r0 < MR * MR; r0 += nwarp * RB) {
-      int node[RB];
-#pragma unroll
-      for (int u = 0; u < RB; ++u) {
-        const int row = r0 + u, cz = row / MR, cy = row - cz * MR;
-        node[u] = (lane < 2 * MR && row < MR * MR)
-                      ? __ldg(lookup + (int64_t(bz + cz + 3 - HALO) * GP + (by + cy + 3 - HALO)) * GP +
-                              (bx + cx + 3 - HALO))
-                      : -1;
-      }
-#pragma unroll
-      for (int u = 0; u < RB; ++u) {
-        const int row = r0 + u, cz = row / MR, cy = row - cz * MR;
-        if (lane < 2 * MR && row < MR * MR) {
-          const bool ok = node[u] >= 0;
-          cp_async16(Ms + cz * ZS + cy * ROW + lane, mp + (ok ? int64_t(node[u]) * S + s0 + sw : 0), ok);
-        }
-      }
+    for (int c = threadIdx.x; c < CELLS; c += blockDim.x) {
+      const int cz = c / (MR * MR), cy = (c / MR) % MR, cx = c % MR;
+      nodes[c] = __ldg(lookup + (int64_t(bz + cz + 3 - HALO) * GP + (by + cy + 3 - HALO)) * GP + (bx + cx + 3 - HALO));
     }
   }
-  cp_async_wait_all();
-  __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int py = warp & 1, pz = warp >> 1;
   const int sw = lane & 1, r = lane >> 1;
   const int oy = 2 * (r & 3) + py, oz = 2 * (r >> 2) + pz;
-  double2 acc[MB];
-#pragma unroll
-  for (int k = 0; k < MB; ++k) acc[k] = make_double2(0.0, 0.0);
+  const int64_t pairs = S / 2;
+  const int64_t pb = int64_t(blockIdx.y) * ppc, pe = pb + ppc < pairs ? pb + ppc : pairs;
 
-  for (int dz = -3; dz <= 3; ++dz) {
-    if (!parent_near(pz, dz)) continue;
-    for (int dy = -3; dy <= 3; ++dy) {
-      if (!parent_near(py, dy)) continue;
-      const double2* row = Ms + (oz - dz + HALO) * ZS + (oy - dy + HALO) * ROW + sw;
-      double2 m[MR];
-#pragma unroll
-      for (int i = 0; i < MR; ++i) m[i] = row[2 * i];
-      const double2* trow = Ts + ((dy + 3) * 7 + (dz + 3)) * 2 + sw;
-      double2 t[7];
-#pragma unroll
-      for (int j = 0; j < 7; ++j) t[j] = trow[j * 49 * 2];
-      if (iabs(dy) <= 1 && iabs(dz) <= 1)
-        tap_row<true>(acc, m, t);
-      else
-        tap_row<false>(acc, m, t);
+  for (int64_t pr = pb; pr < pe; ++pr) {
+    const int64_t s0 = pr * 2;
+    __syncthreads();  // node table ready / previous pair done with the buffers
+    // Stage the T taps and the region's two samples with cp.async (LDGSTS):
+    // every load in flight at once; empty cells are zero-filled by the copy.
+    for (int t = threadIdx.x; t < kSlots * 2; t += blockDim.x)
+      cp_async16(Ts + t, T + int64_t(t >> 1) * S + s0 + (t & 1), true);
+    for (int t = threadIdx.x; t < CELLS * 2; t += blockDim.x) {
+      const int c = t >> 1, cz = c / (MR * MR), cy = (c / MR) % MR, cx = c % MR;
+      const int node = nodes[c];
+      cp_async16(Ms + cz * ZS + cy * ROW + 2 * cx + (t & 1), mp + (node >= 0 ? int64_t(node) * S + s0 + (t & 1) : 0),
+                 node >= 0);
     }
-  }
+    cp_async_wait_all();
+    __syncthreads();
 
-  const int gy = by + oy, gz = bz + oz;
-  if (gy < G && gz < G) {
+    double2 acc[MB];
 #pragma unroll
-    for (int k = 0; k < MB; ++k) {
-      const int gx = bx + k;
-      if (gx < G) {
-        const int GP = (G > MB ? G : MB) + 6;
-        const int node = lookup[(int64_t(gz + 3) * GP + (gy + 3)) * GP + (gx + 3)];
-        if (node >= 0) loc[int64_t(node) * S + s0 + sw] = acc[k];
+    for (int k = 0; k < MB; ++k) acc[k] = make_double2(0.0, 0.0);
+
+    for (int dz = -3; dz <= 3; ++dz) {
+      if (!parent_near(pz, dz)) continue;
+      for (int dy = -3; dy <= 3; ++dy) {
+        if (!parent_near(py, dy)) continue;
+        const double2* row = Ms + (oz - dz + HALO) * ZS + (oy - dy + HALO) * ROW + sw;
+        double2 m[MR];
+#pragma unroll
+        for (int i = 0; i < MR; ++i) m[i] = row[2 * i];
+        const double2* trow = Ts + ((dy + 3) * 7 + (dz + 3)) * 2 + sw;
+        double2 t[7];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) t[j] = trow[j * 49 * 2];
+        if (iabs(dy) <= 1 && iabs(dz) <= 1)
+          tap_row<true>(acc, m, t);
+        else
+          tap_row<false>(acc, m, t);
       }
     }
+
+    // observers are region cells (k + HALO, oy + HALO, oz + HALO)
+    const int* orow = nodes + ((oz + HALO) * MR + (oy + HALO)) * MR + HALO;
+#pragma unroll
+    for (int k = 0; k < MB; ++k) {
+      const int node = orow[k];
+      if (node >= 0) loc[int64_t(node) * S + s0 + sw] = acc[k];
+    }
   }
+}
+
+// Sample pairs per CTA: enough CTAs for ~6 waves at 3 CTAs/SM, at most 16.
+inline int m2l_pairs_per_cta(int nblocks, int64_t S, int sms) {
+  const int64_t target = int64_t(sms) * 3 * 6;
+  int64_t ppc = int64_t(nblocks) * (S / 2) / (target > 0 ? target : 1);
+  return int(ppc < 1 ? 1 : ppc > 16 ? 16 : ppc);
 }
 
 }  // namespace hfmm_b200
