@@ -64,7 +64,7 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;  // debugging aid: runtime-shaped kernels only
   // debugging aid: large-level path 0 = two-stage (default), 1 = fused runtime, 2 = legacy two-pass
   if (const char* p = std::getenv("HFMM_BIG_PATH")) path_ = std::atoi(p);
-  l2l_ct_ = std::getenv("HFMM_L2L_CT") != nullptr;
+  l2l_ct_ = std::getenv("HFMM_L2L_BIG") == nullptr;  // debugging aid: two-stage L2L everywhere
   if (const char* p = std::getenv("HFMM_BIG_THREADS")) big_threads_ = std::atoi(p);
   ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   for (auto& e : ev_) ck(cudaEventCreate(&e), "event");

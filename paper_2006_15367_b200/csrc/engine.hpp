@@ -143,7 +143,7 @@ class Engine {
   std::vector<void*> allocs_;
   int64_t launches_ = 0;
   bool use_ct_ = true;
-  bool l2l_ct_ = false;
+  bool l2l_ct_ = true;
   int big_threads_ = 256;  // block size of the two-stage large-grid kernels
   int path_ = 0;           // large-level M2M/L2L path (see constructor)
   size_t tmp_need_ = 0;    // temp elements required by the large-level kernels

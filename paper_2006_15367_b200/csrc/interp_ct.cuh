@@ -65,6 +65,9 @@ struct Shape {
 struct F2x2 {
   double2 v[2];
 };
+struct D2 {
+  double v[2];
+};
 struct NoPre {
   __device__ __forceinline__ int operator()(int, int) const { return 0; }
 };
@@ -352,19 +355,39 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::L2L_MINB)) k
     const double2* L = DB ? Lp : lpg;
     for (int b0 = cb; b0 < ce; b0 += CB) {
       const int nb = min(CB, ce - b0);
-      for (int row = warp; row < CB * HALF; row += ct::kWarps) {
-        const int c = row / HALF, p = row - c * HALF;
-        double2* f = Fs + row * S::DTH_LDA;
-        if (c < nb) {
-          const double2* sh = shift_dn + int64_t(oct_c[children[b0 + c]]) * SP;
+      // Child pointers of the batch first (dependent loads), then the shifted
+      // parent circles: flat over (child, circle, sample), FB elements per
+      // thread per round with every load of the round in flight together.
+      int64_t cnode[CB];
+      const double2* shc[CB];
 #pragma unroll
-          for (int i = lane; i < 2 * NP; i += 32) {
+      for (int c = 0; c < CB; ++c) {
+        cnode[c] = c < nb ? children[b0 + c] : 0;
+        shc[c] = shift_dn + int64_t(c < nb ? oct_c[cnode[c]] : 0) * SP;
+      }
+      {
+        constexpr int FE = CB * HALF * 2 * NP, FPT = (FE + ct::kThreads - 1) / ct::kThreads, FB = 5;
+#pragma unroll
+        for (int j0 = 0; j0 < FPT; j0 += FB) {
+          double2 lv[FB], sv[FB];
+#pragma unroll
+          for (int u = 0; u < FB; ++u) {
+            const int t = threadIdx.x + (j0 + u) * ct::kThreads;
+            const int c = t / (HALF * 2 * NP), rem = t - c * (HALF * 2 * NP), p = rem / (2 * NP), i = rem - p * (2 * NP);
             const int s = i < NP ? i * NP + p : (2 * NP - 1 - i) * NP + p + HALF;
-            f[i] = cmul(L[s], __ldg(sh + s));
-          }
-        } else {
+            const double2* sh = shc[0];
 #pragma unroll
-          for (int i = lane; i < 2 * NP; i += 32) f[i] = make_double2(0.0, 0.0);
+            for (int cc = 1; cc < CB; ++cc) sh = c == cc ? shc[cc] : sh;
+            const bool ok = j0 + u < FPT && t < FE && c < nb;
+            lv[u] = ok ? L[s] : make_double2(0.0, 0.0);
+            sv[u] = ok ? __ldg(sh + s) : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < FB; ++u) {
+            const int t = threadIdx.x + (j0 + u) * ct::kThreads;
+            const int c = t / (HALF * 2 * NP), rem = t - c * (HALF * 2 * NP), p = rem / (2 * NP), i = rem - p * (2 * NP);
+            if (j0 + u < FPT && t < FE) Fs[(c * HALF + p) * S::DTH_LDA + i] = cmul(lv[u], sv[u]);
+          }
         }
       }
       __syncthreads();
@@ -389,15 +412,33 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::L2L_MINB)) k
       ct::rank1_ct<CB * NC, NP, S::DPHI_LDA>(Ns, vphi);
       __syncthreads();
       ct::gemm_ct<CB * NC * 2, S::DPHI_N, S::DPHI_K>(
-          [&](int r) { return Ns + r * S::DPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1, int) {
+          [&](int r) { return Ns + r * S::DPHI_LDA; }, Bphi,
+          [&](int m0, int n0, double v0, double v1, const ct::D2& old) {
             const int r = m0 + g, ci = r >> 1, c = ci / NC, row = ci - c * NC;
             if (c >= nb) return;
-            double* dst = lc + 2 * (int64_t(children[b0 + c]) * SC + row * NC) + (r & 1);
+            int64_t node = cnode[0];
+#pragma unroll
+            for (int cc = 1; cc < CB; ++cc) node = c == cc ? cnode[cc] : node;
+            double* dst = lc + 2 * (node * SC + row * NC) + (r & 1);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
               const int n = n0 + 2 * tq + q;
-              if (n < NC) dst[2 * n] += q ? v1 : v0;
+              if (n < NC) dst[2 * n] = old.v[q] + (q ? v1 : v0);
             }
+          },
+          [&](int m0, int n0) {  // the child locals this lane adds to, loaded ahead of the k-loop
+            const int r = m0 + g, ci = r >> 1, c = ci / NC, row = ci - c * NC;
+            int64_t node = cnode[0];
+#pragma unroll
+            for (int cc = 1; cc < CB; ++cc) node = c == cc ? cnode[cc] : node;
+            const double* dst = lc + 2 * (node * SC + row * NC) + (r & 1);
+            ct::D2 o;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int n = n0 + 2 * tq + q;
+              o.v[q] = (c < nb && n < NC) ? dst[2 * n] : 0.0;
+            }
+            return o;
           });
       __syncthreads();
     }
@@ -448,7 +489,9 @@ template <int A, int B>
 bool try_l2l_ct(const CtLaunch& L, const double2* loc_p, double2* loc_c, const double* Bth, const double* vth,
                 const double* Bphi, const double* vphi, const double2* shift_dn) {
   using S = ct::Shape<A, B>;
-  if constexpr (S::L2L_CB > 0) {
+  // Fused L2L only where two CTAs fit per SM; otherwise the two-stage kernels
+  // (interp_big.cuh) are faster (measured: (26,34) 7.9 vs 9.9 ms, (34,52) 3.1 vs 2.9 ms).
+  if constexpr (S::L2L_CB > 0 && S::L2L_MINB == 2) {
     auto fn = k_l2l_ct<A, B>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::L2L_BYTES);
     const int grid = ct_grid<A, B>(L.n_par, S::L2L_BYTES, reinterpret_cast<const void*>(fn));
