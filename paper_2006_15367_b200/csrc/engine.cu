@@ -454,7 +454,7 @@ void Engine::build_T() {
     DevLevel& d = lv_[size_t(l)];
     if (d.n_far == 0) continue;
     dim3 grid(unsigned((d.S + 127) / 128), kSlots);
-    k_tbuild<<<grid, 128, size_t(d.trunc + 1) * sizeof(double2), st_>>>(d.S, d.trunc, d.dir, d.side,
+    k_tbuild<<<grid, 128, 2 * size_t(d.trunc + 1) * sizeof(double2), st_>>>(d.S, d.trunc, d.dir, d.side,
                                                                          d.tcoef, d.slot_used, d.T);
     ++launches_;
   }

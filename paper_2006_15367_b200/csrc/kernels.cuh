@@ -76,8 +76,14 @@ __global__ void k_tbuild(int64_t S, int trunc, const double* __restrict__ dir, d
                          double2* __restrict__ T) {
   const int slot = blockIdx.y;
   if (!used[slot]) return;
+  // coefficients + Legendre recurrence factors a_l = (2l-1)/l, b_l = (l-1)/l
+  // (one division per l per CTA instead of one per l per sample)
   extern __shared__ double2 coef[];
-  for (int l = threadIdx.x; l <= trunc; l += blockDim.x) coef[l] = tcoef[slot * (trunc + 1) + l];
+  double2* ab = coef + (trunc + 1);
+  for (int l = threadIdx.x; l <= trunc; l += blockDim.x) {
+    coef[l] = tcoef[slot * (trunc + 1) + l];
+    ab[l] = l > 0 ? make_double2(double(2 * l - 1) / double(l), double(l - 1) / double(l)) : make_double2(0.0, 0.0);
+  }
   __syncthreads();
   const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= S) return;
@@ -90,7 +96,8 @@ __global__ void k_tbuild(int64_t S, int trunc, const double* __restrict__ dir, d
   double pm1 = 0.0, p0 = 1.0;
   double2 acc = coef[0];
   for (int l = 1; l <= trunc; ++l) {
-    const double p1 = (double(2 * l - 1) * u * p0 - double(l - 1) * pm1) / double(l);
+    const double2 f = ab[l];
+    const double p1 = fma(f.x * u, p0, -f.y * pm1);
     pm1 = p0;
     p0 = p1;
     acc.x = fma(coef[l].x, p0, acc.x);
