@@ -180,6 +180,13 @@ hfmm_status hfmm_gpu_synchronize(hfmm_gpu* g);
 hfmm_status hfmm_gpu_load_charges_device(hfmm_gpu* g, const double* d_charges_sorted);
 /* This rank's sorted particle range [*begin, *end). */
 hfmm_status hfmm_gpu_particle_range(hfmm_gpu* g, int64_t* begin, int64_t* end);
+/* Copies this rank's potentials (sorted order, its particle range) into the
+ * device array d_pot_sorted at the same offsets, asynchronously on the
+ * engine's stream (the per-rank output of l2o_near_phase, traversal.cpp:717-788). */
+hfmm_status hfmm_gpu_store_potentials_device(hfmm_gpu* g, double* d_pot_sorted);
+/* Kernels this handle has launched so far (cumulative; a bench counts its
+ * timed region by difference). */
+hfmm_status hfmm_gpu_launch_count(hfmm_gpu* g, int64_t* launches);
 
 /* One-shot: build_setup + evaluate on one device (evaluate_potential,
  * traversal.cpp:819-823).  Requires cfg->num_ranks == 1. */

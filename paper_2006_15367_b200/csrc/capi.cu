@@ -247,6 +247,22 @@ hfmm_status hfmm_gpu_particle_range(hfmm_gpu* g, int64_t* b, int64_t* e) {
   });
 }
 
+hfmm_status hfmm_gpu_store_potentials_device(hfmm_gpu* g, double* d_pot) {
+  return guard([&] {
+    need(g, "hfmm_gpu_store_potentials_device(gpu)");
+    need(d_pot, "hfmm_gpu_store_potentials_device(pot)");
+    g->eng->store_potentials_device(d_pot);
+  });
+}
+
+hfmm_status hfmm_gpu_launch_count(hfmm_gpu* g, int64_t* n) {
+  return guard([&] {
+    need(g, "hfmm_gpu_launch_count(gpu)");
+    need(n, "hfmm_gpu_launch_count(out)");
+    *n = g->eng->launch_count();
+  });
+}
+
 hfmm_status hfmm_evaluate_potential(const double* positions, const double* charges, size_t n,
                                     const hfmm_run_config* cfg, int device, double* pot_out) {
   return guard([&] {

@@ -966,6 +966,15 @@ void Engine::load_charges_device(const double* d_q_sorted) {
        "charges");
 }
 
+void Engine::store_potentials_device(double* d_pot_sorted) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  const int64_t b = dist_ ? part_b_ : 0, e = dist_ ? part_e_ : int64_t(s_.n);
+  if (e > b)
+    ck(cudaMemcpyAsync(reinterpret_cast<double2*>(d_pot_sorted) + b, d_pot + b, size_t(e - b) * sizeof(double2),
+                       cudaMemcpyDeviceToDevice, st_),
+       "potentials");
+}
+
 void direct_sum(const double* positions, const double* charges, size_t n, const int64_t* obs,
                 size_t m, double k, int device, double* pot_out) {
     int ndev = 0;

@@ -111,6 +111,8 @@ class Engine {
   void set_stream(cudaStream_t st);
   void synchronize();
   void load_charges_device(const double* d_q_sorted);
+  void store_potentials_device(double* d_pot_sorted);
+  int64_t launch_count() const { return launches_; }
   int64_t particle_begin() const { return part_b_; }
   int64_t particle_end() const { return part_e_; }
   void get_potentials_sorted(double* out, size_t cap_doubles);

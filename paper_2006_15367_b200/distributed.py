@@ -56,6 +56,8 @@ class DistributedEvaluator:
         return 8 * sum(int(self.send[kind, q].numel()) for q in range(self.world) if q != self.rank)
 
     def exchange(self, kind: int) -> None:
+        if self.world == 1:  # nothing to exchange (single-rank engines have no plan)
+            return
         dist = self.torch.distributed
         if kind == KIND_MULTIPOLE:
             self.eng.exchange_begin(kind)
@@ -79,17 +81,29 @@ class DistributedEvaluator:
             if q != self.rank and self.recv[kind, q].numel():
                 self.eng.unpack(kind, q, self.recv[kind, q])
 
-    def step(self) -> None:
-        """One evaluation from the charges already loaded into the engine."""
+    def step(self, mark=None) -> None:
+        """One evaluation from the charges already loaded into the engine.
+
+        `mark(name)` (optional) is called after every stage, e.g. to record
+        CUDA events for per-phase device timing."""
+        mark = mark or (lambda name: None)
         self.exchange(KIND_GHOST)
+        mark("ghosts")
         self.eng.run_phase(Phase.NearStart)  # near field overlaps the far-field chain
         self.eng.run_phase(Phase.C2M)
+        mark("C2M")
         self.eng.run_phase(Phase.M2M)
+        mark("M2M")
         self.exchange(KIND_MULTIPOLE)
+        mark("multipoles")
         self.eng.run_phase(Phase.M2L)
+        mark("M2L")
         self.eng.run_phase(Phase.L2L)
+        mark("L2L")
         self.eng.run_phase(Phase.L2T)
+        mark("L2T")
         self.eng.run_phase(Phase.Near)
+        mark("Near")
 
 
 def gpu_rank_engine(setup, rank: int, device: int):
@@ -99,64 +113,3 @@ def gpu_rank_engine(setup, rank: int, device: int):
     eng = RankEngine(setup, rank, device)
     eng.set_stream(torch.cuda.current_stream(device).cuda_stream)
     return eng
-
-
-def bench_main(args, config, workload_name):
-    """bench.py --gpus N under torchrun: strong scaling of one configuration."""
-    import torch
-    import torch.distributed as dist
-    from . import hfmm as hb
-
-    rank = dist.get_rank() if dist.is_initialized() else None
-    if rank is None:
-        dist.init_process_group("nccl")
-        rank = dist.get_rank()
-    world = dist.get_world_size()
-    local = torch.cuda.current_device()
-    shape, n, ext, seed, digits = config
-    pos, q = hb.generate_inputs(shape, n, ext, seed)
-    setup = hb.build_setup(pos, q, hb.RunConfig(digits=digits, num_ranks=world))
-    stream = torch.cuda.Stream(local)
-    torch.cuda.set_stream(stream)
-    eng = gpu_rank_engine(setup, rank, local)
-    ev = DistributedEvaluator(eng, rank, world, torch.device("cuda", local))
-    orig = setup.original_index
-    q_sorted = torch.from_numpy(np.stack([q.real, q.imag], -1)[orig].copy()).cuda()
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-
-    def step():
-        eng.load_charges_device(q_sorted.data_ptr())
-        ev.step()
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = []
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        step()
-        e1.record(stream)
-        e1.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
-        ms.append(float(t.item()))
-    total_ms = sum(ms)
-    line = None
-    if rank == 0:
-        line = {
-            "metric": "targets evaluated/sec (full MLFMA)", "value": n * args.steps / (total_ms / 1e3),
-            "unit": "targets/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name, "N": n, "parallelism": f"{world} GPUs, Morton-range sharding",
-                       "exchange_bytes_per_step": {"multipole": ev.exchange_bytes(KIND_MULTIPOLE),
-                                                   "ghost": ev.exchange_bytes(KIND_GHOST)}},
-        }
-    dist.barrier()
-    return line

@@ -248,6 +248,16 @@ class RankEngine:
     def load_charges_device(self, d_q_sorted_ptr: int) -> None:
         check(lib().hfmm_gpu_load_charges_device(self._h, ctypes.c_void_p(d_q_sorted_ptr)))
 
+    def store_potentials_device(self, d_pot_sorted_ptr: int) -> None:
+        """Async device copy of this rank's potentials (sorted, own range)."""
+        check(lib().hfmm_gpu_store_potentials_device(self._h, ctypes.c_void_p(d_pot_sorted_ptr)))
+
+    def launch_count(self) -> int:
+        """Kernels launched by this engine so far (cumulative)."""
+        n = ctypes.c_int64()
+        check(lib().hfmm_gpu_launch_count(self._h, ctypes.byref(n)))
+        return n.value
+
     def particle_range(self) -> tuple[int, int]:
         b = ctypes.c_int64()
         e = ctypes.c_int64()

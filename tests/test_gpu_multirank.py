@@ -50,9 +50,14 @@ def _run_ranks(hb, setup, q, engs):
             e.run_phase(ph)
         e.synchronize()
     pot = np.full(setup.n, np.nan, complex)
+    dev = torch.full((setup.n, 2), float("nan"), dtype=torch.float64, device="cuda")
     for e in engs:
         b, en = e.particle_range()
         pot[b:en] = e.potentials_sorted()[b:en]
+        e.store_potentials_device(dev.data_ptr())  # own range only, async on the engine stream
+        e.synchronize()
+    d = dev.cpu().numpy()
+    assert np.array_equal(d[:, 0] + 1j * d[:, 1], pot)  # ranges tile [0, n) exactly
     return pot
 
 
@@ -67,7 +72,9 @@ def test_ranks_emulated_on_one_gpu(ranks, case, native, refo):
     pos, q = hb.generate_inputs(shape, n, ext, seed)
     setup = hb.build_setup(pos, q, hb.RunConfig(digits=dig, num_ranks=ranks))
     engs = [hb.RankEngine(setup, r, 0) for r in range(ranks)]
+    l0 = [e.launch_count() for e in engs]
     pot_sorted = _run_ranks(hb, setup, q, engs)
+    assert all(e.launch_count() - c >= 6 for e, c in zip(engs, l0))  # every phase launched kernels
     assert np.all(np.isfinite(pot_sorted))
     q2 = np.stack([q.real, q.imag], -1)
     want, _, _ = refo.RefSetup(pos, q2, refo.config(digits=dig, num_ranks=os.cpu_count() or 1,
