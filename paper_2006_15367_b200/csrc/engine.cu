@@ -82,15 +82,13 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
-  if (st_) cudaStreamSynchronize(st_);
+  for (cudaStream_t s : {st_, st2_})  // both streams idle before the buffers go
+    if (s) cudaStreamSynchronize(s);
   for (void* p : allocs_) cudaFree(p);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (st_ && owns_stream_) cudaStreamDestroy(st_);
-  if (st2_) {
-    cudaStreamSynchronize(st2_);
-    cudaStreamDestroy(st2_);
-  }
+  if (st2_) cudaStreamDestroy(st2_);
   for (cudaEvent_t e : {ev_fork_, ev_join_, ev_near0_, ev_near1_})
     if (e) cudaEventDestroy(e);
 }
