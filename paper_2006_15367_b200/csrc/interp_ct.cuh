@@ -72,6 +72,33 @@ struct NoPre {
   __device__ __forceinline__ int operator()(int, int) const { return 0; }
 };
 
+// One warp tile's k-loop, specialised on its shape (MV x NV live 8x8
+// sub-tiles) so the unrolled loop is branch-free: no per-DMMA guards, loads
+// unconditional (rows past M point at row 0 and produce finite values the
+// epilogues discard), and the compiler can run the loads ahead of the DMMAs.
+template <int K, int N, int MV, int NV>
+__device__ __forceinline__ void tile_k(const double* __restrict__ a0p, const double* __restrict__ a1p,
+                                       const double* __restrict__ bp, double (&c)[2][2][2]) {
+#pragma unroll
+  for (int k = 0; k < K; k += 4) {
+    const double a0 = a0p[2 * k];
+    const double b0 = bp[k * N];
+    dmma884(c[0][0][0], c[0][0][1], a0, b0);
+    if (NV == 2) {
+      const double b1 = bp[k * N + 8];
+      dmma884(c[0][1][0], c[0][1][1], a0, b1);
+      if (MV == 2) {
+        const double a1 = a1p[2 * k];
+        dmma884(c[1][0][0], c[1][0][1], a1, b0);
+        dmma884(c[1][1][0], c[1][1][1], a1, b1);
+      }
+    } else if (MV == 2) {
+      const double a1 = a1p[2 * k];
+      dmma884(c[1][0][0], c[1][0][1], a1, b0);
+    }
+  }
+}
+
 template <int M, int N, int K, class RowPtr, class Epi, class Pre = NoPre>
 __device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ Bs, Epi epi, Pre pre = Pre()) {
   constexpr int MT8 = (M + 7) / 8, NT8 = N / 8;
@@ -87,34 +114,23 @@ __device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ 
     const auto p10 = pre(vm1 ? m0 + 8 : m0, n0);
     const auto p11 = pre(vm1 ? m0 + 8 : m0, vn1 ? n0 + 8 : n0);
     const int r0 = m0 + g, r1 = m0 + 8 + g;
-    const bool ok0 = r0 < M, ok1 = r1 < M;
-    const double* a0p = reinterpret_cast<const double*>(rowp(ok0 ? r0 >> 1 : 0)) + (r0 & 1) + 2 * tq;
-    const double* a1p = reinterpret_cast<const double*>(rowp(ok1 ? r1 >> 1 : 0)) + (r1 & 1) + 2 * tq;
+    const double* a0p = reinterpret_cast<const double*>(rowp(r0 < M ? r0 >> 1 : 0)) + (r0 < M ? r0 & 1 : 0) + 2 * tq;
+    const double* a1p = reinterpret_cast<const double*>(rowp(r1 < M ? r1 >> 1 : 0)) + (r1 < M ? r1 & 1 : 0) + 2 * tq;
     const double* bp = Bs + tq * N + n0 + g;
-    double c00a = 0, c00b = 0, c01a = 0, c01b = 0, c10a = 0, c10b = 0, c11a = 0, c11b = 0;
-#pragma unroll
-    for (int k = 0; k < K; k += 4) {
-      const double a0 = ok0 ? a0p[2 * k] : 0.0;
-      const double b0 = bp[k * N];
-      dmma884(c00a, c00b, a0, b0);
-      if (vn1) {
-        const double b1 = bp[k * N + 8];
-        dmma884(c01a, c01b, a0, b1);
-        if (vm1) {
-          const double a1 = ok1 ? a1p[2 * k] : 0.0;
-          dmma884(c10a, c10b, a1, b0);
-          dmma884(c11a, c11b, a1, b1);
-        }
-      } else if (vm1) {
-        const double a1 = ok1 ? a1p[2 * k] : 0.0;
-        dmma884(c10a, c10b, a1, b0);
-      }
-    }
-    epi(m0, n0, c00a, c00b, p00);
-    if (vn1) epi(m0, n0 + 8, c01a, c01b, p01);
+    double c[2][2][2] = {};
+    if (vm1 && vn1)
+      tile_k<K, N, 2, 2>(a0p, a1p, bp, c);
+    else if (vm1)
+      tile_k<K, N, 2, 1>(a0p, a1p, bp, c);
+    else if (vn1)
+      tile_k<K, N, 1, 2>(a0p, a1p, bp, c);
+    else
+      tile_k<K, N, 1, 1>(a0p, a1p, bp, c);
+    epi(m0, n0, c[0][0][0], c[0][0][1], p00);
+    if (vn1) epi(m0, n0 + 8, c[0][1][0], c[0][1][1], p01);
     if (vm1) {
-      epi(m0 + 8, n0, c10a, c10b, p10);
-      if (vn1) epi(m0 + 8, n0 + 8, c11a, c11b, p11);
+      epi(m0 + 8, n0, c[1][0][0], c[1][0][1], p10);
+      if (vn1) epi(m0 + 8, n0 + 8, c[1][1][0], c[1][1][1], p11);
     }
   }
 }
