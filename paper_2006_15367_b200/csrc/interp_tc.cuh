@@ -55,18 +55,20 @@ __device__ __forceinline__ void warp_gemm_rc(int M, int N, int K, RowPtr rowp, c
     const int m0 = (w / nt) << 4, n0 = (w % nt) << 4;
     double c[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
     const int r0 = m0 + g, r1 = m0 + 8 + g;
-    const bool ok0 = r0 < M, ok1 = r1 < M;
-    const double* a0p = reinterpret_cast<const double*>(rowp(ok0 ? r0 >> 1 : 0)) + (r0 & 1);
-    const double* a1p = reinterpret_cast<const double*>(rowp(ok1 ? r1 >> 1 : 0)) + (r1 & 1);
-    const bool bn1 = n0 + 8 < N;
+    // Unconditional loads: rows past M read row 0 and a missing second n8
+    // block re-reads the first (finite values in outputs the epilogue drops),
+    // so the k-loop has no predicated loads.
+    const double* a0p = reinterpret_cast<const double*>(rowp(r0 < M ? r0 >> 1 : 0)) + (r0 < M ? r0 & 1 : 0);
+    const double* a1p = reinterpret_cast<const double*>(rowp(r1 < M ? r1 >> 1 : 0)) + (r1 < M ? r1 & 1 : 0);
     const double* bp = B + tq * N + n0 + g;
-#pragma unroll 2
+    const double* bp1 = n0 + 8 < N ? bp + 8 : bp;
+#pragma unroll 4
     for (int k = 0; k < K; k += 4) {
       const int kk = k + tq;
-      const double a0 = ok0 ? a0p[2 * kk] : 0.0;
-      const double a1 = ok1 ? a1p[2 * kk] : 0.0;
+      const double a0 = a0p[2 * kk];
+      const double a1 = a1p[2 * kk];
       const double b0 = __ldg(bp + k * N);
-      const double b1 = bn1 ? __ldg(bp + k * N + 8) : 0.0;
+      const double b1 = __ldg(bp1 + k * N);
       dmma884(c[0][0][0], c[0][0][1], a0, b0);
       dmma884(c[0][1][0], c[0][1][1], a0, b1);
       dmma884(c[1][0][0], c[1][0][1], a1, b0);
@@ -80,25 +82,28 @@ __device__ __forceinline__ void warp_gemm_rc(int M, int N, int K, RowPtr rowp, c
   }
 }
 
-// x[row][kin] = i * (v . x[row][0:kin]) for `rows` complex rows (warp per row).
+// x[row][kin] = i * (v . x[row][0:kin]) for `rows` complex rows: four lanes
+// per row, eight rows per warp pass, two shuffle levels.
 template <class RowPtr>
 __device__ __forceinline__ void rank1_column(int rows, int kin, const double* __restrict__ v, RowPtr rowp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  for (int r = warp; r < rows; r += nwarp) {
+  const int sub = lane & 3;
+  const int rup = (rows + 7) & ~7;  // whole warps iterate together (shuffles)
+  for (int r = warp * 8 + (lane >> 2); r < rup; r += nwarp * 8) {
+    const bool live = r < rows;
     double sr = 0.0, si = 0.0;
-    double2* x = rowp(r);
-    for (int k = lane; k < kin; k += 32) {
+    double2* x = rowp(live ? r : 0);
+    for (int k = sub; k < kin; k += 4) {
       const double vk = __ldg(v + k);
       const double2 xv = x[k];
       sr = fma(vk, xv.x, sr);
       si = fma(vk, xv.y, si);
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      sr += __shfl_xor_sync(0xffffffffu, sr, off);
-      si += __shfl_xor_sync(0xffffffffu, si, off);
-    }
-    if (lane == 0) x[kin] = make_double2(-si, sr);
+    sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+    si += __shfl_xor_sync(0xffffffffu, si, 1);
+    sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+    si += __shfl_xor_sync(0xffffffffu, si, 2);
+    if (live && sub == 0) x[kin] = make_double2(-si, sr);
   }
 }
 
