@@ -505,9 +505,9 @@ template <int A, int B>
 bool try_l2l_ct(const CtLaunch& L, const double2* loc_p, double2* loc_c, const double* Bth, const double* vth,
                 const double* Bphi, const double* vphi, const double2* shift_dn) {
   using S = ct::Shape<A, B>;
-  // Fused L2L only where two CTAs fit per SM; otherwise the two-stage kernels
-  // (interp_big.cuh) are faster (measured: (26,34) 7.9 vs 9.9 ms, (34,52) 3.1 vs 2.9 ms).
-  if constexpr (S::L2L_CB > 0 && S::L2L_MINB == 2) {
+  // Measured against the two-stage kernels (interp_big.cuh) at config 2:
+  // (26,34) 7.9 vs 9.9 ms; (34,52) L2L phase 12.33 vs 12.74 ms; neutral on configs 1, 3-5.
+  if constexpr (S::L2L_CB > 0) {
     auto fn = k_l2l_ct<A, B>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, S::L2L_BYTES);
     const int grid = ct_grid<A, B>(L.n_par, S::L2L_BYTES, reinterpret_cast<const void*>(fn));
