@@ -459,11 +459,22 @@ void Engine::build_T() {
   ck(cudaGetLastError(), "k_tbuild");
 }
 
+namespace {
+// Quad-symmetric leaf kernels need an even, square grid with n/2 <= kQuadHalfMax.
+bool quad_ok(const DevLevel& d) {
+  return d.nt == d.np && d.nt % 2 == 0 && d.nt / 2 <= kQuadHalfMax && std::getenv("HFMM_NO_QUAD") == nullptr;
+}
+}  // namespace
+
 void Engine::phase_c2m() {
   const DevLevel& d = lv_[size_t(s_.L)];
   const int64_t nl = leaf_e_ - leaf_b_;
-  k_c2m<<<unsigned(nl), 128, 0, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.S,
-                                       s_.k, d.mp);
+  if (quad_ok(d))
+    k_c2m_quad<<<unsigned((nl + 3) / 4), 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,
+                                                         d.dir, d.nt, s_.k, d.mp);
+  else
+    k_c2m<<<unsigned(nl), 128, 0, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.S, s_.k,
+                                         d.mp);
   ++launches_;
   ck(cudaGetLastError(), "k_c2m");
 }
@@ -625,11 +636,19 @@ void Engine::phase_l2l() {
 void Engine::phase_l2t() {
   const DevLevel& d = lv_[size_t(s_.L)];
   const int64_t nl = leaf_e_ - leaf_b_;
-  const size_t smem = size_t(d.S) * (sizeof(double2) + 3 * sizeof(double));
-  if (smem > 48 * 1024)
-    ck(cudaFuncSetAttribute(k_l2t, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-  k_l2t<<<unsigned(nl), 128, smem, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.S,
-                                          s_.k, d.loc, d_pot);
+  if (quad_ok(d)) {
+    const size_t smem = 4 * size_t(d.S + kQuadP * (d.nt / 2)) * sizeof(double2);
+    if (smem > 48 * 1024)
+      ck(cudaFuncSetAttribute(k_l2t_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+    k_l2t_quad<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,
+                                                            d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+  } else {
+    const size_t smem = size_t(d.S) * (sizeof(double2) + 3 * sizeof(double));
+    if (smem > 48 * 1024)
+      ck(cudaFuncSetAttribute(k_l2t, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+    k_l2t<<<unsigned(nl), 128, smem, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.S,
+                                            s_.k, d.loc, d_pot);
+  }
   ++launches_;
   ck(cudaGetLastError(), "k_l2t");
 }

@@ -317,6 +317,188 @@ __global__ void k_l2l_phi(int n_c, int n_p, int64_t child_b, const double2* __re
 }
 
 // ---------------------------------------------------------------------------
+// Quad-symmetric C2M / L2T.  The sample grid (sphere_grid.cpp:25-50) is
+// symmetric: theta_{n-1-i} = pi - theta_i and phi_{j+n/2} = phi_j + pi, so the
+// four samples (i, j), (n-1-i, j), (i, j+n/2), (n-1-i, j+n/2) of a quad have
+// phases  A + B, A - B, -A + B, -A - B  with
+//   A = k sin(theta_i) (x cos(phi_j) + y sin(phi_j)),  B = k z cos(theta_i)
+// (A, B read from the direction table of sample (i, j)).  One sincos of A per
+// quad and one of B per theta pair and particle give all four exponentials
+// (a quarter of the direct sincos count); the phases equal the reference's
+// per-sample ones to rounding.  One warp per leaf.
+constexpr int kQuadHalfMax = 16;  // n/2 <= 16 (leaf grids of the BASELINE configs: n <= 26)
+constexpr int kQuadR = 3;         // quads per lane per pass (C2M)
+constexpr int kQuadP = 32;        // particles per B-table chunk
+
+// exp(i(A+B)), exp(i(A-B)); the other two are their conjugates.
+__device__ __forceinline__ void quad_exp(double ca, double sa, double2 eb, double2& e1, double2& e2) {
+  const double P = ca * eb.x, Q = sa * eb.y, R = sa * eb.x, T = ca * eb.y;
+  e1 = make_double2(P - Q, R + T);
+  e2 = make_double2(P + Q, R - T);
+}
+
+__global__ void __launch_bounds__(128) k_c2m_quad(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
+                                                  const double* __restrict__ x, const double* __restrict__ y,
+                                                  const double* __restrict__ z, const double2* __restrict__ q,
+                                                  const double* __restrict__ centers, const double* __restrict__ dir,
+                                                  int n, double k, double2* __restrict__ mp) {
+  __shared__ double2 sB[4][kQuadP][kQuadHalfMax];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
+  if (li >= nl) return;  // whole warp
+  const int64_t leaf = leaf_b + li;
+  const int half = n / 2, quads = half * half, nphi = n;
+  const int64_t S = int64_t(n) * n;
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  double2 (*B)[kQuadHalfMax] = sB[warp];
+  for (int qc = 0; qc < quads; qc += 32 * kQuadR) {
+    double ax[kQuadR], ay[kQuadR];
+    int qi[kQuadR];
+    double2 acc[kQuadR][4];
+#pragma unroll
+    for (int r = 0; r < kQuadR; ++r) {
+      const int qd = qc + lane + 32 * r;
+      const int i = qd < quads ? qd / half : 0, j = qd < quads ? qd - (qd / half) * half : 0;
+      qi[r] = i;
+      const int64_t s1 = int64_t(i) * nphi + j;
+      ax[r] = k * dir[3 * s1];
+      ay[r] = k * dir[3 * s1 + 1];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[r][u] = make_double2(0.0, 0.0);
+    }
+    for (int64_t pc = p0; pc < p1; pc += kQuadP) {
+      const int np = int(p1 - pc < kQuadP ? p1 - pc : kQuadP);
+      __syncwarp();
+      for (int t = lane; t < np * half; t += 32) {  // B table: exp(i k z cos(theta_i))
+        const int pp = t / half, i = t - pp * half;
+        double sn, cs;
+        sincos_fast(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), &sn, &cs);
+        B[pp][i] = make_double2(cs, sn);
+      }
+      __syncwarp();
+      for (int pp = 0; pp < np; ++pp) {
+        const double rx = x[pc + pp] - cx, ry = y[pc + pp] - cy;
+        const double2 qq = q[pc + pp];
+#pragma unroll
+        for (int r = 0; r < kQuadR; ++r) {
+          double sa, ca;
+          sincos_fast(fma(ax[r], rx, ay[r] * ry), &sa, &ca);
+          double2 e1, e2;
+          quad_exp(ca, sa, B[pp][qi[r]], e1, e2);
+          // q * e (samples 1, 2) and q * conj(e) (samples 4, 3)
+          acc[r][0].x = fma(qq.x, e1.x, fma(-qq.y, e1.y, acc[r][0].x));
+          acc[r][0].y = fma(qq.x, e1.y, fma(qq.y, e1.x, acc[r][0].y));
+          acc[r][3].x = fma(qq.x, e1.x, fma(qq.y, e1.y, acc[r][3].x));
+          acc[r][3].y = fma(-qq.x, e1.y, fma(qq.y, e1.x, acc[r][3].y));
+          acc[r][1].x = fma(qq.x, e2.x, fma(-qq.y, e2.y, acc[r][1].x));
+          acc[r][1].y = fma(qq.x, e2.y, fma(qq.y, e2.x, acc[r][1].y));
+          acc[r][2].x = fma(qq.x, e2.x, fma(qq.y, e2.y, acc[r][2].x));
+          acc[r][2].y = fma(-qq.x, e2.y, fma(qq.y, e2.x, acc[r][2].y));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kQuadR; ++r) {
+      const int qd = qc + lane + 32 * r;
+      if (qd < quads) {
+        const int i = qd / half, j = qd - i * half;
+        double2* m = mp + leaf * S;
+        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
+        m[s1] = acc[r][0];             // A + B
+        m[s2] = acc[r][1];             // A - B   (pi - theta)
+        m[s1 + half] = acc[r][2];      // -A + B  (phi + pi)
+        m[s2 + half] = acc[r][3];      // -A - B
+      }
+    }
+  }
+}
+
+// L2T: potentials of a leaf's observers from its local samples, weighted
+// w_s L_s staged per warp in shared memory; lanes over quads, kQuadOB
+// observers per pass (the four samples of a quad are loaded once for all of
+// them and their sincos chains interleave), one shuffle reduction each.
+constexpr int kQuadOB = 4;
+__global__ void __launch_bounds__(128) k_l2t_quad(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
+                                                  const double* __restrict__ x, const double* __restrict__ y,
+                                                  const double* __restrict__ z, const double* __restrict__ centers,
+                                                  const double* __restrict__ dir, const double* __restrict__ wq,
+                                                  int n, double k, const double2* __restrict__ loc,
+                                                  double2* __restrict__ pot) {
+  extern __shared__ double2 qsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = n / 2, quads = half * half, nphi = n;
+  const int64_t S = int64_t(n) * n;
+  double2* Lw = qsm + warp * (S + kQuadP * half);  // w_s L_s, then the B table
+  double2* Bt = Lw + S;
+  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
+  if (li >= nl) return;
+  const int64_t leaf = leaf_b + li;
+  for (int64_t s = lane; s < S; s += 32) {
+    const double2 v = loc[leaf * S + s];
+    const double w = wq[s];
+    Lw[s] = make_double2(w * v.x, w * v.y);
+  }
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
+  for (int64_t pc = p0; pc < p1; pc += kQuadP) {
+    const int np = int(p1 - pc < kQuadP ? p1 - pc : kQuadP);
+    __syncwarp();
+    for (int t = lane; t < np * half; t += 32) {  // exp(i k z cos(theta_i)) (conjugated below)
+      const int pp = t / half, i = t - pp * half;
+      double sn, cs;
+      sincos_fast(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), &sn, &cs);
+      Bt[pp * half + i] = make_double2(cs, sn);
+    }
+    __syncwarp();
+    for (int pb = 0; pb < np; pb += kQuadOB) {
+      double rx[kQuadOB], ry[kQuadOB], ar[kQuadOB], ai[kQuadOB];
+#pragma unroll
+      for (int o = 0; o < kQuadOB; ++o) {
+        const int pp = pb + o < np ? pb + o : pb;  // idle slots repeat a live observer
+        rx[o] = k * (x[pc + pp] - cx);
+        ry[o] = k * (y[pc + pp] - cy);
+        ar[o] = 0.0;
+        ai[o] = 0.0;
+      }
+      for (int qd = lane; qd < quads; qd += 32) {
+        const int i = qd / half, j = qd - i * half;
+        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
+        const double dxs = dir[3 * s1], dys = dir[3 * s1 + 1];
+        const double2 l1 = Lw[s1], l2 = Lw[s2], l3 = Lw[s1 + half], l4 = Lw[s2 + half];
+#pragma unroll
+        for (int o = 0; o < kQuadOB; ++o) {
+          const int pp = pb + o < np ? pb + o : pb;
+          double sa, ca;
+          sincos_fast(fma(dxs, rx[o], dys * ry[o]), &sa, &ca);
+          double2 e1, e2;
+          quad_exp(ca, sa, Bt[pp * half + i], e1, e2);
+          // sum_s Lw_s exp(-i phase_s): conj(e1) at s1, conj(e2) at s2, e2 at s1 + half, e1 at s2 + half
+          ar[o] = fma(l1.x, e1.x, fma(l1.y, e1.y, ar[o]));
+          ai[o] = fma(l1.y, e1.x, fma(-l1.x, e1.y, ai[o]));
+          ar[o] = fma(l2.x, e2.x, fma(l2.y, e2.y, ar[o]));
+          ai[o] = fma(l2.y, e2.x, fma(-l2.x, e2.y, ai[o]));
+          ar[o] = fma(l3.x, e2.x, fma(-l3.y, e2.y, ar[o]));
+          ai[o] = fma(l3.y, e2.x, fma(l3.x, e2.y, ai[o]));
+          ar[o] = fma(l4.x, e1.x, fma(-l4.y, e1.y, ar[o]));
+          ai[o] = fma(l4.y, e1.x, fma(l4.x, e1.y, ai[o]));
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < kQuadOB; ++o) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          ar[o] += __shfl_xor_sync(0xffffffffu, ar[o], off);
+          ai[o] += __shfl_xor_sync(0xffffffffu, ai[o], off);
+        }
+        if (lane == 0 && pb + o < np) pot[pc + pb + o] = make_double2(-c * ai[o], c * ar[o]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // L2T (operators.cpp:89-108, driver traversal.cpp:717-728): one CTA per leaf,
 // one warp per observer, lanes over samples, warp-shuffle reduction.
 __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __restrict__ leaf_start,
