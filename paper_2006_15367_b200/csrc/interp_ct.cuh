@@ -28,13 +28,17 @@ struct Shape {
   // L2L passes
   static constexpr int DTH_K = round4(2 * NP + 1), DTH_N = round8(2 * NC), DTH_LDA = lda_for(DTH_K);
   static constexpr int DPHI_K = round4(NP + 1), DPHI_N = round8(NC), DPHI_LDA = lda_for(DPHI_K);
+  // B row strides: a multiple of 16 doubles puts the four k-rows of a DMMA
+  // B fragment on the same 8 banks, so pad those by 8 (two wavefronts, ideal)
+  static constexpr int ldb(int n) { return n % 16 == 0 ? n + 8 : n; }
+  static constexpr int UPHI_LDB = ldb(UPHI_N), UTH_LDB = ldb(UTH_N), DTH_LDB = ldb(DTH_N), DPHI_LDB = ldb(DPHI_N);
   // shared-memory footprints in bytes
   static constexpr int m2m_bytes(int cb, int db) {
     return ((db ? 2 : 1) * cb * NC * UPHI_LDA + cb * HALF * UTH_LDA + SP) * 16 +
-           (UPHI_K * UPHI_N + UTH_K * UTH_N) * 8;
+           (UPHI_K * UPHI_LDB + UTH_K * UTH_LDB) * 8;
   }
   static constexpr int l2l_bytes(int cb, int db) {
-    return ((db ? SP : 0) + cb * HALF * DTH_LDA + cb * NC * DPHI_LDA) * 16 + (DTH_K * DTH_N + DPHI_K * DPHI_N) * 8;
+    return ((db ? SP : 0) + cb * HALF * DTH_LDA + cb * NC * DPHI_LDA) * 16 + (DTH_K * DTH_LDB + DPHI_K * DPHI_LDB) * 8;
   }
   // plan: children per batch and buffering, two CTAs/SM if possible
   static constexpr int kBudget2 = 113 * 1024, kBudget1 = 227 * 1024;
@@ -82,7 +86,7 @@ __device__ __forceinline__ void tile_k(const double* __restrict__ a0p, const dou
 #pragma unroll
   for (int k = 0; k < K; k += 4) {
     const double a0 = a0p[2 * k];
-    const double b0 = bp[k * N];
+    const double b0 = bp[k * N];  // N = B row stride here
     dmma884(c[0][0][0], c[0][0][1], a0, b0);
     if (NV == 2) {
       const double b1 = bp[k * N + 8];
@@ -99,7 +103,7 @@ __device__ __forceinline__ void tile_k(const double* __restrict__ a0p, const dou
   }
 }
 
-template <int M, int N, int K, class RowPtr, class Epi, class Pre = NoPre>
+template <int M, int N, int K, int LDB = N, class RowPtr, class Epi, class Pre = NoPre>
 __device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ Bs, Epi epi, Pre pre = Pre()) {
   constexpr int MT8 = (M + 7) / 8, NT8 = N / 8;
   constexpr int MT = (MT8 + 1) / 2, NT = (NT8 + 1) / 2;
@@ -116,16 +120,16 @@ __device__ __forceinline__ void gemm_ct(RowPtr rowp, const double* __restrict__ 
     const int r0 = m0 + g, r1 = m0 + 8 + g;
     const double* a0p = reinterpret_cast<const double*>(rowp(r0 < M ? r0 >> 1 : 0)) + (r0 < M ? r0 & 1 : 0) + 2 * tq;
     const double* a1p = reinterpret_cast<const double*>(rowp(r1 < M ? r1 >> 1 : 0)) + (r1 < M ? r1 & 1 : 0) + 2 * tq;
-    const double* bp = Bs + tq * N + n0 + g;
+    const double* bp = Bs + tq * LDB + n0 + g;
     double c[2][2][2] = {};
     if (vm1 && vn1)
-      tile_k<K, N, 2, 2>(a0p, a1p, bp, c);
+      tile_k<K, LDB, 2, 2>(a0p, a1p, bp, c);
     else if (vm1)
-      tile_k<K, N, 2, 1>(a0p, a1p, bp, c);
+      tile_k<K, LDB, 2, 1>(a0p, a1p, bp, c);
     else if (vn1)
-      tile_k<K, N, 1, 2>(a0p, a1p, bp, c);
+      tile_k<K, LDB, 1, 2>(a0p, a1p, bp, c);
     else
-      tile_k<K, N, 1, 1>(a0p, a1p, bp, c);
+      tile_k<K, LDB, 1, 1>(a0p, a1p, bp, c);
     epi(m0, n0, c[0][0][0], c[0][0][1], p00);
     if (vn1) epi(m0, n0 + 8, c[0][1][0], c[0][1][1], p01);
     if (vm1) {
@@ -162,6 +166,15 @@ __device__ __forceinline__ void rank1_ct(double2* X, const double* __restrict__ 
   }
 }
 
+// K x N row-major (global) -> rows of stride ldb (shared), cp.async 16 B.
+__device__ __forceinline__ void stage_rows(double* dst, const double* __restrict__ src, int K, int N, int ldb) {
+  const int h = N / 2;  // N even
+  for (int t = threadIdx.x; t < K * h; t += kThreads) {
+    const int r = t / h, c = 2 * (t - r * h);
+    cp_async16(dst + r * ldb + c, src + r * N + c, true);
+  }
+}
+
 __device__ __forceinline__ void stage_doubles(double* dst, const double* __restrict__ src, int n) {
   for (int t = threadIdx.x * 2; t < n; t += kThreads * 2) {
     if (t + 1 < n)
@@ -192,11 +205,11 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::M2M_MINB)) k
   double2* Fs = sm + (DB ? 2 : 1) * XSZ;
   double2* Sacc = Fs + CB * HALF * S::UTH_LDA;
   double* Bphi = reinterpret_cast<double*>(Sacc + SP);
-  double* Bth = Bphi + S::UPHI_K * S::UPHI_N;
+  double* Bth = Bphi + S::UPHI_K * S::UPHI_LDB;
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
 
-  ct::stage_doubles(Bphi, RphiT, S::UPHI_K * S::UPHI_N);
-  ct::stage_doubles(Bth, RthT, S::UTH_K * S::UTH_N);
+  ct::stage_rows(Bphi, RphiT, S::UPHI_K, S::UPHI_N, S::UPHI_LDB);
+  ct::stage_rows(Bth, RthT, S::UTH_K, S::UTH_N, S::UTH_LDB);
   cp_async_commit();
   for (int t = threadIdx.x; t < CB * HALF * S::UTH_LDA; t += ct::kThreads) Fs[t] = make_double2(0.0, 0.0);
   for (int t = threadIdx.x; t < SP; t += ct::kThreads) Sacc[t] = make_double2(0.0, 0.0);
@@ -238,7 +251,7 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::M2M_MINB)) k
     ct::rank1_ct<CB * NC, NC, S::UPHI_LDA>(X, vphi);
     __syncthreads();
     // phi pass -> folded circles
-    ct::gemm_ct<CB * NC * 2, S::UPHI_N, S::UPHI_K>(
+    ct::gemm_ct<CB * NC * 2, S::UPHI_N, S::UPHI_K, S::UPHI_LDB>(
         [&](int r) { return X + r * S::UPHI_LDA; }, Bphi, [&](int m0, int n0, double v0, double v1, int) {
           const int r = m0 + g, ci = r >> 1, c = ci / NC, i = ci - c * NC;
           if (c >= CB) return;
@@ -261,7 +274,7 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::M2M_MINB)) k
 #pragma unroll
     for (int c = 0; c < CB; ++c) octs[c] = c < nb ? oct_c[children[b0 + c]] : 0;
     // theta pass, rows (circle, child, re/im); children reduce in-warp
-    ct::gemm_ct<HALF * R2, S::UTH_N, S::UTH_K>(
+    ct::gemm_ct<HALF * R2, S::UTH_N, S::UTH_K, S::UTH_LDB>(
         [&](int row) {
           const int p = row / CB, c = row - p * CB;
           return Fs + (c * HALF + p) * S::UTH_LDA;
@@ -347,13 +360,13 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::L2L_MINB)) k
   double2* Fs = DB ? sm + SP : sm;
   double2* Ns = Fs + CB * HALF * S::DTH_LDA;
   double* Bth = reinterpret_cast<double*>(Ns + CB * NC * S::DPHI_LDA);
-  double* Bphi = Bth + S::DTH_K * S::DTH_N;
+  double* Bphi = Bth + S::DTH_K * S::DTH_LDB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   double* lc = reinterpret_cast<double*>(loc_c);
 
-  ct::stage_doubles(Bth, RthT, S::DTH_K * S::DTH_N);
-  ct::stage_doubles(Bphi, RphiT, S::DPHI_K * S::DPHI_N);
+  ct::stage_rows(Bth, RthT, S::DTH_K, S::DTH_N, S::DTH_LDB);
+  ct::stage_rows(Bphi, RphiT, S::DPHI_K, S::DPHI_N, S::DPHI_LDB);
   cp_async_commit();
   for (int t = threadIdx.x; t < CB * HALF * S::DTH_LDA; t += ct::kThreads) Fs[t] = make_double2(0.0, 0.0);
   for (int t = threadIdx.x; t < CB * NC * S::DPHI_LDA; t += ct::kThreads) Ns[t] = make_double2(0.0, 0.0);
@@ -409,7 +422,7 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::L2L_MINB)) k
       __syncthreads();
       ct::rank1_ct<CB * HALF, 2 * NP, S::DTH_LDA>(Fs, vth);
       __syncthreads();
-      ct::gemm_ct<CB * HALF * 2, S::DTH_N, S::DTH_K>(
+      ct::gemm_ct<CB * HALF * 2, S::DTH_N, S::DTH_K, S::DTH_LDB>(
           [&](int r) { return Fs + r * S::DTH_LDA; }, Bth, [&](int m0, int n0, double v0, double v1, int) {
             const int r = m0 + g, ci = r >> 1, c = ci / HALF, p = ci - c * HALF;
             if (c >= CB) return;
@@ -427,7 +440,7 @@ __global__ void __launch_bounds__(ct::kThreads, (ct::Shape<NC, NP>::L2L_MINB)) k
       __syncthreads();
       ct::rank1_ct<CB * NC, NP, S::DPHI_LDA>(Ns, vphi);
       __syncthreads();
-      ct::gemm_ct<CB * NC * 2, S::DPHI_N, S::DPHI_K>(
+      ct::gemm_ct<CB * NC * 2, S::DPHI_N, S::DPHI_K, S::DPHI_LDB>(
           [&](int r) { return Ns + r * S::DPHI_LDA; }, Bphi,
           [&](int m0, int n0, double v0, double v1, const ct::D2& old) {
             const int r = m0 + g, ci = r >> 1, c = ci / NC, row = ci - c * NC;
