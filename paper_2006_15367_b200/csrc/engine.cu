@@ -11,6 +11,7 @@
 #include "interp.hpp"
 #include "kernels.cuh"
 #include "m2l.cuh"
+#include "m2l_tc.cuh"
 #include "interp_tc.cuh"
 #include "interp_ct.cuh"
 #include "interp_big.cuh"
@@ -553,14 +554,19 @@ void Engine::phase_m2m() {
 }
 
 void Engine::phase_m2l() {
+  const bool dmma = std::getenv("HFMM_M2L_DFMA") == nullptr;  // debugging aid: the DFMA stencil
   ck(cudaFuncSetAttribute(k_m2l_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
+  ck(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
   for (int l = s_.top; l <= s_.L; ++l) {
     DevLevel& d = lv_[size_t(l)];
     if (d.dense) {
       const int nb = (d.G + m2l::MB - 1) / m2l::MB;
       const int ppc = m2l_pairs_per_cta(nb * nb * nb, d.S, sms_);
       dim3 grid(unsigned(nb * nb * nb), unsigned((d.S / 2 + ppc - 1) / ppc));
-      k_m2l_dense<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, d.lookup, d.T, d.mp, d.loc);
+      if (dmma)
+        k_m2l_dmma<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, d.lookup, d.T, d.mp, d.loc);
+      else
+        k_m2l_dense<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, d.lookup, d.T, d.mp, d.loc);
     } else {
       dim3 grid(unsigned(d.n_nodes), unsigned((d.S + 127) / 128));
       k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, d.far_off, d.far, d.T, d.mp, d.loc);
