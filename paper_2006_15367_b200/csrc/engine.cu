@@ -12,6 +12,7 @@
 #include "kernels.cuh"
 #include "m2l.cuh"
 #include "m2l_tc.cuh"
+#include "interp_rb.cuh"
 #include "interp_tc.cuh"
 #include "interp_ct.cuh"
 #include "interp_big.cuh"
@@ -62,7 +63,8 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   dist_ = s.P > 1;
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
-  use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;  // debugging aid: runtime-shaped kernels only
+  use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;
+  use_rb_ = std::getenv("HFMM_NO_RB") == nullptr;  // debugging aid: compile-time fused kernels instead  // debugging aid: runtime-shaped kernels only
   // debugging aid: large-level path 0 = two-stage (default), 1 = fused runtime, 2 = legacy two-pass
   if (const char* p = std::getenv("HFMM_BIG_PATH")) path_ = std::atoi(p);
   l2l_ct_ = std::getenv("HFMM_L2L_BIG") == nullptr;  // debugging aid: two-stage L2L everywhere
@@ -429,6 +431,8 @@ void Engine::upload() {
     P.shift_dn = upload_vec(dn);
     setup_fused(P, C, tp, tc);
     tmp = std::max(tmp, size_t(C.n_nodes) * size_t(nc) * size_t(np));
+    tmp = std::max(tmp, rb_m2m_scratch(C.n_nodes, nc, np));
+    tmp = std::max(tmp, rb_l2l_scratch(C.n_nodes, nc, np));
   }
   tmp_elems_ = std::max(tmp, tmp_need_);
   d_tmp = alloc<double2>(tmp_elems_);
@@ -499,6 +503,15 @@ void Engine::phase_m2m() {
     const CtLaunch cl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
                       R ? R->children : P.children, oct_[size_t(l + 1)], st_};
     if (cl.n_par == 0) continue;
+    if (use_rb_ && rb_pair(nc, np)) {
+      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_};
+      if (launch_m2m_rb(nc, np, rl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up, d_tmp)) {
+        launches_ += 2;
+        ck(cudaGetLastError(), "k_m2m_rb");
+        continue;
+      }
+    }
     if (use_ct_ && launch_m2m_ct(nc, np, cl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v,
                                  P.shift_up)) {
       ++launches_;
@@ -840,6 +853,7 @@ void Engine::upload_rank_plan() {
     R.plist = upload_vec(rp.held[size_t(l)]);
     R.child_off = upload_vec(rp.child_off[size_t(l)]);
     R.children = upload_vec(rp.children[size_t(l)]);
+    R.n_children = int64_t(rp.children[size_t(l)].size());
   }
   held_.assign(size_t(L + 1), nullptr);
   held_cnt_.assign(size_t(L + 1), 0);

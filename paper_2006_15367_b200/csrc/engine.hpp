@@ -70,6 +70,7 @@ struct RankLevel {
   int* plist = nullptr;      // held parents (global node indices)
   int* child_off = nullptr;  // CSR over plist
   int* children = nullptr;   // held children (global indices at level + 1)
+  int64_t n_children = 0;    // entries of children
 };
 
 // Static exchange plan with one peer (distributed mode).
@@ -146,6 +147,7 @@ class Engine {
   int64_t launches_ = 0;
   bool use_ct_ = true;
   bool l2l_ct_ = true;
+  bool use_rb_ = true;
   int big_threads_ = 256;  // block size of the two-stage large-grid kernels
   int path_ = 0;           // large-level M2M/L2L path (see constructor)
   size_t tmp_need_ = 0;    // temp elements required by the large-level kernels

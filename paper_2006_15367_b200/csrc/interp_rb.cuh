@@ -1,0 +1,284 @@
+// Streaming M2M / L2L on DMMA with complex-row warp tiles.
+//
+// Same algorithm as interp_ct.cuh (real matrix + rank-1 imaginary part of
+// resample_circle, sphere_grid.cpp:128-155; M2M = phi pass, fold, theta pass,
+// shift, child sum, traversal.cpp:322-429; L2L mirrored, :583-707), organised
+// for throughput:
+//  * a warp tile is 8 COMPLEX rows x N: two m8 DMMA fragments (real parts,
+//    imaginary parts) that share every B fragment, so a lane holds both parts
+//    of its row -- the rank-1 column i (v . x) needs no partner shuffle and the
+//    epilogue sees complex values;
+//  * B (the level's real interpolation matrix) is staged once per persistent
+//    CTA in shared memory; A rows stream from global memory / L1 straight
+//    into registers; there are no barriers after the B staging;
+//  * the two passes are two kernels with the intermediate in HBM scratch
+//    (M2M: folded circles F; L2L: narrow rows Nb);
+//  * the M2M theta pass puts the 8 child slots of a parent in the 8 rows of a
+//    tile, so the child sum is a 3-level shuffle and every parent sample is
+//    written exactly once (no shared accumulator).
+#ifndef HFMM_B200_INTERP_RB_CUH
+#define HFMM_B200_INTERP_RB_CUH
+
+#include "interp_tc.cuh"
+
+namespace hfmm_b200 {
+namespace rb {
+
+__host__ __device__ constexpr int r4(int v) { return (v + 3) / 4 * 4; }
+__host__ __device__ constexpr int r8(int v) { return (v + 7) / 8 * 8; }
+__host__ __device__ constexpr int ldb(int n) { return n % 16 == 0 ? n + 8 : n; }  // bank-conflict-free B fragments
+constexpr int kThreads = 256;
+
+// K x N row-major B (global) -> shared rows of stride LDB (persistent CTA, once).
+template <int K, int N, int LDB>
+__device__ __forceinline__ void stage_b(double* dst, const double* __restrict__ src) {
+  for (int t = threadIdx.x; t < K * N / 2; t += blockDim.x) {
+    const int r = t / (N / 2), c = 2 * (t - r * (N / 2));
+    cp_async16(dst + r * LDB + c, src + r * N + c, true);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+}
+
+// Rank-1 column: lane (g, tq) holds x_re / x_im of row g at columns 4 kk + tq
+// (zeros past KIN); inject i (v . x) at column KIN.
+template <int KS, int KIN>
+__device__ __forceinline__ void rank1_inject(double (&are)[KS], double (&aim)[KS], const double* __restrict__ v) {
+  const int tq = threadIdx.x & 3;
+  double sr = 0.0, si = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int k = 4 * kk + tq;
+    if (k < KIN) {
+      const double vk = __ldg(v + k);
+      sr = fma(vk, are[kk], sr);
+      si = fma(vk, aim[kk], si);
+    }
+  }
+  sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+  si += __shfl_xor_sync(0xffffffffu, si, 1);
+  sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+  si += __shfl_xor_sync(0xffffffffu, si, 2);
+  constexpr int KR = KIN / 4, TR = KIN % 4;
+  if (tq == TR) {
+    are[KR] = -si;  // Re(i alpha)
+    aim[KR] = sr;   // Im(i alpha)
+  }
+}
+
+// C (8 complex rows x NT n8 tiles) += A (8 x K) B (K x 8 NT): 2 NT DMMA per k-step.
+template <int KS, int NT, int LDB>
+__device__ __forceinline__ void tile_mma(const double (&are)[KS], const double (&aim)[KS], const double* __restrict__ Bs,
+                                         double (&cre)[NT][2], double (&cim)[NT][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const double* bp = Bs + tq * LDB + g;
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const double b = bp[4 * kk * LDB + 8 * j];
+      dmma884(cre[j][0], cre[j][1], are[kk], b);
+      dmma884(cim[j][0], cim[j][1], aim[kk], b);
+    }
+}
+
+template <int NC, int NP>
+struct Dims {
+  static constexpr int HALF = NP / 2, SC = NC * NC, SP = NP * NP;
+  // M2M phi: X (NC x NC) rows -> NP outputs; theta: folded circles 2NC -> 2NP
+  static constexpr int UPHI_K = r4(NC + 1), UPHI_N = r8(NP), UPHI_LDB = ldb(UPHI_N);
+  static constexpr int UTH_K = r4(2 * NC + 1), UTH_N = r8(2 * NP), UTH_LDB = ldb(UTH_N);
+  static constexpr int LDF = UTH_K;  // F scratch row stride (complex): the theta pass's K
+  // L2L theta: 2NP -> 2NC; phi: NP -> NC
+  static constexpr int DTH_K = r4(2 * NP + 1), DTH_N = r8(2 * NC), DTH_LDB = ldb(DTH_N);
+  static constexpr int DPHI_K = r4(NP + 1), DPHI_N = r8(NC), DPHI_LDB = ldb(DPHI_N);
+  static constexpr int LDN = DPHI_K;  // Nb scratch row stride (complex): the phi pass's K
+};
+
+}  // namespace rb
+
+// ---------------------------------------------------------------------------
+// M2M stage 1: phi pass of every child row -> folded circles F[j][p][ii]
+// (j = position in the children array, ii < 2 NC; columns >= 2 NC unused).
+template <int NC, int NP>
+__global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_phi_rb(int64_t nch, const int* __restrict__ children,
+                                                                const double2* __restrict__ mp_c,
+                                                                const double* __restrict__ B,
+                                                                const double* __restrict__ v,
+                                                                double2* __restrict__ F) {
+  using D = rb::Dims<NC, NP>;
+  constexpr int KS = D::UPHI_K / 4, NT = D::UPHI_N / 8, HALF = D::HALF;
+  __shared__ __align__(16) double Bs[D::UPHI_K * D::UPHI_LDB];
+  rb::stage_b<D::UPHI_K, D::UPHI_N, D::UPHI_LDB>(Bs, B);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t rows = nch * NC, tiles = (rows + 7) / 8;
+  for (int64_t t = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; t < tiles;
+       t += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int64_t R = t * 8 + g;
+    const bool ok = R < rows;
+    const int64_t j = ok ? R / NC : 0;
+    const int i = ok ? int(R - j * NC) : 0;
+    const int64_t node = children ? children[j] : j;
+    const double2* x = mp_c + node * D::SC + i * NC;
+    double are[KS], aim[KS];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      const int k = 4 * kk + tq;
+      const double2 xv = (ok && k < NC) ? __ldg(x + k) : make_double2(0.0, 0.0);
+      are[kk] = xv.x;
+      aim[kk] = xv.y;
+    }
+    rb::rank1_inject<KS, NC>(are, aim, v);
+    double cre[NT][2] = {}, cim[NT][2] = {};
+    rb::tile_mma<KS, NT, D::UPHI_LDB>(are, aim, Bs, cre, cim);
+    if (ok) {
+      double2* Fj = F + j * HALF * D::LDF;
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = 8 * jn + 2 * tq + q;
+          if (n < NP) {
+            const int p = n < HALF ? n : n - HALF;
+            const int ii = n < HALF ? i : 2 * NC - 1 - i;
+            Fj[p * D::LDF + ii] = make_double2(cre[jn][q], cim[jn][q]);
+          }
+        }
+    }
+  }
+}
+
+// M2M stage 2: theta pass + shift + child sum.  Work item = (parent, circle p);
+// tile rows = the parent's 8 child slots (absent children read as zero).
+template <int NC, int NP>
+__global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, const int* __restrict__ plist,
+                                                                  const int* __restrict__ child_off,
+                                                                  const int* __restrict__ children,
+                                                                  const uint8_t* __restrict__ oct_c,
+                                                                  const double2* __restrict__ F,
+                                                                  const double* __restrict__ B,
+                                                                  const double* __restrict__ v,
+                                                                  const double2* __restrict__ shift_up,
+                                                                  double2* __restrict__ mp_p) {
+  using D = rb::Dims<NC, NP>;
+  constexpr int KS = D::UTH_K / 4, NT = D::UTH_N / 8, HALF = D::HALF, SP = D::SP;
+  extern __shared__ __align__(16) double Bsm[];
+  rb::stage_b<D::UTH_K, D::UTH_N, D::UTH_LDB>(Bsm, B);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t items = int64_t(n_par) * HALF;
+  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
+       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int par = int(it / HALF), p = int(it - int64_t(par) * HALF);
+    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const bool ok = g < nchp;
+    const double2* frow = F + (int64_t(cb + (ok ? g : 0)) * HALF + p) * D::LDF;
+    const double2* sh = shift_up + int64_t(ok ? oct_c[children[cb + g]] : 0) * SP;
+    double are[KS], aim[KS];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      const int k = 4 * kk + tq;
+      const double2 fv = (ok && k < 2 * NC) ? __ldg(frow + k) : make_double2(0.0, 0.0);
+      are[kk] = fv.x;
+      aim[kk] = fv.y;
+    }
+    rb::rank1_inject<KS, 2 * NC>(are, aim, v);
+    double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
+    // N in chunks of NTC n8 tiles (A stays in registers): shift factors of the
+    // chunk's outputs are loaded ahead of its DMMAs.
+    constexpr int NTC = 3;
+#pragma unroll
+    for (int j0 = 0; j0 < NT; j0 += NTC) {
+      double2 shv[NTC][2];
+#pragma unroll
+      for (int jc = 0; jc < NTC; ++jc)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = 8 * (j0 + jc) + 2 * tq + q;
+          const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
+          shv[jc][q] = (ok && j0 + jc < NT && n < 2 * NP) ? __ldg(sh + s) : make_double2(0.0, 0.0);
+        }
+      double cre[NTC][2] = {}, cim[NTC][2] = {};
+      const double* bp = Bsm + tq * D::UTH_LDB + g + 8 * j0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int jc = 0; jc < NTC; ++jc)
+          if (j0 + jc < NT) {
+            const double b = bp[4 * kk * D::UTH_LDB + 8 * jc];
+            dmma884(cre[jc][0], cre[jc][1], are[kk], b);
+            dmma884(cim[jc][0], cim[jc][1], aim[kk], b);
+          }
+#pragma unroll
+      for (int jc = 0; jc < NTC; ++jc)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (j0 + jc >= NT) continue;
+          const double2 f = shv[jc][q];
+          double vr = cre[jc][q] * f.x - cim[jc][q] * f.y;
+          double vi = cre[jc][q] * f.y + cim[jc][q] * f.x;
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {  // sum over the 8 child slots (g)
+            vr += __shfl_xor_sync(0xffffffffu, vr, off);
+            vi += __shfl_xor_sync(0xffffffffu, vi, off);
+          }
+          const int n = 8 * (j0 + jc) + 2 * tq + q;
+          if (g == 0 && n < 2 * NP) {
+            const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
+            out[s] = make_double2(vr, vi);
+          }
+        }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dispatch over the level pairs with a theta-pass K <= 72 (register budget).
+#define HFMM_RB_PAIRS(X) X(18, 28) X(28, 42) X(22, 30) X(30, 44) X(26, 34) X(34, 52)
+
+inline bool rb_pair(int nc, int np) {
+#define HFMM_RB_HAS(A, B) if (nc == A && np == B) return true;
+  HFMM_RB_PAIRS(HFMM_RB_HAS)
+#undef HFMM_RB_HAS
+  return false;
+}
+// complex elements of the M2M F scratch / L2L Nb scratch for nch children
+inline size_t rb_m2m_scratch(int64_t nch, int nc, int np) { return size_t(nch) * size_t(np / 2) * size_t(rb::r4(2 * nc + 1)); }
+inline size_t rb_l2l_scratch(int64_t nch, int nc, int np) { return size_t(nch) * size_t(nc) * size_t(rb::r4(np + 1)); }
+
+struct RbLaunch {
+  int n_par;
+  const int* plist;
+  const int* child_off;  // device CSR over parents
+  const int* children;
+  int64_t nch;           // total children (= child_off[n_par])
+  const uint8_t* oct_c;
+  int grid;              // persistent CTAs
+  cudaStream_t st;
+};
+
+template <int A, int B>
+void m2m_rb(const RbLaunch& L, const double2* mp_c, double2* mp_p, const double* Bphi, const double* vphi,
+            const double* Bth, const double* vth, const double2* shift_up, double2* F) {
+  using D = rb::Dims<A, B>;
+  if (L.nch > 0)
+    k_m2m_phi_rb<A, B><<<L.grid, rb::kThreads, 0, L.st>>>(L.nch, L.children, mp_c, Bphi, vphi, F);
+  const int smem = D::UTH_K * D::UTH_LDB * 8;
+  cudaFuncSetAttribute(k_m2m_theta_rb<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_m2m_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c, F,
+                                                            Bth, vth, shift_up, mp_p);
+}
+
+inline bool launch_m2m_rb(int nc, int np, const RbLaunch& L, const double2* mp_c, double2* mp_p, const double* Bphi,
+                          const double* vphi, const double* Bth, const double* vth, const double2* shift_up,
+                          double2* F) {
+#define HFMM_RB_M2M(A, B) \
+  if (nc == A && np == B) { m2m_rb<A, B>(L, mp_c, mp_p, Bphi, vphi, Bth, vth, shift_up, F); return true; }
+  HFMM_RB_PAIRS(HFMM_RB_M2M)
+#undef HFMM_RB_M2M
+  return false;
+}
+
+}  // namespace hfmm_b200
+
+#endif
