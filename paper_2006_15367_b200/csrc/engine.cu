@@ -598,8 +598,15 @@ void Engine::phase_l2l() {
     const CtLaunch cl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
                       R ? R->children : P.children, oct_[size_t(l + 1)], st_};
     if (cl.n_par == 0) continue;
-    // L2L: the two-stage kernels measured faster than the fused ones at every
-    // cfg-2 level (profiles/), so the compile-time fused L2L is opt-in.
+    if (use_rb_ && rb_pair(nc, np)) {
+      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_};
+      if (launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn, d_tmp)) {
+        launches_ += 2;
+        ck(cudaGetLastError(), "k_l2l_rb");
+        continue;
+      }
+    }
     if (use_ct_ && l2l_ct_ && launch_l2l_ct(nc, np, cl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v,
                                  P.shift_dn)) {
       ++launches_;

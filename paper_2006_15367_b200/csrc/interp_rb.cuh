@@ -233,6 +233,133 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, con
 }
 
 // ---------------------------------------------------------------------------
+// L2L stage 1: shifted, folded parent circles -> theta anterpolation -> narrow
+// rows Nb[j][row][col] (j = position in the children array).  Work item =
+// (parent, 8 rows of the (child slot, circle) space); each lane builds its A
+// row on the fly, L_p[s] shift_c[s] (one complex product feeds both parts).
+template <int NC, int NP>
+__global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_theta_rb(int n_par, const int* __restrict__ plist,
+                                                                  const int* __restrict__ child_off,
+                                                                  const int* __restrict__ children,
+                                                                  const uint8_t* __restrict__ oct_c,
+                                                                  const double2* __restrict__ loc_p,
+                                                                  const double* __restrict__ B,
+                                                                  const double* __restrict__ v,
+                                                                  const double2* __restrict__ shift_dn,
+                                                                  double2* __restrict__ Nb) {
+  using D = rb::Dims<NC, NP>;
+  constexpr int KS = D::DTH_K / 4, NT = D::DTH_N / 8, HALF = D::HALF, SP = D::SP;
+  extern __shared__ __align__(16) double Bsm[];
+  rb::stage_b<D::DTH_K, D::DTH_N, D::DTH_LDB>(Bsm, B);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t items = int64_t(n_par) * HALF;  // 8 HALF rows per parent = HALF tiles
+  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
+       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int par = int(it / HALF), tile = int(it - int64_t(par) * HALF);
+    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const int rho = tile * 8 + g, c = rho / HALF, p = rho - c * HALF;
+    const bool ok = c < nchp;
+    const double2* L = loc_p + int64_t(plist ? plist[par] : par) * SP;
+    const double2* sh = shift_dn + int64_t(ok ? oct_c[children[cb + c]] : 0) * SP;
+    double are[KS], aim[KS];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      const int k = 4 * kk + tq;
+      double2 f = make_double2(0.0, 0.0);
+      if (ok && k < 2 * NP) {
+        const int s = k < NP ? k * NP + p : (2 * NP - 1 - k) * NP + p + HALF;
+        f = cmul(__ldg(L + s), __ldg(sh + s));
+      }
+      are[kk] = f.x;
+      aim[kk] = f.y;
+    }
+    rb::rank1_inject<KS, 2 * NP>(are, aim, v);
+    double2* Nc = Nb + int64_t(cb + (ok ? c : 0)) * NC * D::LDN;
+    constexpr int NTC = 4;
+#pragma unroll
+    for (int j0 = 0; j0 < NT; j0 += NTC) {
+      double cre[NTC][2] = {}, cim[NTC][2] = {};
+      const double* bp = Bsm + tq * D::DTH_LDB + g + 8 * j0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int jc = 0; jc < NTC; ++jc)
+          if (j0 + jc < NT) {
+            const double b = bp[4 * kk * D::DTH_LDB + 8 * jc];
+            dmma884(cre[jc][0], cre[jc][1], are[kk], b);
+            dmma884(cim[jc][0], cim[jc][1], aim[kk], b);
+          }
+      if (ok) {
+#pragma unroll
+        for (int jc = 0; jc < NTC; ++jc)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = 8 * (j0 + jc) + 2 * tq + q;
+            if (j0 + jc < NT && n < 2 * NC) {
+              const int row = n < NC ? n : 2 * NC - 1 - n;
+              const int col = n < NC ? p : p + HALF;
+              Nc[row * D::LDN + col] = make_double2(cre[jc][q], cim[jc][q]);
+            }
+          }
+      }
+    }
+  }
+}
+
+// L2L stage 2: phi anterpolation of every narrow row, added into the child's
+// local expansion (the old values are loaded ahead of the DMMAs).
+template <int NC, int NP>
+__global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_phi_rb(int64_t nch, const int* __restrict__ children,
+                                                                const double2* __restrict__ Nb,
+                                                                const double* __restrict__ B,
+                                                                const double* __restrict__ v,
+                                                                double2* __restrict__ loc_c) {
+  using D = rb::Dims<NC, NP>;
+  constexpr int KS = D::DPHI_K / 4, NT = D::DPHI_N / 8;
+  __shared__ __align__(16) double Bs[D::DPHI_K * D::DPHI_LDB];
+  rb::stage_b<D::DPHI_K, D::DPHI_N, D::DPHI_LDB>(Bs, B);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t rows = nch * NC, tiles = (rows + 7) / 8;
+  for (int64_t t = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; t < tiles;
+       t += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int64_t R = t * 8 + g;
+    const bool ok = R < rows;
+    const int64_t j = ok ? R / NC : 0;
+    const int row = ok ? int(R - j * NC) : 0;
+    const double2* a = Nb + (j * NC + row) * D::LDN;
+    double2* dst = loc_c + (children ? children[j] : j) * int64_t(D::SC) + row * NC;
+    double are[KS], aim[KS];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) {
+      const int k = 4 * kk + tq;
+      const double2 xv = (ok && k < NP) ? __ldg(a + k) : make_double2(0.0, 0.0);
+      are[kk] = xv.x;
+      aim[kk] = xv.y;
+    }
+    double2 old[NT][2];
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int n = 8 * jn + 2 * tq + q;
+        old[jn][q] = (ok && n < NC) ? dst[n] : make_double2(0.0, 0.0);
+      }
+    rb::rank1_inject<KS, NP>(are, aim, v);
+    double cre[NT][2] = {}, cim[NT][2] = {};
+    rb::tile_mma<KS, NT, D::DPHI_LDB>(are, aim, Bs, cre, cim);
+    if (ok) {
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = 8 * jn + 2 * tq + q;
+          if (n < NC) dst[n] = make_double2(old[jn][q].x + cre[jn][q], old[jn][q].y + cim[jn][q]);
+        }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Dispatch over the level pairs with a theta-pass K <= 72 (register budget).
 #define HFMM_RB_PAIRS(X) X(18, 28) X(28, 42) X(22, 30) X(30, 44) X(26, 34) X(34, 52)
 
@@ -267,6 +394,28 @@ void m2m_rb(const RbLaunch& L, const double2* mp_c, double2* mp_p, const double*
   cudaFuncSetAttribute(k_m2m_theta_rb<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   k_m2m_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c, F,
                                                             Bth, vth, shift_up, mp_p);
+}
+
+template <int A, int B>
+void l2l_rb(const RbLaunch& L, const double2* loc_p, double2* loc_c, const double* Bth, const double* vth,
+            const double* Bphi, const double* vphi, const double2* shift_dn, double2* Nb) {
+  using D = rb::Dims<A, B>;
+  const int smem = D::DTH_K * D::DTH_LDB * 8;
+  cudaFuncSetAttribute(k_l2l_theta_rb<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_l2l_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c,
+                                                            loc_p, Bth, vth, shift_dn, Nb);
+  if (L.nch > 0)
+    k_l2l_phi_rb<A, B><<<L.grid, rb::kThreads, 0, L.st>>>(L.nch, L.children, Nb, Bphi, vphi, loc_c);
+}
+
+inline bool launch_l2l_rb(int nc, int np, const RbLaunch& L, const double2* loc_p, double2* loc_c, const double* Bth,
+                          const double* vth, const double* Bphi, const double* vphi, const double2* shift_dn,
+                          double2* Nb) {
+#define HFMM_RB_L2L(A, B) \
+  if (nc == A && np == B) { l2l_rb<A, B>(L, loc_p, loc_c, Bth, vth, Bphi, vphi, shift_dn, Nb); return true; }
+  HFMM_RB_PAIRS(HFMM_RB_L2L)
+#undef HFMM_RB_L2L
+  return false;
 }
 
 inline bool launch_m2m_rb(int nc, int np, const RbLaunch& L, const double2* mp_c, double2* mp_p, const double* Bphi,
