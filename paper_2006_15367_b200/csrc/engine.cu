@@ -491,6 +491,12 @@ int theta_chunk(int half, int outs_per_circle, int threads) {
 }
 }  // namespace
 
+namespace {
+// Runtime-shaped streaming kernels: any even grid pair (the host B layouts
+// K = round4(n_in + 1), N = round8(n_out) are what they expect).
+bool rbl_ok(int nc, int np) { return nc % 2 == 0 && np % 2 == 0 && std::getenv("HFMM_NO_RBL") == nullptr; }
+}  // namespace
+
 void Engine::phase_m2m() {
   // Distributed mode: halo rows still hold last evaluation's full multipoles;
   // the upward pass must see zeros there (they are summed again after it).
@@ -511,6 +517,17 @@ void Engine::phase_m2m() {
         ck(cudaGetLastError(), "k_m2m_rb");
         continue;
       }
+    }
+    if (use_rb_ && rbl_ok(nc, np)) {  // larger pairs: runtime-shaped streaming kernels
+      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+      if (nch > 0)
+        k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, nch, cl.children, C.mp, P.up_phi_B, P.up_phi_v,
+                                                          d_tmp);
+      k_m2m_theta_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, cl.n_par, cl.plist, cl.child_off, cl.children,
+                                                          cl.oct_c, d_tmp, P.up_th_B, P.up_th_v, P.shift_up, P.mp);
+      launches_ += 2;
+      ck(cudaGetLastError(), "k_m2m_rbl");
+      continue;
     }
     if (use_ct_ && launch_m2m_ct(nc, np, cl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v,
                                  P.shift_up)) {
@@ -606,6 +623,17 @@ void Engine::phase_l2l() {
         ck(cudaGetLastError(), "k_l2l_rb");
         continue;
       }
+    }
+    if (use_rb_ && rbl_ok(nc, np)) {
+      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+      k_l2l_theta_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, cl.n_par, cl.plist, cl.child_off, cl.children,
+                                                          cl.oct_c, P.loc, P.dn_th_B, P.dn_th_v, P.shift_dn, d_tmp);
+      if (nch > 0)
+        k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, nch, cl.children, d_tmp, P.dn_phi_B, P.dn_phi_v,
+                                                          C.loc);
+      launches_ += 2;
+      ck(cudaGetLastError(), "k_l2l_rbl");
+      continue;
     }
     if (use_ct_ && l2l_ct_ && launch_l2l_ct(nc, np, cl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v,
                                  P.shift_dn)) {

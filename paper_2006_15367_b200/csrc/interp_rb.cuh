@@ -360,6 +360,237 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_phi_rb(int64_t nch, con
 }
 
 // ---------------------------------------------------------------------------
+// Runtime-shaped variants for the larger level pairs (upper levels): A values
+// are re-read (L1) per chunk of kChunk n8 tiles instead of living in
+// registers, the rank-1 alpha comes from a first pass over K, and B (up to
+// ~350 KB) is read through L1/L2.
+namespace rb {
+constexpr int kChunk = 4;
+
+// alpha = v . x over the K_in data columns of a complex row; fetch(k) -> double2.
+template <class Fetch>
+__device__ __forceinline__ double2 row_alpha(int kin, const double* __restrict__ v, Fetch fetch) {
+  const int tq = threadIdx.x & 3;
+  double sr = 0.0, si = 0.0;
+  for (int k = tq; k < kin; k += 4) {
+    const double vk = __ldg(v + k);
+    const double2 x = fetch(k);
+    sr = fma(vk, x.x, sr);
+    si = fma(vk, x.y, si);
+  }
+  sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+  si += __shfl_xor_sync(0xffffffffu, si, 1);
+  sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+  si += __shfl_xor_sync(0xffffffffu, si, 2);
+  return make_double2(-si, sr);  // i alpha
+}
+
+// C chunk (8 complex rows x kChunk n8 tiles from n8 tile j0) over K = 4 ks:
+// column kin holds ia (rank-1), columns > kin are zero.
+template <class Fetch>
+__device__ __forceinline__ void chunk_mma(int ks, int kin, double2 ia, Fetch fetch, const double* __restrict__ B, int N,
+                                          int j0, int nt, double (&cre)[kChunk][2], double (&cim)[kChunk][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const double* bp = B + tq * N + 8 * j0 + g;
+#pragma unroll 2
+  for (int kk = 0; kk < ks; ++kk) {
+    const int k = 4 * kk + tq;
+    const double2 x = k < kin ? fetch(k) : (k == kin ? ia : make_double2(0.0, 0.0));
+#pragma unroll
+    for (int jc = 0; jc < kChunk; ++jc)
+      if (j0 + jc < nt) {
+        const double b = __ldg(bp + 4 * kk * N + 8 * jc);
+        dmma884(cre[jc][0], cre[jc][1], x.x, b);
+        dmma884(cim[jc][0], cim[jc][1], x.y, b);
+      }
+  }
+}
+}  // namespace rb
+
+__global__ void __launch_bounds__(rb::kThreads) k_m2m_phi_rbl(int nc, int np, int64_t nch, const int* __restrict__ children,
+                                                              const double2* __restrict__ mp_c,
+                                                              const double* __restrict__ B, const double* __restrict__ v,
+                                                              double2* __restrict__ F) {
+  const int K = rb::r4(nc + 1), N = rb::r8(np), ks = K / 4, nt = N / 8, half = np / 2, ldf = rb::r4(2 * nc + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t rows = nch * nc, tiles = (rows + 7) / 8;
+  for (int64_t t = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; t < tiles;
+       t += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int64_t R = t * 8 + g;
+    const bool ok = R < rows;
+    const int64_t j = ok ? R / nc : 0;
+    const int i = ok ? int(R - j * nc) : 0;
+    const double2* x = mp_c + (children ? children[j] : j) * int64_t(nc) * nc + int64_t(i) * nc;
+    auto fetch = [&](int k) { return ok ? __ldg(x + k) : make_double2(0.0, 0.0); };
+    const double2 ia = rb::row_alpha(nc, v, fetch);
+    double2* Fj = F + j * half * ldf;
+    for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
+      double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
+      rb::chunk_mma(ks, nc, ia, fetch, B, N, j0, nt, cre, cim);
+      if (ok) {
+#pragma unroll
+        for (int jc = 0; jc < rb::kChunk; ++jc)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = 8 * (j0 + jc) + 2 * tq + q;
+            if (j0 + jc < nt && n < np) {
+              const int p = n < half ? n : n - half;
+              const int ii = n < half ? i : 2 * nc - 1 - i;
+              Fj[int64_t(p) * ldf + ii] = make_double2(cre[jc][q], cim[jc][q]);
+            }
+          }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, int n_par, const int* __restrict__ plist,
+                                                                const int* __restrict__ child_off,
+                                                                const int* __restrict__ children,
+                                                                const uint8_t* __restrict__ oct_c,
+                                                                const double2* __restrict__ F,
+                                                                const double* __restrict__ B,
+                                                                const double* __restrict__ v,
+                                                                const double2* __restrict__ shift_up,
+                                                                double2* __restrict__ mp_p) {
+  const int K = rb::r4(2 * nc + 1), N = rb::r8(2 * np), ks = K / 4, nt = N / 8, half = np / 2, ldf = K;
+  const int64_t SP = int64_t(np) * np;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t items = int64_t(n_par) * half;
+  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
+       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int par = int(it / half), p = int(it - int64_t(par) * half);
+    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const bool ok = g < nchp;
+    const double2* frow = F + (int64_t(cb + (ok ? g : 0)) * half + p) * ldf;
+    const double2* sh = shift_up + int64_t(ok ? oct_c[children[cb + g]] : 0) * SP;
+    auto fetch = [&](int k) { return ok ? __ldg(frow + k) : make_double2(0.0, 0.0); };
+    const double2 ia = rb::row_alpha(2 * nc, v, fetch);
+    double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
+    for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
+      double2 shv[rb::kChunk][2];
+#pragma unroll
+      for (int jc = 0; jc < rb::kChunk; ++jc)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = 8 * (j0 + jc) + 2 * tq + q;
+          const int64_t s = n < np ? int64_t(n) * np + p : int64_t(2 * np - 1 - n) * np + p + half;
+          shv[jc][q] = (ok && n < 2 * np) ? __ldg(sh + s) : make_double2(0.0, 0.0);
+        }
+      double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
+      rb::chunk_mma(ks, 2 * nc, ia, fetch, B, N, j0, nt, cre, cim);
+#pragma unroll
+      for (int jc = 0; jc < rb::kChunk; ++jc)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double2 f = shv[jc][q];
+          double vr = cre[jc][q] * f.x - cim[jc][q] * f.y;
+          double vi = cre[jc][q] * f.y + cim[jc][q] * f.x;
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) {
+            vr += __shfl_xor_sync(0xffffffffu, vr, off);
+            vi += __shfl_xor_sync(0xffffffffu, vi, off);
+          }
+          const int n = 8 * (j0 + jc) + 2 * tq + q;
+          if (g == 0 && j0 + jc < nt && n < 2 * np) {
+            const int64_t s = n < np ? int64_t(n) * np + p : int64_t(2 * np - 1 - n) * np + p + half;
+            out[s] = make_double2(vr, vi);
+          }
+        }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, int n_par, const int* __restrict__ plist,
+                                                                const int* __restrict__ child_off,
+                                                                const int* __restrict__ children,
+                                                                const uint8_t* __restrict__ oct_c,
+                                                                const double2* __restrict__ loc_p,
+                                                                const double* __restrict__ B,
+                                                                const double* __restrict__ v,
+                                                                const double2* __restrict__ shift_dn,
+                                                                double2* __restrict__ Nb) {
+  const int K = rb::r4(2 * np + 1), N = rb::r8(2 * nc), ks = K / 4, nt = N / 8, half = np / 2, ldn = rb::r4(np + 1);
+  const int64_t SP = int64_t(np) * np;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t items = int64_t(n_par) * half;
+  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
+       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int par = int(it / half), tile = int(it - int64_t(par) * half);
+    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const int rho = tile * 8 + g, c = rho / half, p = rho - c * half;
+    const bool ok = c < nchp;
+    const double2* L = loc_p + int64_t(plist ? plist[par] : par) * SP;
+    const double2* sh = shift_dn + int64_t(ok ? oct_c[children[cb + c]] : 0) * SP;
+    auto fetch = [&](int k) {
+      if (!ok) return make_double2(0.0, 0.0);
+      const int64_t s = k < np ? int64_t(k) * np + p : int64_t(2 * np - 1 - k) * np + p + half;
+      return cmul(__ldg(L + s), __ldg(sh + s));
+    };
+    const double2 ia = rb::row_alpha(2 * np, v, fetch);
+    double2* Nc = Nb + int64_t(cb + (ok ? c : 0)) * nc * ldn;
+    for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
+      double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
+      rb::chunk_mma(ks, 2 * np, ia, fetch, B, N, j0, nt, cre, cim);
+      if (ok) {
+#pragma unroll
+        for (int jc = 0; jc < rb::kChunk; ++jc)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = 8 * (j0 + jc) + 2 * tq + q;
+            if (j0 + jc < nt && n < 2 * nc) {
+              const int row = n < nc ? n : 2 * nc - 1 - n;
+              const int col = n < nc ? p : p + half;
+              Nc[int64_t(row) * ldn + col] = make_double2(cre[jc][q], cim[jc][q]);
+            }
+          }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(rb::kThreads) k_l2l_phi_rbl(int nc, int np, int64_t nch, const int* __restrict__ children,
+                                                              const double2* __restrict__ Nb,
+                                                              const double* __restrict__ B, const double* __restrict__ v,
+                                                              double2* __restrict__ loc_c) {
+  const int K = rb::r4(np + 1), N = rb::r8(nc), ks = K / 4, nt = N / 8, ldn = K;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int64_t rows = nch * nc, tiles = (rows + 7) / 8;
+  for (int64_t t = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; t < tiles;
+       t += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+    const int64_t R = t * 8 + g;
+    const bool ok = R < rows;
+    const int64_t j = ok ? R / nc : 0;
+    const int row = ok ? int(R - j * nc) : 0;
+    const double2* a = Nb + (j * nc + row) * ldn;
+    double2* dst = loc_c + (children ? children[j] : j) * int64_t(nc) * nc + int64_t(row) * nc;
+    auto fetch = [&](int k) { return ok ? __ldg(a + k) : make_double2(0.0, 0.0); };
+    const double2 ia = rb::row_alpha(np, v, fetch);
+    for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
+      double2 old[rb::kChunk][2];
+#pragma unroll
+      for (int jc = 0; jc < rb::kChunk; ++jc)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int n = 8 * (j0 + jc) + 2 * tq + q;
+          old[jc][q] = (ok && j0 + jc < nt && n < nc) ? dst[n] : make_double2(0.0, 0.0);
+        }
+      double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
+      rb::chunk_mma(ks, np, ia, fetch, B, N, j0, nt, cre, cim);
+      if (ok) {
+#pragma unroll
+        for (int jc = 0; jc < rb::kChunk; ++jc)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int n = 8 * (j0 + jc) + 2 * tq + q;
+            if (j0 + jc < nt && n < nc) dst[n] = make_double2(old[jc][q].x + cre[jc][q], old[jc][q].y + cim[jc][q]);
+          }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Dispatch over the level pairs with a theta-pass K <= 72 (register budget).
 #define HFMM_RB_PAIRS(X) X(18, 28) X(28, 42) X(22, 30) X(30, 44) X(26, 34) X(34, 52)
 
