@@ -223,11 +223,16 @@ void Engine::upload() {
   d_near = upload_vec(nr);
   // P2P launch lists: own leaves by population (k_p2p<false> / <true>)
   {
-    std::vector<int> small, dense;
-    for (int64_t li = leaf_b_; li < leaf_e_; ++li)
-      (s.leaf_start[size_t(li) + 1] - s.leaf_start[size_t(li)] <= 32 ? small : dense).push_back(int(li));
+    // tiny (<= 8: warp per leaf), small (<= 32: CTA per leaf), dense (symmetric)
+    std::vector<int> tiny, small, dense;
+    for (int64_t li = leaf_b_; li < leaf_e_; ++li) {
+      const uint64_t pop = s.leaf_start[size_t(li) + 1] - s.leaf_start[size_t(li)];
+      (pop <= 8 ? tiny : pop <= 32 ? small : dense).push_back(int(li));
+    }
+    n_tiny_ = int(tiny.size());
     n_small_ = int(small.size());
     n_dense_ = int(dense.size());
+    d_tiny_leaves_ = upload_vec(tiny);
     d_small_leaves_ = upload_vec(small);
     d_dense_leaves_ = upload_vec(dense);
     // symmetric pair lists among own dense leaves (k_p2p_sym / k_p2p_gather)
@@ -717,6 +722,12 @@ void Engine::near_start() {
   const int64_t cnt = part_e_ - part_b_;
   if (cnt > 0)
     ck(cudaMemsetAsync(d_pot_near + part_b_, 0, size_t(cnt) * sizeof(double2), st2_), "memset near");
+  if (n_tiny_ > 0) {
+    k_p2p_small_w<<<unsigned((n_tiny_ + 3) / 4), 128, 0, st2_>>>(n_tiny_, d_tiny_leaves_, d_leaf_start, d_near_off,
+                                                                 d_near, d.centers, d_x, d_y, d_z, d_q, s_.k,
+                                                                 d_pot_near);
+    ++launches_;
+  }
   if (n_small_ > 0) {
     k_p2p<false><<<unsigned(n_small_), 128, 0, st2_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
                                                        d_x, d_y, d_z, d_q, s_.k, d_pot_near);

@@ -163,9 +163,10 @@ class Engine {
   int64_t* d_leaf_start = nullptr;
   int64_t* d_near_off = nullptr;
   int* d_near = nullptr;
-  int* d_small_leaves_ = nullptr;  // own leaves with <= 32 particles
+  int* d_tiny_leaves_ = nullptr;   // own leaves with <= 8 particles (warp per leaf)
+  int* d_small_leaves_ = nullptr;  // own leaves with 9..32 particles
   int* d_dense_leaves_ = nullptr;
-  int n_small_ = 0, n_dense_ = 0;
+  int n_small_ = 0, n_dense_ = 0, n_tiny_ = 0;
   int* d_plain_off_ = nullptr;  // symmetric P2P lists over dense own leaves
   int* d_plain_ = nullptr;
   int* d_sym_off_ = nullptr;

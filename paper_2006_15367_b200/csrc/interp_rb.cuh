@@ -365,7 +365,10 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_phi_rb(int64_t nch, con
 // registers, the rank-1 alpha comes from a first pass over K, and B (up to
 // ~350 KB) is read through L1/L2.
 namespace rb {
-constexpr int kChunk = 4;
+#ifndef HFMM_RBL_CHUNK
+#define HFMM_RBL_CHUNK 4
+#endif
+constexpr int kChunk = HFMM_RBL_CHUNK;
 
 // alpha = v . x over the K_in data columns of a complex row; fetch(k) -> double2.
 template <class Fetch>

@@ -712,6 +712,85 @@ __global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, con
   }
 }
 
+// Small leaves (<= 32 observers), one WARP per leaf: the near leaves' prefix
+// sums come from a warp scan, sources are staged kSW at a time in warp-private
+// shared memory (__syncwarp only), G = 32 / n_o lanes share an observer.
+constexpr int kSW = 64;
+__global__ void __launch_bounds__(128) k_p2p_small_w(int n_small, const int* __restrict__ leaves,
+                                                     const int64_t* __restrict__ leaf_start,
+                                                     const int64_t* __restrict__ near_off, const int* __restrict__ near,
+                                                     const double* __restrict__ centers, const double* __restrict__ x,
+                                                     const double* __restrict__ y, const double* __restrict__ z,
+                                                     const double2* __restrict__ q, double k, double2* __restrict__ pot) {
+  __shared__ double sx[4][kSW], sy[4][kSW], sz[4][kSW];
+  __shared__ double2 sq[4][kSW];
+  __shared__ int64_t spref[4][32], sbeg[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 4 + warp;
+  if (i >= n_small) return;  // whole warp
+  const int64_t leaf = leaves[i];
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const int n_o = int(p1 - p0);
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
+  const int64_t nb = near_off[leaf];
+  const int nn = int(near_off[leaf + 1] - nb);
+  int64_t cnt = 0, beg = 0;
+  if (lane < nn) {
+    const int lf = near[nb + lane];
+    beg = leaf_start[lf];
+    cnt = leaf_start[lf + 1] - beg;
+  }
+  int64_t incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t u = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += u;
+  }
+  const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+  spref[warp][lane] = incl - cnt;  // lanes >= nn: total
+  sbeg[warp][lane] = beg;
+  int G = 32;
+  while (G > 1 && G * n_o > 32) G >>= 1;
+  const int o = lane / G, sub = lane - o * G;
+  const bool valid = o < n_o;
+  const double xo = valid ? k * (x[p0 + o] - cx) : 1e300;
+  const double yo = valid ? k * (y[p0 + o] - cy) : 0.0;
+  const double zo = valid ? k * (z[p0 + o] - cz) : 0.0;
+  double ar = 0.0, ai = 0.0;
+  for (int64_t cb = 0; cb < total; cb += kSW) {
+    const int n = int(total - cb < kSW ? total - cb : kSW);
+    __syncwarp();
+    for (int t = lane; t < n; t += 32) {
+      const int64_t v = cb + t;
+      int lo = 0, hi = nn;  // largest j with spref[j] <= v
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (spref[warp][mid] <= v) lo = mid; else hi = mid;
+      }
+      const int64_t src = sbeg[warp][lo] + (v - spref[warp][lo]);
+      sx[warp][t] = k * (x[src] - cx);
+      sy[warp][t] = k * (y[src] - cy);
+      sz[warp][t] = k * (z[src] - cz);
+      const double2 qq = q[src];
+      sq[warp][t] = make_double2(qs * qq.x, qs * qq.y);
+    }
+    __syncwarp();
+    if (valid)
+      for (int t = sub; t < n; t += G) p2p_pair(xo, yo, zo, sx[warp][t], sy[warp][t], sz[warp][t], sq[warp][t], ar, ai);
+  }
+  for (int off = G >> 1; off > 0; off >>= 1) {
+    ar += __shfl_xor_sync(0xffffffffu, ar, off);
+    ai += __shfl_xor_sync(0xffffffffu, ai, off);
+  }
+  if (valid && sub == 0) {
+    double2 cur = pot[p0 + o];
+    cur.x += ar;
+    cur.y += ai;
+    pot[p0 + o] = cur;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Symmetric near field for dense leaves: g(r) is the same for (m <- n) and
 // (n <- m), so every unordered pair of dense own leaves (A, B), A < B, is
