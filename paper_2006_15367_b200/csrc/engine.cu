@@ -696,7 +696,7 @@ void Engine::phase_l2t() {
   const DevLevel& d = lv_[size_t(s_.L)];
   const int64_t nl = leaf_e_ - leaf_b_;
   if (quad_ok(d)) {
-    const size_t smem = 4 * size_t(d.S + kQuadP * (d.nt / 2)) * sizeof(double2);
+    const size_t smem = 4 * size_t(kQuadP * (d.nt / 2)) * sizeof(double2);
     if (smem > 48 * 1024)
       ck(cudaFuncSetAttribute(k_l2t_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
     k_l2t_quad<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,

@@ -327,7 +327,7 @@ __global__ void k_l2l_phi(int n_c, int n_p, int64_t child_b, const double2* __re
 // (a quarter of the direct sincos count); the phases equal the reference's
 // per-sample ones to rounding.  One warp per leaf.
 constexpr int kQuadHalfMax = 16;  // n/2 <= 16 (leaf grids of the BASELINE configs: n <= 26)
-constexpr int kQuadR = 3;         // quads per lane per pass (C2M)
+constexpr int kQuadR = 3;  // quads per lane per pass (C2M; measured best of 2..4)
 constexpr int kQuadP = 32;        // particles per B-table chunk
 
 // exp(i(A+B)), exp(i(A-B)); the other two are their conjugates.
@@ -414,10 +414,10 @@ __global__ void __launch_bounds__(128) k_c2m_quad(int64_t leaf_b, int64_t nl, co
   }
 }
 
-// L2T: potentials of a leaf's observers from its local samples, weighted
-// w_s L_s staged per warp in shared memory; lanes over quads, kQuadOB
-// observers per pass (the four samples of a quad are loaded once for all of
-// them and their sincos chains interleave), one shuffle reduction each.
+// L2T: potentials of a leaf's observers from its local samples; lanes over
+// quads, kQuadOB observers per pass (the four samples w_s L_s of a quad are
+// read once, straight from L1 / global, for all of them -- their latency
+// overlaps the sincos chains, which interleave), one shuffle reduction each.
 constexpr int kQuadOB = 4;
 __global__ void __launch_bounds__(128) k_l2t_quad(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
                                                   const double* __restrict__ x, const double* __restrict__ y,
@@ -429,16 +429,10 @@ __global__ void __launch_bounds__(128) k_l2t_quad(int64_t leaf_b, int64_t nl, co
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = n / 2, quads = half * half, nphi = n;
   const int64_t S = int64_t(n) * n;
-  double2* Lw = qsm + warp * (S + kQuadP * half);  // w_s L_s, then the B table
-  double2* Bt = Lw + S;
+  double2* Bt = qsm + warp * (kQuadP * half);  // B table of this warp
   const int64_t li = int64_t(blockIdx.x) * 4 + warp;
   if (li >= nl) return;
   const int64_t leaf = leaf_b + li;
-  for (int64_t s = lane; s < S; s += 32) {
-    const double2 v = loc[leaf * S + s];
-    const double w = wq[s];
-    Lw[s] = make_double2(w * v.x, w * v.y);
-  }
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
@@ -466,7 +460,13 @@ __global__ void __launch_bounds__(128) k_l2t_quad(int64_t leaf_b, int64_t nl, co
         const int i = qd / half, j = qd - i * half;
         const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
         const double dxs = dir[3 * s1], dys = dir[3 * s1 + 1];
-        const double2 l1 = Lw[s1], l2 = Lw[s2], l3 = Lw[s1 + half], l4 = Lw[s2 + half];
+        const double2* lc = loc + leaf * S;
+        auto lw = [&](int64_t s) {
+          const double2 v = __ldg(lc + s);
+          const double w = __ldg(wq + s);
+          return make_double2(w * v.x, w * v.y);
+        };
+        const double2 l1 = lw(s1), l2 = lw(s2), l3 = lw(s1 + half), l4 = lw(s2 + half);
 #pragma unroll
         for (int o = 0; o < kQuadOB; ++o) {
           const int pp = pb + o < np ? pb + o : pb;
