@@ -886,21 +886,22 @@ __global__ void __launch_bounds__(128) k_p2p_sym(const int* __restrict__ leaves,
           const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
           const double2 qq = sh.sq[t];
           double br = 0.0, bi = 0.0;
+          // Branch- and mask-free: idle observer slots sit at a finite far
+          // point with zero charge (exact-zero terms), and two particles in
+          // different leaves are never coincident (equal positions share a
+          // Morton cell), so r2 > 0 here.
 #pragma unroll
           for (int c = 0; c < kP2PObsPerLane; ++c) {
-            if (c < nc) {
-              const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
-              const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-              const bool self = r2 == 0.0;  // coincident particles in different leaves cannot occur
-              const double ri = rsqrt(self ? 1.0 : r2);
-              double sn, cs;
-              sincos_fast(-(r2 * ri), &sn, &cs);
-              const double gr = self ? 0.0 : cs * ri, gi = self ? 0.0 : sn * ri;
-              ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
-              ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
-              br = fma(gr, qo[c].x, fma(-gi, qo[c].y, br));
-              bi = fma(gr, qo[c].y, fma(gi, qo[c].x, bi));
-            }
+            const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
+            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            const double ri = rsqrt(r2);
+            double sn, cs;
+            sincos_fast(-(r2 * ri), &sn, &cs);
+            const double gr = cs * ri, gi = sn * ri;
+            ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
+            ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
+            br = fma(gr, qo[c].x, fma(-gi, qo[c].y, br));
+            bi = fma(gr, qo[c].y, fma(gi, qo[c].x, bi));
           }
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) {
