@@ -187,6 +187,11 @@ hfmm_status hfmm_gpu_store_potentials_device(hfmm_gpu* g, double* d_pot_sorted);
 /* Kernels this handle has launched so far (cumulative; a bench counts its
  * timed region by difference). */
 hfmm_status hfmm_gpu_launch_count(hfmm_gpu* g, int64_t* launches);
+/* Phase overlap inside hfmm_gpu_evaluate / _evaluate_device (default on):
+ * the leaf-level M2L runs on a low-priority stream beside the high-priority
+ * far-field chain.  Off: strictly sequential phases, so hfmm_gpu_last_timing
+ * reports each phase's own kernel time.  Results are identical either way. */
+hfmm_status hfmm_gpu_set_overlap(hfmm_gpu* g, int on);
 
 /* One-shot: build_setup + evaluate on one device (evaluate_potential,
  * traversal.cpp:819-823).  Requires cfg->num_ranks == 1. */

@@ -106,6 +106,7 @@ _SIG = {
     "hfmm_gpu_particle_range": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "hfmm_gpu_store_potentials_device": (ctypes.c_int, [_P, _P]),
     "hfmm_gpu_launch_count": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
+    "hfmm_gpu_set_overlap": (ctypes.c_int, [_P, ctypes.c_int]),
     "hfmm_evaluate_potential": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.POINTER(RunConfigC),
                                                ctypes.c_int, _P]),
     "hfmm_gpu_direct": (ctypes.c_int, [_P, _P, ctypes.c_size_t, _P, ctypes.c_size_t, ctypes.c_double,

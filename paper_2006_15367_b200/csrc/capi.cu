@@ -255,6 +255,13 @@ hfmm_status hfmm_gpu_store_potentials_device(hfmm_gpu* g, double* d_pot) {
   });
 }
 
+hfmm_status hfmm_gpu_set_overlap(hfmm_gpu* g, int on) {
+  return guard([&] {
+    need(g, "hfmm_gpu_set_overlap(gpu)");
+    g->eng->set_overlap(on != 0);
+  });
+}
+
 hfmm_status hfmm_gpu_launch_count(hfmm_gpu* g, int64_t* n) {
   return guard([&] {
     need(g, "hfmm_gpu_launch_count(gpu)");

@@ -74,6 +74,16 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   // Side stream for the near field.  (Giving the far-field chain a higher
   // stream priority measured slower on cfg 2 and cfg 3: equal priorities.)
   ck(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking), "stream2");
+  {
+    int least = 0, greatest = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priorities");
+    ck(cudaStreamCreateWithPriority(&st_hi_, cudaStreamNonBlocking, greatest), "stream hi");
+    ck(cudaStreamCreateWithPriority(&st_lo_, cudaStreamNonBlocking, least), "stream lo");
+    for (cudaEvent_t* e : {&ev_ofork_, &ev_ojoin_, &ev_c2m_, &ev_m2l_leaf_})
+      ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    for (cudaEvent_t* e : {&ev_lf0_, &ev_lf1_, &ev_la_, &ev_lb_}) ck(cudaEventCreate(e), "event");
+    overlap_ = std::getenv("HFMM_NO_OVERLAP") == nullptr;  // debugging aid: strictly sequential phases
+  }
   ck(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
   ck(cudaEventCreate(&ev_near0_), "event");
@@ -85,13 +95,17 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
-  for (cudaStream_t s : {st_, st2_})  // both streams idle before the buffers go
+  for (cudaStream_t s : {st_, st2_, st_hi_, st_lo_})  // every stream idle before the buffers go
     if (s) cudaStreamSynchronize(s);
   for (void* p : allocs_) cudaFree(p);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (st_ && owns_stream_) cudaStreamDestroy(st_);
   if (st2_) cudaStreamDestroy(st2_);
+  for (cudaStream_t s : {st_hi_, st_lo_})
+    if (s) cudaStreamDestroy(s);
+  for (cudaEvent_t e : {ev_ofork_, ev_ojoin_, ev_c2m_, ev_m2l_leaf_, ev_lf0_, ev_lf1_, ev_la_, ev_lb_})
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {ev_fork_, ev_join_, ev_near0_, ev_near1_})
     if (e) cudaEventDestroy(e);
 }
@@ -588,11 +602,13 @@ void Engine::phase_m2m() {
   }
 }
 
-void Engine::phase_m2l() {
+void Engine::phase_m2l(int lo, int hi) {
+  if (lo < 0) lo = s_.top;
+  if (hi < 0) hi = s_.L;
   const bool dmma = std::getenv("HFMM_M2L_DFMA") == nullptr;  // debugging aid: the DFMA stencil
   ck(cudaFuncSetAttribute(k_m2l_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
   ck(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
-  for (int l = s_.top; l <= s_.L; ++l) {
+  for (int l = lo; l <= hi; ++l) {
     DevLevel& d = lv_[size_t(l)];
     if (d.dense) {
       const int nb = (d.G + m2l::MB - 1) / m2l::MB;
@@ -611,8 +627,10 @@ void Engine::phase_m2l() {
   ck(cudaGetLastError(), "m2l");
 }
 
-void Engine::phase_l2l() {
-  for (int l = s_.top; l < s_.L; ++l) {
+void Engine::phase_l2l(int lo, int hi) {
+  if (lo < 0) lo = s_.top;
+  if (hi < 0) hi = s_.L - 1;
+  for (int l = lo; l <= hi; ++l) {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
@@ -811,6 +829,14 @@ void Engine::last_timing(double* ms, int64_t* launches) {
     ms[i] = f;
   }
   if (cudaEventElapsedTime(&f, ev_near0_, ev_near1_) == cudaSuccess) ms[6] = f;  // side stream
+  if (overlapped_) {
+    // M2L = upper levels on the chain + the leaf level's own duration on its
+    // stream; L2L = the chain's L2L segments without the wait for that leaf M2L.
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, ev_lf0_, ev_lf1_) == cudaSuccess) ms[3] += a;
+    if (cudaEventElapsedTime(&a, ev_[4], ev_la_) == cudaSuccess && cudaEventElapsedTime(&b, ev_lb_, ev_[5]) == cudaSuccess)
+      ms[4] = a + b;
+  }
   cudaEventElapsedTime(&f, ev_[0], ev_[7]);
   ms[7] = f;
   if (launches) *launches = last_launches_;
@@ -827,21 +853,59 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
   if (d_q_sorted && d_q_sorted != reinterpret_cast<const double*>(d_q))
     ck(cudaMemcpyAsync(d_q, d_q_sorted, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "q");
   cudaEventRecord(ev_[0], st_);
+  // The far-field chain runs on a high-priority stream; the leaf-level M2L
+  // (it needs only C2M's multipoles and is consumed only by the last L2L
+  // step) runs beside it on a low-priority stream and fills the SMs that the
+  // small upper-level kernels leave idle.  Dependencies are unchanged.
+  const bool overlap = overlap_ && s_.L > s_.top;
+  cudaStream_t user = st_;
+  overlapped_ = overlap;
+  if (overlap) {
+    ck(cudaEventRecord(ev_ofork_, user), "fork");
+    ck(cudaStreamWaitEvent(st_hi_, ev_ofork_, 0), "fork wait");
+    st_ = st_hi_;
+  }
   near_start();  // side stream, overlapped with the far-field chain
   build_T();
   cudaEventRecord(ev_[1], st_);
   phase_c2m();
   cudaEventRecord(ev_[2], st_);
+  if (overlap) {
+    ck(cudaEventRecord(ev_c2m_, st_), "c2m");
+    ck(cudaStreamWaitEvent(st_lo_, ev_c2m_, 0), "c2m wait");
+    cudaStream_t keep = st_;
+    st_ = st_lo_;
+    cudaEventRecord(ev_lf0_, st_);
+    phase_m2l(s_.L, s_.L);
+    cudaEventRecord(ev_lf1_, st_);
+    ck(cudaEventRecord(ev_m2l_leaf_, st_), "m2l leaf");
+    st_ = keep;
+  }
   phase_m2m();
   cudaEventRecord(ev_[3], st_);
-  phase_m2l();
-  cudaEventRecord(ev_[4], st_);
-  phase_l2l();
+  if (overlap) {
+    phase_m2l(s_.top, s_.L - 1);
+    cudaEventRecord(ev_[4], st_);
+    phase_l2l(s_.top, s_.L - 2);
+    cudaEventRecord(ev_la_, st_);
+    ck(cudaStreamWaitEvent(st_, ev_m2l_leaf_, 0), "m2l leaf wait");
+    cudaEventRecord(ev_lb_, st_);
+    phase_l2l(s_.L - 1, s_.L - 1);
+  } else {
+    phase_m2l();
+    cudaEventRecord(ev_[4], st_);
+    phase_l2l();
+  }
   cudaEventRecord(ev_[5], st_);
   phase_l2t();
   cudaEventRecord(ev_[6], st_);
   phase_near();
   cudaEventRecord(ev_[7], st_);
+  if (overlap) {
+    ck(cudaEventRecord(ev_ojoin_, st_), "join");
+    ck(cudaStreamWaitEvent(user, ev_ojoin_, 0), "join wait");
+    st_ = user;
+  }
   if (d_pot_sorted)
     ck(cudaMemcpyAsync(d_pot_sorted, d_pot, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "pot");
   last_launches_ = launches_ - l0;

@@ -114,6 +114,7 @@ class Engine {
   void load_charges_device(const double* d_q_sorted);
   void store_potentials_device(double* d_pot_sorted);
   int64_t launch_count() const { return launches_; }
+  void set_overlap(bool on) { overlap_ = on; }
   int64_t particle_begin() const { return part_b_; }
   int64_t particle_end() const { return part_e_; }
   void get_potentials_sorted(double* out, size_t cap_doubles);
@@ -127,8 +128,8 @@ class Engine {
   void build_T();
   void phase_c2m();
   void phase_m2m();
-  void phase_m2l();
-  void phase_l2l();
+  void phase_m2l(int lo = -1, int hi = -1);  // levels lo..hi (default all)
+  void phase_l2l(int lo = -1, int hi = -1);  // parent levels lo..hi (default all)
   void phase_l2t();
   void phase_near();
   template <class T>
@@ -183,6 +184,11 @@ class Engine {
   cudaEvent_t ev_[8] = {};
   // near field on a side stream, overlapped with the far-field chain
   cudaStream_t st2_ = nullptr;
+  // evaluate_device overlap: far chain (high priority) + leaf M2L (low priority)
+  cudaStream_t st_hi_ = nullptr, st_lo_ = nullptr;
+  cudaEvent_t ev_ofork_ = nullptr, ev_ojoin_ = nullptr, ev_c2m_ = nullptr, ev_m2l_leaf_ = nullptr;
+  bool overlap_ = true, overlapped_ = false;
+  cudaEvent_t ev_lf0_ = nullptr, ev_lf1_ = nullptr, ev_la_ = nullptr, ev_lb_ = nullptr;  // timing in overlap mode
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_near0_ = nullptr, ev_near1_ = nullptr;
   double2* d_pot_near = nullptr;
   bool near_started_ = false;

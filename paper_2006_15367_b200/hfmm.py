@@ -252,6 +252,11 @@ class RankEngine:
         """Async device copy of this rank's potentials (sorted, own range)."""
         check(lib().hfmm_gpu_store_potentials_device(self._h, ctypes.c_void_p(d_pot_sorted_ptr)))
 
+    def set_overlap(self, on: bool) -> None:
+        """Phase overlap in evaluate (default on); off = sequential phases whose
+        last_timing() entries are each phase's own kernel time."""
+        check(lib().hfmm_gpu_set_overlap(self._h, 1 if on else 0))
+
     def launch_count(self) -> int:
         """Kernels launched by this engine so far (cumulative)."""
         n = ctypes.c_int64()
