@@ -513,7 +513,13 @@ int theta_chunk(int half, int outs_per_circle, int threads) {
 namespace {
 // Runtime-shaped streaming kernels: any even grid pair (the host B layouts
 // K = round4(n_in + 1), N = round8(n_out) are what they expect).
-bool rbl_ok(int nc, int np) { return nc % 2 == 0 && np % 2 == 0 && std::getenv("HFMM_NO_RBL") == nullptr; }
+bool rbl_ok(int nc, int np) {
+  // shared-memory B: whole phi matrices and one theta column block must fit (227 KB)
+  const int lim = 227 * 1024;
+  const bool fits = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8 <= lim && rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8 <= lim &&
+                    rb::r4(2 * np + 1) * rb::blk_ldb(8 * rb::kChunk) * 8 <= lim;
+  return nc % 2 == 0 && np % 2 == 0 && fits && std::getenv("HFMM_NO_RBL") == nullptr;
+}
 }  // namespace
 
 void Engine::phase_m2m() {
@@ -539,11 +545,17 @@ void Engine::phase_m2m() {
     }
     if (use_rb_ && rbl_ok(nc, np)) {  // larger pairs: runtime-shaped streaming kernels
       const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+      const int s_phi = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8;
+      const int nchunk = (rb::r8(2 * np) / 8 + rb::kChunk - 1) / rb::kChunk;
+      const int s_th = rb::r4(2 * nc + 1) * rb::blk_ldb(8 * rb::kChunk) * 8;
+      ck(cudaFuncSetAttribute(k_m2m_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
+      ck(cudaFuncSetAttribute(k_m2m_theta_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_th), "attr");
       if (nch > 0)
-        k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, nch, cl.children, C.mp, P.up_phi_B, P.up_phi_v,
-                                                          d_tmp);
-      k_m2m_theta_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, cl.n_par, cl.plist, cl.child_off, cl.children,
-                                                          cl.oct_c, d_tmp, P.up_th_B, P.up_th_v, P.shift_up, P.mp);
+        k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, nch, cl.children, C.mp, P.up_phi_B, P.up_phi_v,
+                                                              d_tmp);
+      const dim3 gth(unsigned(std::max(1, 2 * sms_ / nchunk)), unsigned(nchunk));
+      k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, cl.n_par, cl.plist, cl.child_off, cl.children,
+                                                        cl.oct_c, d_tmp, P.up_th_B, P.up_th_v, P.shift_up, P.mp);
       launches_ += 2;
       ck(cudaGetLastError(), "k_m2m_rbl");
       continue;
@@ -649,11 +661,13 @@ void Engine::phase_l2l(int lo, int hi) {
     }
     if (use_rb_ && rbl_ok(nc, np)) {
       const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+      const int s_phi = rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8;
+      ck(cudaFuncSetAttribute(k_l2l_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
       k_l2l_theta_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, cl.n_par, cl.plist, cl.child_off, cl.children,
                                                           cl.oct_c, P.loc, P.dn_th_B, P.dn_th_v, P.shift_dn, d_tmp);
       if (nch > 0)
-        k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, nch, cl.children, d_tmp, P.dn_phi_B, P.dn_phi_v,
-                                                          C.loc);
+        k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, nch, cl.children, d_tmp, P.dn_phi_B, P.dn_phi_v,
+                                                              C.loc);
       launches_ += 2;
       ck(cudaGetLastError(), "k_l2l_rbl");
       continue;

@@ -370,6 +370,22 @@ namespace rb {
 #endif
 constexpr int kChunk = HFMM_RBL_CHUNK;
 
+// Rows [0, K) x columns [c0, c0 + nc) of a row-major K x N matrix -> shared
+// rows of stride ldb (cp.async 16 B; nc and c0 even).
+__device__ __forceinline__ void stage_block(double* dst, const double* __restrict__ src, int K, int N, int c0, int nc,
+                                            int ldb) {
+  const int h = nc / 2;
+  for (int t = threadIdx.x; t < K * h; t += blockDim.x) {
+    const int r = t / h, c = 2 * (t - r * h);
+    const bool ok = c0 + c < N;
+    cp_async16(dst + r * ldb + c, ok ? src + r * N + c0 + c : src, ok);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+}
+__host__ __device__ constexpr int blk_ldb(int cols) { return cols % 16 == 0 ? cols + 8 : cols; }
+
 // alpha = v . x over the K_in data columns of a complex row; fetch(k) -> double2.
 template <class Fetch>
 __device__ __forceinline__ double2 row_alpha(int kin, const double* __restrict__ v, Fetch fetch) {
@@ -390,7 +406,7 @@ __device__ __forceinline__ double2 row_alpha(int kin, const double* __restrict__
 
 // C chunk (8 complex rows x kChunk n8 tiles from n8 tile j0) over K = 4 ks:
 // column kin holds ia (rank-1), columns > kin are zero.
-template <class Fetch>
+template <bool GLOBAL_B = false, class Fetch>
 __device__ __forceinline__ void chunk_mma(int ks, int kin, double2 ia, Fetch fetch, const double* __restrict__ B, int N,
                                           int j0, int nt, double (&cre)[kChunk][2], double (&cim)[kChunk][2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
@@ -402,7 +418,7 @@ __device__ __forceinline__ void chunk_mma(int ks, int kin, double2 ia, Fetch fet
 #pragma unroll
     for (int jc = 0; jc < kChunk; ++jc)
       if (j0 + jc < nt) {
-        const double b = __ldg(bp + 4 * kk * N + 8 * jc);
+        const double b = GLOBAL_B ? __ldg(bp + 4 * kk * N + 8 * jc) : bp[4 * kk * N + 8 * jc];
         dmma884(cre[jc][0], cre[jc][1], x.x, b);
         dmma884(cim[jc][0], cim[jc][1], x.y, b);
       }
@@ -415,6 +431,9 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_phi_rbl(int nc, int np, in
                                                               const double* __restrict__ B, const double* __restrict__ v,
                                                               double2* __restrict__ F) {
   const int K = rb::r4(nc + 1), N = rb::r8(np), ks = K / 4, nt = N / 8, half = np / 2, ldf = rb::r4(2 * nc + 1);
+  const int ldb = rb::blk_ldb(N);
+  extern __shared__ __align__(16) double Bsh[];
+  rb::stage_block(Bsh, B, K, N, 0, N, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t rows = nch * nc, tiles = (rows + 7) / 8;
   for (int64_t t = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; t < tiles;
@@ -429,7 +448,7 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_phi_rbl(int nc, int np, in
     double2* Fj = F + j * half * ldf;
     for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
       double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
-      rb::chunk_mma(ks, nc, ia, fetch, B, N, j0, nt, cre, cim);
+      rb::chunk_mma(ks, nc, ia, fetch, Bsh, ldb, j0, nt, cre, cim);
       if (ok) {
 #pragma unroll
         for (int jc = 0; jc < rb::kChunk; ++jc)
@@ -458,6 +477,10 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
                                                                 double2* __restrict__ mp_p) {
   const int K = rb::r4(2 * nc + 1), N = rb::r8(2 * np), ks = K / 4, nt = N / 8, half = np / 2, ldf = K;
   const int64_t SP = int64_t(np) * np;
+  // this CTA's column block of B (kChunk n8 tiles) lives in shared memory
+  const int j0 = blockIdx.y * rb::kChunk, ldb = rb::blk_ldb(8 * rb::kChunk);
+  extern __shared__ __align__(16) double Bsh[];
+  rb::stage_block(Bsh, B, K, N, 8 * j0, 8 * rb::kChunk, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t items = int64_t(n_par) * half;
   for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
@@ -470,7 +493,7 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
     auto fetch = [&](int k) { return ok ? __ldg(frow + k) : make_double2(0.0, 0.0); };
     const double2 ia = rb::row_alpha(2 * nc, v, fetch);
     double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
-    for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
+    {
       double2 shv[rb::kChunk][2];
 #pragma unroll
       for (int jc = 0; jc < rb::kChunk; ++jc)
@@ -481,7 +504,7 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
           shv[jc][q] = (ok && n < 2 * np) ? __ldg(sh + s) : make_double2(0.0, 0.0);
         }
       double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
-      rb::chunk_mma(ks, 2 * nc, ia, fetch, B, N, j0, nt, cre, cim);
+      rb::chunk_mma(ks, 2 * nc, ia, fetch, Bsh, ldb, 0, nt - j0, cre, cim);
 #pragma unroll
       for (int jc = 0; jc < rb::kChunk; ++jc)
 #pragma unroll
@@ -515,6 +538,8 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, 
                                                                 double2* __restrict__ Nb) {
   const int K = rb::r4(2 * np + 1), N = rb::r8(2 * nc), ks = K / 4, nt = N / 8, half = np / 2, ldn = rb::r4(np + 1);
   const int64_t SP = int64_t(np) * np;
+  // (B through L1/L2, all column chunks per warp: this pass's A values are
+  // built on the fly from L_p x shift, so they are not re-built per chunk CTA.)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t items = int64_t(n_par) * half;
   for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
@@ -534,7 +559,7 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, 
     double2* Nc = Nb + int64_t(cb + (ok ? c : 0)) * nc * ldn;
     for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
       double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
-      rb::chunk_mma(ks, 2 * np, ia, fetch, B, N, j0, nt, cre, cim);
+      rb::chunk_mma<true>(ks, 2 * np, ia, fetch, B, N, j0, nt, cre, cim);
       if (ok) {
 #pragma unroll
         for (int jc = 0; jc < rb::kChunk; ++jc)
@@ -557,6 +582,9 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_phi_rbl(int nc, int np, in
                                                               const double* __restrict__ B, const double* __restrict__ v,
                                                               double2* __restrict__ loc_c) {
   const int K = rb::r4(np + 1), N = rb::r8(nc), ks = K / 4, nt = N / 8, ldn = K;
+  const int ldb = rb::blk_ldb(N);
+  extern __shared__ __align__(16) double Bsh[];
+  rb::stage_block(Bsh, B, K, N, 0, N, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t rows = nch * nc, tiles = (rows + 7) / 8;
   for (int64_t t = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; t < tiles;
@@ -579,7 +607,7 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_phi_rbl(int nc, int np, in
           old[jc][q] = (ok && j0 + jc < nt && n < nc) ? dst[n] : make_double2(0.0, 0.0);
         }
       double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
-      rb::chunk_mma(ks, np, ia, fetch, B, N, j0, nt, cre, cim);
+      rb::chunk_mma(ks, np, ia, fetch, Bsh, ldb, j0, nt, cre, cim);
       if (ok) {
 #pragma unroll
         for (int jc = 0; jc < rb::kChunk; ++jc)
