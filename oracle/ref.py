@@ -89,6 +89,38 @@ def generate_geometry(kind: str, extent: float, spacing: float, lam: float = 1.0
     return pos, q
 
 
+_IO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref", "particles_io")
+
+
+def read_particles(path: str):
+    """hfmm::read_particles (geometry.cpp:128-148) -> (positions (n, 3), charges (n, 2)).
+    Runs out of process (oracle/particles_io.cpp); parse errors raise RefError."""
+    import subprocess
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".bin") as tmp:
+        r = subprocess.run([_IO, "read", path, tmp.name], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RefError(r.returncode, r.stderr.strip())
+        raw = open(tmp.name, "rb").read()
+    n = int(np.frombuffer(raw[:8], np.uint64)[0])
+    v = np.frombuffer(raw[8:], np.float64)
+    return v[:3 * n].reshape(n, 3).copy(), v[3 * n:5 * n].reshape(n, 2).copy()
+
+
+def write_particles(path: str, pos, q, header: str = "") -> None:
+    """hfmm::write_particles (geometry.cpp:150-159), out of process."""
+    import subprocess
+    import tempfile
+    pos = np.ascontiguousarray(pos, np.float64)
+    q = np.ascontiguousarray(q, np.float64)
+    with tempfile.NamedTemporaryFile(suffix=".bin") as tmp:
+        tmp.write(np.uint64(pos.shape[0]).tobytes() + pos.tobytes() + q.tobytes())
+        tmp.flush()
+        r = subprocess.run([_IO, "write", tmp.name, path, header], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RefError(r.returncode, r.stderr.strip())
+
+
 class RefSetup:
     """hfmm::build_setup on the reference, with the flat dump accessors."""
 
