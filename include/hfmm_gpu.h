@@ -62,6 +62,13 @@ typedef struct hfmm_run_config {
   int32_t d_override;   /* 0 = classify from geometry            */
   int32_t scheduler;    /* 0 deterministic, 1 adversarial, 2 threaded */
   uint64_t seed;
+  /* Leaf weights of the Morton partition (partition_leaves, tree.cpp:19-75):
+   * 0 = particles per leaf, the reference's rule (traversal.cpp:128-131; the
+   * setup is bit-exact with the reference only in this mode); 1 = near-field
+   * pairs per leaf, n_leaf * sum of its near leaves' populations (opt-in load
+   * balance for P2P-dominated geometries). */
+  int32_t partition_weight;
+  int32_t reserved0;
 } hfmm_run_config;
 
 /* Fills the reference defaults (RunConfig{} in traversal.hpp:21-35). */

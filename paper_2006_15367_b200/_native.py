@@ -68,6 +68,8 @@ class RunConfigC(ctypes.Structure):
         ("d_override", ctypes.c_int32),
         ("scheduler", ctypes.c_int32),
         ("seed", ctypes.c_uint64),
+        ("partition_weight", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
     ]
 
 

@@ -82,6 +82,7 @@ void hfmm_run_config_default(hfmm_run_config* c) {
   c->d_override = 0;
   c->scheduler = 0;
   c->seed = 0;
+  c->partition_weight = 0;
 }
 
 const char* hfmm_last_error(void) { return g_err.c_str(); }

@@ -317,6 +317,24 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
 
   std::vector<uint64_t> weights(nl);
   for (size_t i = 0; i < nl; ++i) weights[i] = s.leaf_start[i + 1] - s.leaf_start[i];
+  if (cfg.partition_weight == 1) {
+    // near-field pairs per leaf: n_i * sum over its near leaves (self included)
+    LevelData t;
+    t.level = L;
+    t.codes = s.leaf_codes;
+    std::vector<uint64_t> pairs(nl, 0);
+    for (size_t i = 0; i < nl; ++i) {
+      uint64_t srcs = 0;
+      for_neighbors(t, t.codes[i], [&](uint64_t nc) {
+        const int64_t j = t.find(nc);
+        srcs += s.leaf_start[size_t(j) + 1] - s.leaf_start[size_t(j)];
+      });
+      pairs[i] = weights[i] * srcs;
+    }
+    weights.swap(pairs);
+  } else if (cfg.partition_weight != 0) {
+    throw std::invalid_argument("build_setup: partition_weight must be 0 (particles) or 1 (near pairs)");
+  }
   partition(s, weights);
 
   // Per-level node sets for every level 1..L (collect_level_nodes,

@@ -59,6 +59,9 @@ class RunConfig:
     scheduler: SchedulerKind = SchedulerKind.Deterministic
     top_level: int = 3
     d_override: int = 0
+    # Morton-partition leaf weights: 0 = particles (the reference's rule,
+    # bit-exact setup), 1 = near-field pairs per leaf (opt-in P2P load balance)
+    partition_weight: int = 0
 
     def validate(self) -> None:
         """RunConfig::validate (traversal.cpp:42-46)."""
@@ -70,7 +73,8 @@ class RunConfig:
         return _native.RunConfigC(
             float(self.lambda_), float(self.digits), float(self.leaf_lambda), int(self.num_ranks),
             int(self.policy), int(self.buffer_limit), int(bool(self.one_particle_per_leaf)),
-            int(self.top_level), int(self.d_override), int(self.scheduler), int(self.seed))
+            int(self.top_level), int(self.d_override), int(self.scheduler), int(self.seed),
+            int(self.partition_weight), 0)
 
 
 def _as_particles(positions, intensities):

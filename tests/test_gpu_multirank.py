@@ -61,16 +61,17 @@ def _run_ranks(hb, setup, q, engs):
     return pot
 
 
-@pytest.mark.parametrize("ranks,case", [
-    (2, ("cube", 30_000, 3.0, 61, 3.0)),
-    (3, ("sphere", 40_000, 2.0, 62, 4.0)),
-    (4, ("cube", 20_000, 2.5, 63, 6.0)),
+@pytest.mark.parametrize("ranks,case,pw", [
+    (2, ("cube", 30_000, 3.0, 61, 3.0), 0),
+    (3, ("sphere", 40_000, 2.0, 62, 4.0), 0),
+    (4, ("cube", 20_000, 2.5, 63, 6.0), 0),
+    (4, ("sphere", 40_000, 2.0, 62, 4.0), 1),  # near-pair-weighted partition (opt-in)
 ])
-def test_ranks_emulated_on_one_gpu(ranks, case, native, refo):
+def test_ranks_emulated_on_one_gpu(ranks, case, pw, native, refo):
     import paper_2006_15367_b200 as hb
     shape, n, ext, seed, dig = case
     pos, q = hb.generate_inputs(shape, n, ext, seed)
-    setup = hb.build_setup(pos, q, hb.RunConfig(digits=dig, num_ranks=ranks))
+    setup = hb.build_setup(pos, q, hb.RunConfig(digits=dig, num_ranks=ranks, partition_weight=pw))
     engs = [hb.RankEngine(setup, r, 0) for r in range(ranks)]
     l0 = [e.launch_count() for e in engs]
     pot_sorted = _run_ranks(hb, setup, q, engs)
