@@ -11,6 +11,7 @@
 #include "interp.hpp"
 #include "kernels.cuh"
 #include "m2l.cuh"
+#include "p2p.cuh"
 #include "m2l_tc.cuh"
 #include "interp_rb.cuh"
 #include "interp_tc.cuh"
@@ -249,36 +250,73 @@ void Engine::upload() {
     d_tiny_leaves_ = upload_vec(tiny);
     d_small_leaves_ = upload_vec(small);
     d_dense_leaves_ = upload_vec(dense);
-    // symmetric pair lists among own dense leaves (k_p2p_sym / k_p2p_gather)
+    // symmetric pair lists among own dense leaves (k_p2p_sym2 / k_p2p_gather).
+    // k_p2p_sym2 runs one CTA per (leaf, pass of 128 observers): each pass
+    // writes its own scratch rows (no read-modify-write across CTAs), and
+    // the gather adds them in (sender leaf, pass) order, so sums are
+    // deterministic.  HFMM_P2P_V1 selects the previous kernel (one CTA per
+    // leaf, one scratch row per pair) for A/B.
+    use_sym_ = std::getenv("HFMM_P2P_NOSYM") == nullptr;
+    p2p_v1_ = std::getenv("HFMM_P2P_V1") != nullptr;
+    const int obs_pass = 32 * kP2PObsPerLane;
+    auto pop = [&](int64_t lf) { return int64_t(s.leaf_start[size_t(lf) + 1] - s.leaf_start[size_t(lf)]); };
     std::vector<int> pos(s.num_leaves(), -1);
     for (size_t i = 0; i < dense.size(); ++i) pos[size_t(dense[i])] = int(i);
     std::vector<int> poff{0}, pl, soff{0}, sl;
-    std::vector<int64_t> sscr;
-    std::vector<std::vector<std::pair<int, int64_t>>> incoming(dense.size());
+    std::vector<int64_t> sscr, srows;
+    std::vector<std::vector<std::pair<std::pair<int, int>, int64_t>>> incoming(dense.size());
+    std::vector<std::pair<int64_t, int2>> items[4];  // by slots per lane - 1: (cost, {leaf idx, pass})
     int64_t scr = 0;
     for (size_t i = 0; i < dense.size(); ++i) {
       const int a = dense[i];
+      const int64_t na = pop(a);
+      const int npass = p2p_v1_ ? 1 : int((na + obs_pass - 1) / obs_pass);
+      int64_t rows = 0, plain_src = 0;
+      const size_t sb = sl.size();
       for (uint64_t z2 = s.near_off[size_t(a)]; z2 < s.near_off[size_t(a) + 1]; ++z2) {
         const int b = int(s.near[z2]);
         if (b > a && pos[size_t(b)] >= 0) {
           sl.push_back(b);
-          sscr.push_back(scr);
-          incoming[size_t(pos[size_t(b)])].push_back({a, scr});
-          scr += int64_t(s.leaf_start[size_t(b) + 1] - s.leaf_start[size_t(b)]);
+          sscr.push_back(scr + rows);
+          rows += pop(b);
         } else if (b == a || pos[size_t(b)] < 0) {
           pl.push_back(b);
+          plain_src += pop(b);
         }
       }
+      for (size_t jj = sb; jj < sl.size(); ++jj)
+        for (int p = 0; p < npass; ++p)
+          incoming[size_t(pos[size_t(sl[jj])])].push_back({{a, p}, sscr[jj] + int64_t(p) * rows});
+      for (int p = 0; p < npass; ++p) {
+        const int64_t no = std::min<int64_t>(na - int64_t(p) * obs_pass, obs_pass);
+        const int nc = int((no + 31) / 32);
+        items[nc - 1].push_back({int64_t(nc) * (plain_src + rows), make_int2(int(i), p)});
+      }
+      srows.push_back(rows);
+      scr += int64_t(npass) * rows;
       poff.push_back(int(pl.size()));
       soff.push_back(int(sl.size()));
     }
     std::vector<int> ioff{0};
     std::vector<int64_t> iscr;
-    for (auto& v : incoming) {  // senders in ascending leaf order: deterministic sums
+    for (auto& v : incoming) {  // senders in ascending (leaf, pass) order: deterministic sums
       std::sort(v.begin(), v.end());
       for (auto& e : v) iscr.push_back(e.second);
       ioff.push_back(int(iscr.size()));
     }
+    // work items per slot count, most expensive first (LPT order)
+    std::vector<int2> it;
+    for (int c = 3; c >= 0; --c) {
+      std::stable_sort(items[c].begin(), items[c].end(),
+                       [](const std::pair<int64_t, int2>& u, const std::pair<int64_t, int2>& v) {
+                         return u.first > v.first;
+                       });
+      p2p_items_b_[c] = int(it.size());
+      for (auto& e : items[c]) it.push_back(e.second);
+      p2p_items_n_[c] = int(items[c].size());
+    }
+    d_p2p_items_ = upload_vec(it);
+    d_sym_rows_ = upload_vec(srows);
     d_plain_off_ = upload_vec(poff);
     d_plain_ = upload_vec(pl);
     d_sym_off_ = upload_vec(soff);
@@ -287,7 +325,6 @@ void Engine::upload() {
     d_in_off_ = upload_vec(ioff);
     d_in_scr_ = upload_vec(iscr);
     d_p2p_scratch_ = alloc<double2>(size_t(std::max<int64_t>(scr, 1)));
-    use_sym_ = std::getenv("HFMM_P2P_NOSYM") == nullptr;
   }
 
   lv_.assign(size_t(L + 1), DevLevel{});
@@ -766,9 +803,23 @@ void Engine::near_start() {
     ++launches_;
   }
   if (n_dense_ > 0 && use_sym_) {
-    k_p2p_sym<<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_, d_sym_off_,
-                                                    d_sym_, d_sym_scr_, d.centers, d_x, d_y, d_z, d_q, s_.k,
-                                                    d_pot_near, d_p2p_scratch_);
+    if (p2p_v1_)
+      k_p2p_sym<<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_,
+                                                      d_sym_off_, d_sym_, d_sym_scr_, d.centers, d_x, d_y, d_z, d_q,
+                                                      s_.k, d_pot_near, d_p2p_scratch_);
+    else
+      for (int c = 3; c >= 0; --c) {
+        if (p2p_items_n_[c] == 0) continue;
+        const int2* itm = d_p2p_items_ + p2p_items_b_[c];
+        const unsigned g = unsigned(p2p_items_n_[c]);
+#define HFMM_SYM2(NC)                                                                                               \
+  k_p2p_sym2<NC><<<g, 128, 0, st2_>>>(itm, d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_, d_sym_off_, d_sym_, \
+                                      d_sym_scr_, d_sym_rows_, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near,     \
+                                      d_p2p_scratch_)
+        if (c == 3) HFMM_SYM2(4); else if (c == 2) HFMM_SYM2(3); else if (c == 1) HFMM_SYM2(2); else HFMM_SYM2(1);
+#undef HFMM_SYM2
+        ++launches_;
+      }
     k_p2p_gather<<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_in_off_, d_in_scr_,
                                                        d_p2p_scratch_, d_pot_near);
     launches_ += 2;
@@ -879,7 +930,9 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
     ck(cudaStreamWaitEvent(st_hi_, ev_ofork_, 0), "fork wait");
     st_ = st_hi_;
   }
-  near_start();  // side stream, overlapped with the far-field chain
+  // Near field: side stream, overlapped with the far-field chain; in the
+  // sequential mode (set_overlap off) it runs after L2T, inside phase_near.
+  if (overlap_) near_start();
   build_T();
   cudaEventRecord(ev_[1], st_);
   phase_c2m();

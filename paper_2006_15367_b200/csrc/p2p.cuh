@@ -1,0 +1,260 @@
+// Near-field P2P, symmetric dense-leaf kernel (operators.cpp:110-122 with
+// green kernel.cpp:9-14, driver traversal.cpp:768-786).  Same pair algebra
+// and leaf schedule as k_p2p_sym (kernels.cuh), organised for the FP64 pipe:
+//
+//  * the scaled kernel g' = exp(-i r') / r' (r' = k r) costs 42 FP64
+//    instructions: 6 for r'^2, 6 for 1/r' and r' (MUFU.RSQ64H + one cubic
+//    Newton step, no special-case branch: r'^2 > 0 here), 20 for sincos
+//    (Cody-Waite by pi/2 + fdlibm's degree 13/14 kernels), 2 for g' and 8
+//    for the two complex multiply-adds (A <- B and B <- A).  The quadrant
+//    swap is a select and the quadrant signs are XORed into 1/r' (integer
+//    pipe), so no FP64 negations;
+//  * each lane evaluates its NC observers in lockstep (independent chains
+//    side by side for the scheduler), NC a template parameter so a pass with
+//    fewer than 4 observer slots does no padded work;
+//  * a warp takes M partner sources per iteration and reduces their M
+//    B-side sums with one split butterfly (M - 1 + 5 - log2 M shuffle steps
+//    instead of 5 M).
+#ifndef HFMM_B200_P2P_CUH
+#define HFMM_B200_P2P_CUH
+
+#include "kernels.cuh"
+
+namespace hfmm_b200 {
+
+// exp(-i r') / r' from r'^2 > 0 (finite): (gr, gi).
+__device__ __forceinline__ void green_scaled(double r2, double& gr, double& gi) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double t = r2 * y0;
+  const double e = fma(-t, y0, 1.0);  // 1 - r2 y0^2
+  const double p = fma(e, 0.375, 0.5);
+  const double ri = fma(y0 * e, p, y0);  // 1 / r'
+  const double x = r2 * ri;             // r'
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double tq = fma(x, kSinCos[12], kMagic);
+  const int quad = __double2loint(tq);
+  const double n = tq - kMagic;
+  double y = fma(n, -1.5707963267948966, x);
+  y = fma(n, kSinCos[13], y);
+  const double y2 = y * y;
+  double ps = kSinCos[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) ps = fma(ps, y2, kSinCos[i]);
+  const double sn = fma(ps * y2, y, y);
+  double pc = kSinCos[6];
+#pragma unroll
+  for (int i = 7; i < 12; ++i) pc = fma(pc, y2, kSinCos[i]);
+  const double cs = fma(pc, y2 * y2, fma(-0.5, y2, 1.0));
+  // exp(-i (y + quad pi/2)) = (cos y - i sin y) (-i)^quad:
+  //   quad 0: ( c, -s)   1: (-s, -c)   2: (-c,  s)   3: ( s,  c)
+  const bool swap = quad & 1;
+  const double mr = swap ? sn : cs, mi = swap ? cs : sn;
+  const unsigned q30 = unsigned(quad) << 30;
+  const unsigned sr = (q30 + 0x40000000u) & 0x80000000u;  // re < 0 for quad 1, 2
+  const unsigned si = ~q30 & 0x80000000u;                 // im < 0 for quad 0, 1
+  const int rhi = __double2hiint(ri), rlo = __double2loint(ri);
+  gr = mr * __hiloint2double(rhi ^ int(sr), rlo);
+  gi = mi * __hiloint2double(rhi ^ int(si), rlo);
+}
+
+// Symmetric dense-leaf near field: as k_p2p_sym (same lists, scratch layout
+// and gather), with the pair loop above.  Block = 128 threads.
+template <int NC, int M>
+__device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double k, double cx, double cy,
+                                             double cz, double qs, int64_t p0, int64_t total,
+                                             const int* __restrict__ sym, int j0, int j1,
+                                             const int64_t* __restrict__ sym_scr, int64_t scr_pass,
+                                             const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
+                                             const double* __restrict__ y, const double* __restrict__ z,
+                                             const double2* __restrict__ q, double2* __restrict__ pot,
+                                             double2* __restrict__ scratch, double2 (*red)[32 * kP2PObsPerLane]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  double xo[NC], yo[NC], zo[NC], qr[NC], qi[NC], ar[NC], ai[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int o = lane + 32 * c;
+    const bool v = o < n_o_pass;
+    // idle slots: far away but finite, zero charge -> exact-zero terms
+    xo[c] = v ? k * (x[p0 + o] - cx) : 1.0e4;
+    yo[c] = v ? k * (y[p0 + o] - cy) : 0.0;
+    zo[c] = v ? k * (z[p0 + o] - cz) : 0.0;
+    const double2 qq = v ? q[p0 + o] : make_double2(0.0, 0.0);
+    qr[c] = qs * qq.x;
+    qi[c] = qs * qq.y;
+    ar[c] = 0.0;
+    ai[c] = 0.0;
+  }
+  // one-sided part: self leaf + small / ghost neighbours (exact-zero
+  // separation masked, operators.cpp:118)
+  for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
+    const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
+    __syncthreads();
+    p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
+    __syncthreads();
+    for (int t = warp; t < n; t += nwarp) {
+      const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
+      const double2 qq = sh.sq[t];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const bool self = r2 == 0.0;
+        double gr, gi;
+        green_scaled(self ? 1.0 : r2, gr, gi);
+        gr = self ? 0.0 : gr;
+        gi = self ? 0.0 : gi;
+        ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
+        ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
+      }
+    }
+  }
+  // symmetric part: dense partners B > A; M sources per warp iteration
+  for (int j = j0; j < j1; ++j) {
+    const int lb = sym[j];
+    const int64_t b0 = leaf_start[lb], nbp = leaf_start[lb + 1] - b0;
+    double2* scr = scratch + sym_scr[j] + scr_pass;
+    for (int64_t cb = 0; cb < nbp; cb += kP2PChunk) {
+      const int n = int(nbp - cb < kP2PChunk ? nbp - cb : kP2PChunk);
+      const int npad = (n + M - 1) / M * M;
+      __syncthreads();
+      for (int t = threadIdx.x; t < npad; t += blockDim.x) {
+        if (t < n) {
+          const int64_t src = b0 + cb + t;
+          sh.sx[t] = k * (x[src] - cx);
+          sh.sy[t] = k * (y[src] - cy);
+          sh.sz[t] = k * (z[src] - cz);
+          const double2 qq = q[src];
+          sh.sq[t] = make_double2(qs * qq.x, qs * qq.y);
+        } else {  // padding source: far, zero charge
+          sh.sx[t] = -1.0e4;
+          sh.sy[t] = 0.0;
+          sh.sz[t] = 0.0;
+          sh.sq[t] = make_double2(0.0, 0.0);
+        }
+      }
+      __syncthreads();
+      for (int t = warp * M; t < npad; t += nwarp * M) {
+        double br[M], bi[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const double px = sh.sx[t + m], py = sh.sy[t + m], pz = sh.sz[t + m];
+          const double2 qq = sh.sq[t + m];
+          br[m] = 0.0;
+          bi[m] = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
+            double gr, gi;
+            green_scaled(fma(dz, dz, fma(dy, dy, dx * dx)), gr, gi);
+            ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
+            ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
+            br[m] = fma(gr, qr[c], fma(-gi, qi[c], br[m]));
+            bi[m] = fma(gr, qi[c], fma(gi, qr[c], bi[m]));
+          }
+        }
+        // split butterfly: after the first log2(M) steps lane group g holds
+        // the partial of source g, then a plain butterfly over the rest
+        int width = 16;
+        int cnt = M;
+#pragma unroll
+        for (int s = 0; (1 << s) < M; ++s) {
+          const bool hi = lane & width;
+          cnt >>= 1;
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            if (m >= cnt) break;
+            const double sr = hi ? br[m] : br[m + cnt], si = hi ? bi[m] : bi[m + cnt];
+            const double kr = hi ? br[m + cnt] : br[m], ki = hi ? bi[m + cnt] : bi[m];
+            br[m] = kr + __shfl_xor_sync(0xffffffffu, sr, width);
+            bi[m] = ki + __shfl_xor_sync(0xffffffffu, si, width);
+          }
+          width >>= 1;
+        }
+        double vr = br[0], vi = bi[0];
+        for (int off = width; off > 0; off >>= 1) {
+          vr += __shfl_xor_sync(0xffffffffu, vr, off);
+          vi += __shfl_xor_sync(0xffffffffu, vi, off);
+        }
+        // lane group g (of 32 / M lanes) holds source index sidx(g): the
+        // split keeps the upper half's source in the upper lanes
+        if ((lane & (32 / M - 1)) == 0) {
+          int sidx = 0, w2 = 16;
+#pragma unroll
+          for (int s = 0, c2 = M; (1 << s) < M; ++s) {
+            c2 >>= 1;
+            if (lane & w2) sidx += c2;
+            w2 >>= 1;
+          }
+          const int tt = t + sidx;
+          if (tt < n) scr[cb + tt] = make_double2(vr, vi);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) red[warp][lane + 32 * c] = make_double2(ar[c], ai[c]);
+  __syncthreads();
+  for (int o = threadIdx.x; o < n_o_pass; o += blockDim.x) {
+    double2 sum = red[0][o];
+    for (int w = 1; w < nwarp; ++w) {
+      sum.x += red[w][o].x;
+      sum.y += red[w][o].y;
+    }
+    double2 cur = pot[p0 + o];
+    cur.x += sum.x;
+    cur.y += sum.y;
+    pot[p0 + o] = cur;
+  }
+  __syncthreads();
+}
+
+#ifndef HFMM_P2P_M
+#define HFMM_P2P_M 4
+#endif
+
+// One CTA per work item {dense leaf index, pass}: the pass's observers
+// (ob = 128 pass, NC slots per lane) against the leaf's one-sided list and
+// its symmetric partners; pass p writes the scratch rows sym_scr + p rows.
+template <int NC>
+__global__ void __launch_bounds__(128, 4) k_p2p_sym2(const int2* __restrict__ items, const int* __restrict__ leaves,
+                                                     const int64_t* __restrict__ leaf_start,
+                                                     const int* __restrict__ plain_off, const int* __restrict__ plain,
+                                                     const int* __restrict__ sym_off, const int* __restrict__ sym,
+                                                     const int64_t* __restrict__ sym_scr,
+                                                     const int64_t* __restrict__ sym_rows,
+                                                     const double* __restrict__ centers, const double* __restrict__ x,
+                                                     const double* __restrict__ y, const double* __restrict__ z,
+                                                     const double2* __restrict__ q, double k,
+                                                     double2* __restrict__ pot, double2* __restrict__ scratch) {
+  __shared__ P2PShared sh;
+  __shared__ double2 red[4][32 * kP2PObsPerLane];
+  const int2 item = items[blockIdx.x];
+  const int i = item.x, pass = item.y;
+  const int64_t leaf = leaves[i];
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
+  if (threadIdx.x == 0) {
+    const int b = plain_off[i], nn = plain_off[i + 1] - b;
+    int64_t run = 0;
+    for (int j = 0; j < nn; ++j) {
+      const int lf = plain[b + j];
+      sh.pref[j] = run;
+      sh.nbeg[j] = leaf_start[lf];
+      run += leaf_start[lf + 1] - leaf_start[lf];
+    }
+    sh.pref[nn] = run;
+    sh.nn = nn;
+  }
+  __syncthreads();
+  const int64_t total = sh.pref[sh.nn];
+  const int ob = pass * 32 * kP2PObsPerLane;
+  const int no = min(int(p1 - p0) - ob, 32 * kP2PObsPerLane);
+  p2p_sym_pass<NC, HFMM_P2P_M>(sh, no, k, cx, cy, cz, qs, p0 + ob, total, sym, sym_off[i], sym_off[i + 1],
+                               sym_scr, int64_t(pass) * sym_rows[i], leaf_start, x, y, z, q, pot, scratch, red);
+}
+
+}  // namespace hfmm_b200
+
+#endif  // HFMM_B200_P2P_CUH
