@@ -12,6 +12,7 @@
 #include "kernels.cuh"
 #include "m2l.cuh"
 #include "p2p.cuh"
+#include "leaf.cuh"
 #include "m2l_tc.cuh"
 #include "interp_rb.cuh"
 #include "interp_tc.cuh"
@@ -258,6 +259,7 @@ void Engine::upload() {
     // leaf, one scratch row per pair) for A/B.
     use_sym_ = std::getenv("HFMM_P2P_NOSYM") == nullptr;
     p2p_v1_ = std::getenv("HFMM_P2P_V1") != nullptr;
+    leaf_v1_ = std::getenv("HFMM_LEAF_V1") != nullptr;
     const int obs_pass = 32 * kP2PObsPerLane;
     auto pop = [&](int64_t lf) { return int64_t(s.leaf_start[size_t(lf) + 1] - s.leaf_start[size_t(lf)]); };
     std::vector<int> pos(s.num_leaves(), -1);
@@ -530,7 +532,10 @@ bool quad_ok(const DevLevel& d) {
 void Engine::phase_c2m() {
   const DevLevel& d = lv_[size_t(s_.L)];
   const int64_t nl = leaf_e_ - leaf_b_;
-  if (quad_ok(d))
+  if (quad_ok(d) && !leaf_v1_)
+    k_c2m_quad2<<<unsigned((nl + 3) / 4), 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,
+                                                         d.dir, d.nt, s_.k, d.mp);
+  else if (quad_ok(d))
     k_c2m_quad<<<unsigned((nl + 3) / 4), 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,
                                                          d.dir, d.nt, s_.k, d.mp);
   else
@@ -768,8 +773,15 @@ void Engine::phase_l2t() {
     const size_t smem = 4 * size_t(kQuadP * (d.nt / 2)) * sizeof(double2);
     if (smem > 48 * 1024)
       ck(cudaFuncSetAttribute(k_l2t_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-    k_l2t_quad<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,
-                                                            d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+    if (leaf_v1_) {
+      k_l2t_quad<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,
+                                                              d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+    } else {
+      if (smem > 48 * 1024)
+        ck(cudaFuncSetAttribute(k_l2t_quad2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+      k_l2t_quad2<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,
+                                                               d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+    }
   } else {
     const size_t smem = size_t(d.S) * (sizeof(double2) + 3 * sizeof(double));
     if (smem > 48 * 1024)

@@ -180,7 +180,8 @@ class Engine {
   int2* d_p2p_items_ = nullptr;  // k_p2p_sym2 work items {dense leaf idx, pass}, grouped by slots per lane
   int64_t* d_sym_rows_ = nullptr;
   int p2p_items_b_[4] = {0, 0, 0, 0}, p2p_items_n_[4] = {0, 0, 0, 0};
-  bool p2p_v1_ = false;  // HFMM_P2P_V1: the previous symmetric kernel (A/B)
+  bool p2p_v1_ = false;
+  bool leaf_v1_ = false;  // HFMM_LEAF_V1: the previous quad C2M / L2T kernels (A/B)  // HFMM_P2P_V1: the previous symmetric kernel (A/B)
   double2* d_tmp = nullptr;  // interpolation temporaries
   size_t tmp_elems_ = 0;
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range

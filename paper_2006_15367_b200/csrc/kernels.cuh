@@ -560,15 +560,51 @@ __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __re
 constexpr int kP2PChunk = 512;
 constexpr int kP2PObsPerLane = 4;  // dense leaves: 32 x 4 observers per pass (measured best of 2..8)
 
+// exp(-i r') / r' from r'^2 > 0 (finite): (gr, gi).
+__device__ __forceinline__ void green_scaled(double r2, double& gr, double& gi) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double t = r2 * y0;
+  const double e = fma(-t, y0, 1.0);  // 1 - r2 y0^2
+  const double p = fma(e, 0.375, 0.5);
+  const double ri = fma(y0 * e, p, y0);  // 1 / r'
+  const double x = r2 * ri;             // r'
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double tq = fma(x, kSinCos[12], kMagic);
+  const int quad = __double2loint(tq);
+  const double n = tq - kMagic;
+  double y = fma(n, -1.5707963267948966, x);
+  y = fma(n, kSinCos[13], y);
+  const double y2 = y * y;
+  double ps = kSinCos[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) ps = fma(ps, y2, kSinCos[i]);
+  const double sn = fma(ps * y2, y, y);
+  double pc = kSinCos[6];
+#pragma unroll
+  for (int i = 7; i < 12; ++i) pc = fma(pc, y2, kSinCos[i]);
+  const double cs = fma(pc, y2 * y2, fma(-0.5, y2, 1.0));
+  // exp(-i (y + quad pi/2)) = (cos y - i sin y) (-i)^quad:
+  //   quad 0: ( c, -s)   1: (-s, -c)   2: (-c,  s)   3: ( s,  c)
+  const bool swap = quad & 1;
+  const double mr = swap ? sn : cs, mi = swap ? cs : sn;
+  const unsigned q30 = unsigned(quad) << 30;
+  const unsigned sr = (q30 + 0x40000000u) & 0x80000000u;  // re < 0 for quad 1, 2
+  const unsigned si = ~q30 & 0x80000000u;                 // im < 0 for quad 0, 1
+  const int rhi = __double2hiint(ri), rlo = __double2loint(ri);
+  gr = mr * __hiloint2double(rhi ^ int(sr), rlo);
+  gi = mi * __hiloint2double(rhi ^ int(si), rlo);
+}
+
 __device__ __forceinline__ void p2p_pair(double xo, double yo, double zo, double sx, double sy, double sz,
                                          double2 qq, double& ar, double& ai) {
   const double dx = xo - sx, dy = yo - sy, dz = zo - sz;
   const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-  const bool self = r2 == 0.0;
-  const double ri = rsqrt(self ? 1.0 : r2);
-  double sn, cs;
-  sincos_fast(-(r2 * ri), &sn, &cs);  // exp(-i r')
-  const double gr = self ? 0.0 : cs * ri, gi = self ? 0.0 : sn * ri;
+  const bool self = r2 == 0.0;  // exact-zero separation (operators.cpp:118)
+  double gr, gi;
+  green_scaled(self ? 1.0 : r2, gr, gi);
+  gr = self ? 0.0 : gr;
+  gi = self ? 0.0 : gi;
   ar = fma(gr, qq.x, fma(-gi, qq.y, ar));
   ai = fma(gr, qq.y, fma(gi, qq.x, ai));
 }

@@ -1,0 +1,217 @@
+// Quad-symmetric C2M and L2T with factored phase sums (operators.cpp:15-26
+// and :89-108; drivers traversal.cpp:306-320 and :717-728).
+//
+// The four samples of a quad, (i, j), (n-1-i, j), (i, j+n/2), (n-1-i, j+n/2),
+// have phases +-A +-B with A = k sin(theta_i)(x cos(phi_j) + y sin(phi_j))
+// and B = k z cos(theta_i) (see k_c2m_quad, kernels.cuh).  B depends only on
+// the particle and the theta row, so each kernel folds it into a per-warp
+// table first and spends per (quad, particle) one sincos of A plus 8 FMA:
+//
+//  C2M: with Q+ = q e^{iB}, Q- = q e^{-iB} (table per particle and row),
+//       M(i,j) = sum Q+ e^{iA}, M(n-1-i,j) = sum Q- e^{iA},
+//       M(i,j+n/2) = sum Q+ e^{-iA}, M(n-1-i,j+n/2) = sum Q- e^{-iA};
+//       accumulating Re(Q.) e^{iA} and Im(Q.) e^{iA} separately gives all
+//       four from 8 real FMA (vs 16 for four complex MACs).
+//  L2T: with G = L1+L2+L3+L4, H = L2-L1+L4-L3, G' = L3+L4-L1-L2,
+//       H' = L1-L2-L3+L4 (weighted locals of the quad, formed once per
+//       observer pass),  sum_quad = cos B (cos A G + i sin A G')
+//                                 + sin B (i cos A H - sin A H').
+//
+// The sincos here applies the quadrant signs by XOR on the high word
+// (integer pipe) instead of FP64 negations.  FP64 per (quad, particle):
+// 2 (argument) + 20 (sincos) + 8 (C2M) or 12 (L2T), against 48 before.
+#ifndef HFMM_B200_LEAF_CUH
+#define HFMM_B200_LEAF_CUH
+
+#include "kernels.cuh"
+
+namespace hfmm_b200 {
+
+__device__ __forceinline__ double xor_sign(double v, unsigned s) {
+  return __hiloint2double(__double2hiint(v) ^ int(s), __double2loint(v));
+}
+
+// sin, cos of |x| < 2^20 (same reduction and kernels as sincos_fast).
+__device__ __forceinline__ void sincos_q(double x, double& sp, double& cp) {
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double t = fma(x, kSinCos[12], kMagic);
+  const int quad = __double2loint(t);
+  const double n = t - kMagic;
+  double y = fma(n, -1.5707963267948966, x);
+  y = fma(n, kSinCos[13], y);
+  const double y2 = y * y;
+  double ps = kSinCos[0];
+#pragma unroll
+  for (int i = 1; i < 6; ++i) ps = fma(ps, y2, kSinCos[i]);
+  const double sn = fma(ps * y2, y, y);
+  double pc = kSinCos[6];
+#pragma unroll
+  for (int i = 7; i < 12; ++i) pc = fma(pc, y2, kSinCos[i]);
+  const double cs = fma(pc, y2 * y2, fma(-0.5, y2, 1.0));
+  const bool swap = quad & 1;
+  const unsigned q30 = unsigned(quad) << 30;
+  sp = xor_sign(swap ? cs : sn, q30 & 0x80000000u);                  // sin < 0 for quad 2, 3
+  cp = xor_sign(swap ? sn : cs, (q30 + 0x40000000u) & 0x80000000u);  // cos < 0 for quad 1, 2
+}
+
+constexpr int kQuadP2 = 16;  // particles per table chunk
+
+__global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
+                                                   const double* __restrict__ x, const double* __restrict__ y,
+                                                   const double* __restrict__ z, const double2* __restrict__ q,
+                                                   const double* __restrict__ centers, const double* __restrict__ dir,
+                                                   int n, double k, double2* __restrict__ mp) {
+  __shared__ double4 sQ[4][kQuadP2][kQuadHalfMax];  // (Q+, Q-) per particle and theta row
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
+  if (li >= nl) return;  // whole warp
+  const int64_t leaf = leaf_b + li;
+  const int half = n / 2, quads = half * half, nphi = n;
+  const int64_t S = int64_t(n) * n;
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  double4 (*Qt)[kQuadHalfMax] = sQ[warp];
+  for (int qc = 0; qc < quads; qc += 32 * kQuadR) {
+    double ax[kQuadR], ay[kQuadR];
+    int qi[kQuadR];
+    double upx[kQuadR], upy[kQuadR], vpx[kQuadR], vpy[kQuadR];
+    double umx[kQuadR], umy[kQuadR], vmx[kQuadR], vmy[kQuadR];
+#pragma unroll
+    for (int r = 0; r < kQuadR; ++r) {
+      const int qd = qc + lane + 32 * r;
+      const int i = qd < quads ? qd / half : 0, j = qd < quads ? qd - (qd / half) * half : 0;
+      qi[r] = i;
+      const int64_t s1 = int64_t(i) * nphi + j;
+      ax[r] = k * dir[3 * s1];
+      ay[r] = k * dir[3 * s1 + 1];
+      upx[r] = upy[r] = vpx[r] = vpy[r] = umx[r] = umy[r] = vmx[r] = vmy[r] = 0.0;
+    }
+    for (int64_t pc = p0; pc < p1; pc += kQuadP2) {
+      const int np = int(p1 - pc < kQuadP2 ? p1 - pc : kQuadP2);
+      __syncwarp();
+      for (int t = lane; t < np * half; t += 32) {
+        const int pp = t / half, i = t - pp * half;
+        double sb, cb;
+        sincos_q(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), sb, cb);
+        const double2 qq = q[pc + pp];
+        Qt[pp][i] = make_double4(fma(qq.x, cb, -qq.y * sb), fma(qq.x, sb, qq.y * cb),   // q e^{iB}
+                                 fma(qq.x, cb, qq.y * sb), fma(qq.y, cb, -qq.x * sb));  // q e^{-iB}
+      }
+      __syncwarp();
+      for (int pp = 0; pp < np; ++pp) {
+        const double rx = x[pc + pp] - cx, ry = y[pc + pp] - cy;
+#pragma unroll
+        for (int r = 0; r < kQuadR; ++r) {
+          double sa, ca;
+          sincos_q(fma(ax[r], rx, ay[r] * ry), sa, ca);
+          const double4 Q = Qt[pp][qi[r]];
+          upx[r] = fma(Q.x, ca, upx[r]);
+          upy[r] = fma(Q.x, sa, upy[r]);
+          vpx[r] = fma(Q.y, ca, vpx[r]);
+          vpy[r] = fma(Q.y, sa, vpy[r]);
+          umx[r] = fma(Q.z, ca, umx[r]);
+          umy[r] = fma(Q.z, sa, umy[r]);
+          vmx[r] = fma(Q.w, ca, vmx[r]);
+          vmy[r] = fma(Q.w, sa, vmy[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kQuadR; ++r) {
+      const int qd = qc + lane + 32 * r;
+      if (qd < quads) {
+        const int i = qd / half, j = qd - i * half;
+        double2* m = mp + leaf * S;
+        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
+        m[s1] = make_double2(upx[r] - vpy[r], upy[r] + vpx[r]);         // A + B
+        m[s2] = make_double2(umx[r] - vmy[r], umy[r] + vmx[r]);         // A - B   (pi - theta)
+        m[s1 + half] = make_double2(upx[r] + vpy[r], vpx[r] - upy[r]);  // -A + B  (phi + pi)
+        m[s2 + half] = make_double2(umx[r] + vmy[r], vmx[r] - umy[r]);  // -A - B
+      }
+    }
+  }
+}
+
+// L2T, one warp per leaf: lanes over quads, kQuadOB observers per pass
+// (warp-shuffle reduction per observer), e^{iB} table per particle and row.
+__global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
+                                                   const double* __restrict__ x, const double* __restrict__ y,
+                                                   const double* __restrict__ z, const double* __restrict__ centers,
+                                                   const double* __restrict__ dir, const double* __restrict__ wq,
+                                                   int n, double k, const double2* __restrict__ loc,
+                                                   double2* __restrict__ pot) {
+  extern __shared__ double2 qsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = n / 2, quads = half * half, nphi = n;
+  const int64_t S = int64_t(n) * n;
+  double2* Bt = qsm + warp * (kQuadP * half);  // e^{iB} table of this warp
+  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
+  if (li >= nl) return;
+  const int64_t leaf = leaf_b + li;
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
+  const double2* lc = loc + leaf * S;
+  for (int64_t pc = p0; pc < p1; pc += kQuadP) {
+    const int np = int(p1 - pc < kQuadP ? p1 - pc : kQuadP);
+    __syncwarp();
+    for (int t = lane; t < np * half; t += 32) {
+      const int pp = t / half, i = t - pp * half;
+      double sn, cs;
+      sincos_q(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), sn, cs);
+      Bt[pp * half + i] = make_double2(cs, sn);
+    }
+    __syncwarp();
+    for (int pb = 0; pb < np; pb += kQuadOB) {
+      double rx[kQuadOB], ry[kQuadOB], ar[kQuadOB], ai[kQuadOB];
+#pragma unroll
+      for (int o = 0; o < kQuadOB; ++o) {
+        const int pp = pb + o < np ? pb + o : pb;  // idle slots repeat a live observer
+        rx[o] = k * (x[pc + pp] - cx);
+        ry[o] = k * (y[pc + pp] - cy);
+        ar[o] = 0.0;
+        ai[o] = 0.0;
+      }
+      for (int qd = lane; qd < quads; qd += 32) {
+        const int i = qd / half, j = qd - i * half;
+        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
+        const double dxs = dir[3 * s1], dys = dir[3 * s1 + 1];
+        auto lw = [&](int64_t s) {
+          const double2 v = __ldg(lc + s);
+          const double w = __ldg(wq + s);
+          return make_double2(w * v.x, w * v.y);
+        };
+        const double2 l1 = lw(s1), l2 = lw(s2), l3 = lw(s1 + half), l4 = lw(s2 + half);
+        const double2 s12 = make_double2(l1.x + l2.x, l1.y + l2.y), s34 = make_double2(l3.x + l4.x, l3.y + l4.y);
+        const double2 d12 = make_double2(l2.x - l1.x, l2.y - l1.y), d34 = make_double2(l4.x - l3.x, l4.y - l3.y);
+        const double2 G = make_double2(s12.x + s34.x, s12.y + s34.y);
+        const double2 Gp = make_double2(s34.x - s12.x, s34.y - s12.y);
+        const double2 H = make_double2(d12.x + d34.x, d12.y + d34.y);
+        const double2 Hp = make_double2(d34.x - d12.x, d34.y - d12.y);
+#pragma unroll
+        for (int o = 0; o < kQuadOB; ++o) {
+          const int pp = pb + o < np ? pb + o : pb;
+          double sa, ca;
+          sincos_q(fma(dxs, rx[o], dys * ry[o]), sa, ca);
+          const double2 eb = Bt[pp * half + i];
+          const double u = eb.x * ca, v = eb.x * sa, w = eb.y * ca, zz = eb.y * sa;
+          ar[o] = fma(u, G.x, fma(-v, Gp.y, fma(-w, H.y, fma(-zz, Hp.x, ar[o]))));
+          ai[o] = fma(u, G.y, fma(v, Gp.x, fma(w, H.x, fma(-zz, Hp.y, ai[o]))));
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < kQuadOB; ++o) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          ar[o] += __shfl_xor_sync(0xffffffffu, ar[o], off);
+          ai[o] += __shfl_xor_sync(0xffffffffu, ai[o], off);
+        }
+        if (lane == 0 && pb + o < np) pot[pc + pb + o] = make_double2(-c * ai[o], c * ar[o]);
+      }
+    }
+  }
+}
+
+}  // namespace hfmm_b200
+
+#endif  // HFMM_B200_LEAF_CUH

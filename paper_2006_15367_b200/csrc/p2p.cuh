@@ -22,41 +22,7 @@
 
 namespace hfmm_b200 {
 
-// exp(-i r') / r' from r'^2 > 0 (finite): (gr, gi).
-__device__ __forceinline__ void green_scaled(double r2, double& gr, double& gi) {
-  double y0;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
-  const double t = r2 * y0;
-  const double e = fma(-t, y0, 1.0);  // 1 - r2 y0^2
-  const double p = fma(e, 0.375, 0.5);
-  const double ri = fma(y0 * e, p, y0);  // 1 / r'
-  const double x = r2 * ri;             // r'
-  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-  const double tq = fma(x, kSinCos[12], kMagic);
-  const int quad = __double2loint(tq);
-  const double n = tq - kMagic;
-  double y = fma(n, -1.5707963267948966, x);
-  y = fma(n, kSinCos[13], y);
-  const double y2 = y * y;
-  double ps = kSinCos[0];
-#pragma unroll
-  for (int i = 1; i < 6; ++i) ps = fma(ps, y2, kSinCos[i]);
-  const double sn = fma(ps * y2, y, y);
-  double pc = kSinCos[6];
-#pragma unroll
-  for (int i = 7; i < 12; ++i) pc = fma(pc, y2, kSinCos[i]);
-  const double cs = fma(pc, y2 * y2, fma(-0.5, y2, 1.0));
-  // exp(-i (y + quad pi/2)) = (cos y - i sin y) (-i)^quad:
-  //   quad 0: ( c, -s)   1: (-s, -c)   2: (-c,  s)   3: ( s,  c)
-  const bool swap = quad & 1;
-  const double mr = swap ? sn : cs, mi = swap ? cs : sn;
-  const unsigned q30 = unsigned(quad) << 30;
-  const unsigned sr = (q30 + 0x40000000u) & 0x80000000u;  // re < 0 for quad 1, 2
-  const unsigned si = ~q30 & 0x80000000u;                 // im < 0 for quad 0, 1
-  const int rhi = __double2hiint(ri), rlo = __double2loint(ri);
-  gr = mr * __hiloint2double(rhi ^ int(sr), rlo);
-  gi = mi * __hiloint2double(rhi ^ int(si), rlo);
-}
+// green_scaled (exp(-i r') / r') lives in kernels.cuh next to p2p_pair.
 
 // Symmetric dense-leaf near field: as k_p2p_sym (same lists, scratch layout
 // and gather), with the pair loop above.  Block = 128 threads.
