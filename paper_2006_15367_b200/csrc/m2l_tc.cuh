@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, i
   // source child as above.  value = +Tr, -Ti, +Ti, +Tr by (part_o, part_c).
   const int po = g & 1, pc = tq & 1;
   const int comp = po ^ pc;                        // 0: Tr, 1: Ti
-  const double sgn = (po == 0 && pc == 1) ? -1.0 : 1.0;
+  const int sgn = (po == 0 && pc == 1) ? int(0x80000000u) : 0;  // -Ti: sign bit XOR (integer pipe)
   const int bxo = ((g >> 1) & 1) - (tq >> 1);      // ox - cx
   // lane base of the tap gather: Td[4 tap + 2 sw + comp], tap's lane part bxo 49 + (g >> 2) 7
   const double* Tl = Td + (bxo * 49 + (g >> 2) * 7) * 4 + 2 * sw + comp;
@@ -76,8 +76,13 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, i
   for (int64_t pr = pb; pr < pe; ++pr) {
     const int64_t s0 = pr * 2;
     __syncthreads();
-    for (int t = threadIdx.x; t < kSlots * 2; t += blockDim.x)
-      cp_async16(Ts + t, T + int64_t(t >> 1) * S + s0 + (t & 1), true);
+    for (int t = threadIdx.x; t < kSlots * 2; t += blockDim.x) {
+      // taps of adjacent boxes (|offset| <= 1 per axis) are never far: staged
+      // as zeros, so K_D needs no per-entry mask
+      const int sl = t >> 1, ax = sl / 49 - 3, ay = (sl / 7) % 7 - 3, az = sl % 7 - 3;
+      const bool far_tap = iabs(ax) > 1 || iabs(ay) > 1 || iabs(az) > 1;
+      cp_async16(Ts + t, T + (far_tap ? int64_t(sl) * S + s0 + (t & 1) : 0), far_tap);
+    }
     for (int t = threadIdx.x; t < CELLS * 2; t += blockDim.x) {
       const int c = t >> 1, cz = c / (MR * MR), cy = (c / MR) % MR, cx = c % MR;
       const int node = nodes[c];
@@ -103,12 +108,11 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, i
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int kj = 0; kj < 4; ++kj) {
-          const int ox = bxo - 2 * Dx, oy = (g >> 2) - (kj & 1) - 2 * Dy, oz = mi - (kj >> 1) - 2 * Dz;
-          const bool nearb = iabs(ox) <= 1 && iabs(oy) <= 1 && iabs(oz) <= 1;
-          // tap = (ox + 3) 49 + (oy + 3) 7 + (oz + 3) = lane part + compile-time part
+          // tap = (ox + 3) 49 + (oy + 3) 7 + (oz + 3) = lane part + compile-time part;
+          // adjacent taps read the staged zeros
           const int tofs = ((-2 * Dx + 3) * 49 + (-(kj & 1) - 2 * Dy + 3) * 7 + (mi - (kj >> 1) - 2 * Dz + 3)) * 4;
           const double v = Tl[tofs];
-          a[mi][kj] = nearb ? 0.0 : sgn * v;
+          a[mi][kj] = __hiloint2double(__double2hiint(v) ^ sgn, __double2loint(v));
         }
 #pragma unroll
       for (int kj = 0; kj < 4; ++kj)

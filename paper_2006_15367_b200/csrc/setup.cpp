@@ -3,6 +3,9 @@
 #include "setup.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -13,6 +16,18 @@
 namespace hfmm_b200 {
 
 namespace {
+
+// HFMM_SETUP_TIMING=1: per-section wall time of build_setup on stderr.
+struct SectionTimer {
+  bool on = std::getenv("HFMM_SETUP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-22s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
 
 constexpr uint64_t kCodeMask = (uint64_t(1) << 58) - 1;
 
@@ -230,6 +245,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
     throw std::invalid_argument("RunConfig: invalid fields");
   if (n == 0) throw std::invalid_argument("build_setup: no particles");
 
+  SectionTimer timer;
   Setup s;
   s.cfg = cfg;
   s.k = 2.0 * M_PI / cfg.lambda;  // Wavenumber::from_lambda, geometry.cpp:17-20
@@ -245,6 +261,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
       hi[a] = std::max(hi[a], p[a]);
     }
   }
+  timer.mark("bbox");
   // traversal.cpp:85-98
   for (int a = 0; a < 3; ++a) s.corner[a] = std::floor(lo[a] / leaf) * leaf;
   double span = std::max({hi[0] - s.corner[0], hi[1] - s.corner[1], hi[2] - s.corner[2]});
@@ -298,6 +315,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
     std::memcpy(&s.xyz[3 * i], xyz + 3 * j, 3 * sizeof(double));
     std::memcpy(&s.q[2 * i], q + 2 * j, 2 * sizeof(double));
   }
+  timer.mark("keys+sort+gather");
   // Leaves and particle ranges (traversal.cpp:112-126)
   for (size_t i = 0; i < n; ++i) {
     uint64_t pk = keys[order[i]];
@@ -337,6 +355,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
   }
   partition(s, weights);
 
+  timer.mark("leaves+partition");
   // Per-level node sets for every level 1..L (collect_level_nodes,
   // interaction_lists.cpp:21-37); tables are kept for top..L.
   s.levels.assign(size_t(L + 1), LevelData{});
@@ -380,6 +399,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
       t.plural[i] = t.first_user[i] != t.last_user[i];
     }
   }
+  timer.mark("levels+centers");
   // Child links (traversal.cpp:165-173): children in ascending index order.
   for (int l = s.top; l < L; ++l) {
     LevelData& t = lv[size_t(l)];
@@ -397,6 +417,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
   }
   lv[size_t(L)].child_off.assign(lv[size_t(L)].codes.size() + 1, 0);
 
+  timer.mark("child links");
   // Sample slices bottom-up (traversal.cpp:174-195)
   for (int l = L; l >= s.top; --l) {
     LevelData& t = lv[size_t(l)];
@@ -462,6 +483,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
     }
   }
 
+  timer.mark("slices+interp");
   // Far lists, levels max(top, 2)..L (interaction_lists.cpp:54-98)
   for (int l = s.top; l <= L; ++l) {
     LevelData& t = lv[size_t(l)];
@@ -485,6 +507,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
       t.far_off.push_back(t.far.size());
     }
   }
+  timer.mark("far lists");
   // Near lists per leaf
   {
     const LevelData& t = lv[size_t(L)];
@@ -495,6 +518,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
     }
   }
 
+  timer.mark("near lists");
   // M2L exchange plan (comm_plan.cpp:31-82)
   {
     const int P = s.P;
@@ -539,6 +563,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
       s.m2l_plan.push_back(std::move(pp));
     }
   }
+  timer.mark("m2l plan");
   // Near ghost plan (comm_plan.cpp:84-109)
   {
     const int P = s.P;
@@ -554,6 +579,7 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
     for (size_t i = 0; i < needed.size(); ++i)
       s.near_send[i].assign(needed[i].begin(), needed[i].end());
   }
+  timer.mark("near plan");
   return s;
 }
 
