@@ -68,7 +68,9 @@ typedef struct hfmm_run_config {
    * pairs per leaf, n_leaf * sum of its near leaves' populations (opt-in load
    * balance for P2P-dominated geometries). */
   int32_t partition_weight;
-  int32_t reserved0;
+  /* 1 = build the Morton keys / sort and the far and near lists on the CUDA
+   * device (bit-exact with the host build); 0 = host only. */
+  int32_t setup_device;
 } hfmm_run_config;
 
 /* Fills the reference defaults (RunConfig{} in traversal.hpp:21-35). */

@@ -69,7 +69,7 @@ class RunConfigC(ctypes.Structure):
         ("scheduler", ctypes.c_int32),
         ("seed", ctypes.c_uint64),
         ("partition_weight", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("setup_device", ctypes.c_int32),
     ]
 
 

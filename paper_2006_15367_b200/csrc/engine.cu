@@ -404,7 +404,9 @@ void Engine::upload() {
     // Dense cell lookup for well-populated levels (stencil M2L).
     d.G = 1 << (l - 1);
     const double cells = double(d.G) * d.G * d.G;
-    if (d.n_far > 0 && d.G <= 512 && double(d.n_nodes) >= 0.25 * cells) {
+    // (grids smaller than one 8^3 observer block -- level 3 -- leave the block
+    // mostly empty: far-list CSR kernel there)
+    if (d.n_far > 0 && d.G >= m2l::MB && d.G <= 512 && double(d.n_nodes) >= 0.25 * cells) {
       // row-major cell -> node table padded by a 3-cell halo of -1 (m2l.cuh)
       const size_t GP = size_t(std::max(d.G, m2l::MB)) + 6;
       std::vector<int> lk(GP * GP * GP, -1);

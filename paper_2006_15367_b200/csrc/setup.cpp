@@ -277,48 +277,57 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
   // order-identical to std::stable_sort with the packed-key comparator.
   const uint32_t cells = uint32_t(1) << (L - 1);
   const double inv = double(cells) / s.root_side;
-  std::vector<uint64_t> keys(n);
-  for (size_t i = 0; i < n; ++i) {
-    uint32_t c3[3];
-    for (int a = 0; a < 3; ++a) {
-      double v = xyz[3 * i + a] - s.corner[a];
-      if (v < 0.0 || v > s.root_side)
-        throw std::out_of_range("morton_key: position outside root box");
-      c3[a] = std::min(uint32_t(v * inv), cells - 1);
-    }
-    keys[i] = interleave(c3[0], c3[1], c3[2], L);
-  }
-  std::vector<uint64_t> order(n), tmp(n);
-  std::iota(order.begin(), order.end(), 0);
-  {
-    const int bits = 3 * (L - 1);
-    std::vector<size_t> count(1 << 16);
-    for (int shift = 0; shift < bits; shift += 16) {
-      std::fill(count.begin(), count.end(), 0);
-      for (size_t i = 0; i < n; ++i) ++count[(keys[order[i]] >> shift) & 0xffff];
-      size_t run = 0;
-      for (auto& c : count) {
-        size_t v = c;
-        c = run;
-        run += v;
-      }
-      for (size_t i = 0; i < n; ++i) tmp[count[(keys[order[i]] >> shift) & 0xffff]++] = order[i];
-      order.swap(tmp);
-    }
-  }
   s.n = n;
-  s.original_index = order;
-  s.xyz.resize(3 * n);
-  s.q.resize(2 * n);
-  for (size_t i = 0; i < n; ++i) {
-    const size_t j = order[i];
-    std::memcpy(&s.xyz[3 * i], xyz + 3 * j, 3 * sizeof(double));
-    std::memcpy(&s.q[2 * i], q + 2 * j, 2 * sizeof(double));
+  std::vector<uint64_t> skeys;  // keys in sorted order
+  if (cfg.setup_device == 1) {
+    device_keys_sort(xyz, q, n, s.corner, s.root_side, inv, cells, L, skeys, s.original_index, s.xyz, s.q);
+  } else if (cfg.setup_device != 0) {
+    throw std::invalid_argument("build_setup: setup_device must be 0 (host) or 1 (device)");
+  } else {
+    std::vector<uint64_t> keys(n);
+    for (size_t i = 0; i < n; ++i) {
+      uint32_t c3[3];
+      for (int a = 0; a < 3; ++a) {
+        double v = xyz[3 * i + a] - s.corner[a];
+        if (v < 0.0 || v > s.root_side)
+          throw std::out_of_range("morton_key: position outside root box");
+        c3[a] = std::min(uint32_t(v * inv), cells - 1);
+      }
+      keys[i] = interleave(c3[0], c3[1], c3[2], L);
+    }
+    std::vector<uint64_t> order(n), tmp(n);
+    std::iota(order.begin(), order.end(), 0);
+    {
+      const int bits = 3 * (L - 1);
+      std::vector<size_t> count(1 << 16);
+      for (int shift = 0; shift < bits; shift += 16) {
+        std::fill(count.begin(), count.end(), 0);
+        for (size_t i = 0; i < n; ++i) ++count[(keys[order[i]] >> shift) & 0xffff];
+        size_t run = 0;
+        for (auto& c : count) {
+          size_t v = c;
+          c = run;
+          run += v;
+        }
+        for (size_t i = 0; i < n; ++i) tmp[count[(keys[order[i]] >> shift) & 0xffff]++] = order[i];
+        order.swap(tmp);
+      }
+    }
+    skeys.resize(n);
+    for (size_t i = 0; i < n; ++i) skeys[i] = keys[order[i]];
+    s.original_index = order;
+    s.xyz.resize(3 * n);
+    s.q.resize(2 * n);
+    for (size_t i = 0; i < n; ++i) {
+      const size_t jj = order[i];
+      std::memcpy(&s.xyz[3 * i], xyz + 3 * jj, 3 * sizeof(double));
+      std::memcpy(&s.q[2 * i], q + 2 * jj, 2 * sizeof(double));
+    }
   }
   timer.mark("keys+sort+gather");
   // Leaves and particle ranges (traversal.cpp:112-126)
   for (size_t i = 0; i < n; ++i) {
-    uint64_t pk = keys[order[i]];
+    const uint64_t pk = skeys[i];
     if (s.leaf_codes.empty() || s.leaf_codes.back() != pk) {
       s.leaf_codes.push_back(pk);
       s.leaf_start.push_back(i);
@@ -484,46 +493,49 @@ Setup build_setup(const double* xyz, const double* q, size_t n,
   }
 
   timer.mark("slices+interp");
-  // Far lists, levels max(top, 2)..L (interaction_lists.cpp:54-98)
-  for (int l = s.top; l <= L; ++l) {
-    LevelData& t = lv[size_t(l)];
-    t.far_off.assign(1, 0);
-    const bool has_far = l >= std::max(s.top, 2);
-    std::vector<uint64_t> far;
-    for (size_t i = 0; i < t.codes.size(); ++i) {
-      if (has_far) {
-        far.clear();
-        const uint64_t c = t.codes[i];
-        for_neighbors(lv[size_t(l - 1)], c >> 3, [&](uint64_t pn) {
-          for (uint64_t oct = 0; oct < 8; ++oct) {
-            uint64_t cand = (pn << 3) | oct;
-            if (t.find(cand) < 0) continue;
-            if (!boxes_near(c, cand, l)) far.push_back(cand);
-          }
-        });
-        std::sort(far.begin(), far.end());
-        for (uint64_t fc : far) t.far.push_back(uint32_t(t.find(fc)));
+  if (cfg.setup_device == 1) {
+    device_lists(s);  // far + near lists on the device (setup_gpu.cu)
+  } else {
+    // Far lists, levels max(top, 2)..L (interaction_lists.cpp:54-98)
+    for (int l = s.top; l <= L; ++l) {
+      LevelData& t = lv[size_t(l)];
+      t.far_off.assign(1, 0);
+      const bool has_far = l >= std::max(s.top, 2);
+      std::vector<uint64_t> far;
+      for (size_t i = 0; i < t.codes.size(); ++i) {
+        if (has_far) {
+          far.clear();
+          const uint64_t c = t.codes[i];
+          for_neighbors(lv[size_t(l - 1)], c >> 3, [&](uint64_t pn) {
+            for (uint64_t oct = 0; oct < 8; ++oct) {
+              uint64_t cand = (pn << 3) | oct;
+              if (t.find(cand) < 0) continue;
+              if (!boxes_near(c, cand, l)) far.push_back(cand);
+            }
+          });
+          std::sort(far.begin(), far.end());
+          for (uint64_t fc : far) t.far.push_back(uint32_t(t.find(fc)));
+        }
+        t.far_off.push_back(t.far.size());
       }
-      t.far_off.push_back(t.far.size());
+    }
+    timer.mark("far lists");
+    // Near lists per leaf
+    {
+      const LevelData& t = lv[size_t(L)];
+      s.near_off.assign(1, 0);
+      for (size_t i = 0; i < nl; ++i) {
+        for_neighbors(t, t.codes[i], [&](uint64_t nc) { s.near.push_back(uint32_t(t.find(nc))); });
+        s.near_off.push_back(s.near.size());
+      }
     }
   }
-  timer.mark("far lists");
-  // Near lists per leaf
-  {
-    const LevelData& t = lv[size_t(L)];
-    s.near_off.assign(1, 0);
-    for (size_t i = 0; i < nl; ++i) {
-      for_neighbors(t, t.codes[i], [&](uint64_t nc) { s.near.push_back(uint32_t(t.find(nc))); });
-      s.near_off.push_back(s.near.size());
-    }
-  }
-
   timer.mark("near lists");
   // M2L exchange plan (comm_plan.cpp:31-82)
   {
     const int P = s.P;
     std::map<std::pair<int, int>, std::map<uint64_t, std::vector<std::pair<int64_t, int64_t>>>> raw;
-    for (int l = s.top; l <= L; ++l) {
+    for (int l = s.top; l <= L && P > 1; ++l) {  // one rank: every slice is its own, no items
       const LevelData& t = lv[size_t(l)];
       for (size_t o = 0; o < t.codes.size(); ++o)
         for (uint64_t f = t.far_off[o]; f < t.far_off[o + 1]; ++f) {

@@ -119,6 +119,12 @@ RankPlan build_rank_plan(const struct Setup& s, int r);
 Setup build_setup(const double* xyz, const double* q, size_t n,
                   const hfmm_run_config& cfg);
 
+// Device parts of the setup (setup_gpu.cu), used when cfg.setup_device = 1.
+void device_keys_sort(const double* xyz, const double* q, size_t n, const double corner[3], double root_side,
+                      double inv, uint32_t cells, int L, std::vector<uint64_t>& sorted_keys,
+                      std::vector<uint64_t>& order, std::vector<double>& xyz_s, std::vector<double>& q_s);
+void device_lists(Setup& s);
+
 // Flat dump under the names used by oracle/ref_driver.cpp.
 std::vector<unsigned char> setup_array(const Setup& s, const std::string& name);
 

@@ -62,6 +62,9 @@ class RunConfig:
     # Morton-partition leaf weights: 0 = particles (the reference's rule,
     # bit-exact setup), 1 = near-field pairs per leaf (opt-in P2P load balance)
     partition_weight: int = 0
+    # 1 = Morton keys / sort and the far / near lists built on the device
+    # (bit-exact with the host build)
+    setup_device: int = 0
 
     def validate(self) -> None:
         """RunConfig::validate (traversal.cpp:42-46)."""
@@ -74,7 +77,7 @@ class RunConfig:
             float(self.lambda_), float(self.digits), float(self.leaf_lambda), int(self.num_ranks),
             int(self.policy), int(self.buffer_limit), int(bool(self.one_particle_per_leaf)),
             int(self.top_level), int(self.d_override), int(self.scheduler), int(self.seed),
-            int(self.partition_weight), 0)
+            int(self.partition_weight), int(self.setup_device))
 
 
 def _as_particles(positions, intensities):

@@ -19,7 +19,7 @@ cfg = sys.argv[1]
 envs = sys.argv[2:]
 shape, n, ext, seed, digits = CONFIGS[cfg]
 pos, q = hb.generate_inputs(shape, n, ext, seed)
-setup = hb.build_setup(pos, q, hb.RunConfig(digits=digits))
+setup = hb.build_setup(pos, q, hb.RunConfig(digits=digits, setup_device=1))
 ref = None
 for var in [None] + envs:
     for e in envs:
