@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhfmm_b200.so")
+# HFMM_LIB_PATH: an alternative build of the same library (A/B dev tools only)
+LIB_PATH = os.environ.get("HFMM_LIB_PATH") or os.path.join(_HERE, "_lib", "libhfmm_b200.so")
 
 HFMM_OK = 0
 

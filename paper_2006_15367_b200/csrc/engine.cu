@@ -590,8 +590,8 @@ void Engine::phase_m2m() {
     if (use_rb_ && rbl_ok(nc, np)) {  // larger pairs: runtime-shaped streaming kernels
       const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
       const int s_phi = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8;
-      const int nchunk = (rb::r8(2 * np) / 8 + rb::kChunk - 1) / rb::kChunk;
-      const int s_th = rb::r4(2 * nc + 1) * rb::blk_ldb(8 * rb::kChunk) * 8;
+      const int nchunk = (rb::r8(2 * np) / 8 + rb::kChunkM2M - 1) / rb::kChunkM2M;
+      const int s_th = rb::r4(2 * nc + 1) * rb::blk_ldb(8 * rb::kChunkM2M) * 8;
       ck(cudaFuncSetAttribute(k_m2m_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
       ck(cudaFuncSetAttribute(k_m2m_theta_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_th), "attr");
       if (nch > 0)

@@ -369,6 +369,10 @@ namespace rb {
 #define HFMM_RBL_CHUNK 4
 #endif
 constexpr int kChunk = HFMM_RBL_CHUNK;
+#ifndef HFMM_M2M_RBL_CHUNK
+#define HFMM_M2M_RBL_CHUNK 4
+#endif
+constexpr int kChunkM2M = HFMM_M2M_RBL_CHUNK;  // M2M theta: B column block per CTA (n8 tiles)
 
 // Rows [0, K) x columns [c0, c0 + nc) of a row-major K x N matrix -> shared
 // rows of stride ldb (cp.async 16 B; nc and c0 even).
@@ -406,9 +410,9 @@ __device__ __forceinline__ double2 row_alpha(int kin, const double* __restrict__
 
 // C chunk (8 complex rows x kChunk n8 tiles from n8 tile j0) over K = 4 ks:
 // column kin holds ia (rank-1), columns > kin are zero.
-template <bool GLOBAL_B = false, class Fetch>
+template <bool GLOBAL_B = false, int CH = kChunk, class Fetch>
 __device__ __forceinline__ void chunk_mma(int ks, int kin, double2 ia, Fetch fetch, const double* __restrict__ B, int N,
-                                          int j0, int nt, double (&cre)[kChunk][2], double (&cim)[kChunk][2]) {
+                                          int j0, int nt, double (&cre)[CH][2], double (&cim)[CH][2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const double* bp = B + tq * N + 8 * j0 + g;
 #pragma unroll 2
@@ -416,7 +420,7 @@ __device__ __forceinline__ void chunk_mma(int ks, int kin, double2 ia, Fetch fet
     const int k = 4 * kk + tq;
     const double2 x = k < kin ? fetch(k) : (k == kin ? ia : make_double2(0.0, 0.0));
 #pragma unroll
-    for (int jc = 0; jc < kChunk; ++jc)
+    for (int jc = 0; jc < CH; ++jc)
       if (j0 + jc < nt) {
         const double b = GLOBAL_B ? __ldg(bp + 4 * kk * N + 8 * jc) : bp[4 * kk * N + 8 * jc];
         dmma884(cre[jc][0], cre[jc][1], x.x, b);
@@ -477,10 +481,11 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
                                                                 double2* __restrict__ mp_p) {
   const int K = rb::r4(2 * nc + 1), N = rb::r8(2 * np), ks = K / 4, nt = N / 8, half = np / 2, ldf = K;
   const int64_t SP = int64_t(np) * np;
-  // this CTA's column block of B (kChunk n8 tiles) lives in shared memory
-  const int j0 = blockIdx.y * rb::kChunk, ldb = rb::blk_ldb(8 * rb::kChunk);
+  // this CTA's column block of B (CH n8 tiles) lives in shared memory
+  constexpr int CH = rb::kChunkM2M;
+  const int j0 = blockIdx.y * CH, ldb = rb::blk_ldb(8 * CH);
   extern __shared__ __align__(16) double Bsh[];
-  rb::stage_block(Bsh, B, K, N, 8 * j0, 8 * rb::kChunk, ldb);
+  rb::stage_block(Bsh, B, K, N, 8 * j0, 8 * CH, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t items = int64_t(n_par) * half;
   for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
@@ -494,19 +499,19 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
     const double2 ia = rb::row_alpha(2 * nc, v, fetch);
     double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
     {
-      double2 shv[rb::kChunk][2];
+      double2 shv[CH][2];
 #pragma unroll
-      for (int jc = 0; jc < rb::kChunk; ++jc)
+      for (int jc = 0; jc < CH; ++jc)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int n = 8 * (j0 + jc) + 2 * tq + q;
           const int64_t s = n < np ? int64_t(n) * np + p : int64_t(2 * np - 1 - n) * np + p + half;
           shv[jc][q] = (ok && n < 2 * np) ? __ldg(sh + s) : make_double2(0.0, 0.0);
         }
-      double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
-      rb::chunk_mma(ks, 2 * nc, ia, fetch, Bsh, ldb, 0, nt - j0, cre, cim);
+      double cre[CH][2] = {}, cim[CH][2] = {};
+      rb::chunk_mma<false, CH>(ks, 2 * nc, ia, fetch, Bsh, ldb, 0, nt - j0, cre, cim);
 #pragma unroll
-      for (int jc = 0; jc < rb::kChunk; ++jc)
+      for (int jc = 0; jc < CH; ++jc)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const double2 f = shv[jc][q];
@@ -527,6 +532,9 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
   }
 }
 
+#ifndef HFMM_L2L_RBL_CHUNK
+#define HFMM_L2L_RBL_CHUNK 7
+#endif
 __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, int n_par, const int* __restrict__ plist,
                                                                 const int* __restrict__ child_off,
                                                                 const int* __restrict__ children,
@@ -557,12 +565,15 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, 
     };
     const double2 ia = rb::row_alpha(2 * np, v, fetch);
     double2* Nc = Nb + int64_t(cb + (ok ? c : 0)) * nc * ldn;
-    for (int j0 = 0; j0 < nt; j0 += rb::kChunk) {
-      double cre[rb::kChunk][2] = {}, cim[rb::kChunk][2] = {};
-      rb::chunk_mma<true>(ks, 2 * np, ia, fetch, B, N, j0, nt, cre, cim);
+    // wide column chunks: the A values (L_p x shift, two loads and a complex
+    // product each) are rebuilt once per chunk
+    constexpr int CH = HFMM_L2L_RBL_CHUNK;
+    for (int j0 = 0; j0 < nt; j0 += CH) {
+      double cre[CH][2] = {}, cim[CH][2] = {};
+      rb::chunk_mma<true, CH>(ks, 2 * np, ia, fetch, B, N, j0, nt, cre, cim);
       if (ok) {
 #pragma unroll
-        for (int jc = 0; jc < rb::kChunk; ++jc)
+        for (int jc = 0; jc < CH; ++jc)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int n = 8 * (j0 + jc) + 2 * tq + q;
