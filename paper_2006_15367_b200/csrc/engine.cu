@@ -251,6 +251,14 @@ void Engine::upload() {
     d_tiny_leaves_ = upload_vec(tiny);
     d_small_leaves_ = upload_vec(small);
     d_dense_leaves_ = upload_vec(dense);
+    {  // leaves with <= 32 particles (L2T lanes-over-quads kernel)
+      std::vector<int> sp(tiny);
+      sp.insert(sp.end(), small.begin(), small.end());
+      std::sort(sp.begin(), sp.end());
+      n_sparse_ = int(sp.size());
+      d_sparse_leaves_ = upload_vec(sp);
+    }
+    l2t_noobs_ = std::getenv("HFMM_L2T_NOOBS") != nullptr;
     // symmetric pair lists among own dense leaves (k_p2p_sym2 / k_p2p_gather).
     // k_p2p_sym2 runs one CTA per (leaf, pass of 128 observers): each pass
     // writes its own scratch rows (no read-modify-write across CTAs), and
@@ -534,10 +542,32 @@ bool quad_ok(const DevLevel& d) {
 void Engine::phase_c2m() {
   const DevLevel& d = lv_[size_t(s_.L)];
   const int64_t nl = leaf_e_ - leaf_b_;
-  if (quad_ok(d) && !leaf_v1_)
-    k_c2m_quad2<<<unsigned((nl + 3) / 4), 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,
-                                                         d.dir, d.nt, s_.k, d.mp);
-  else if (quad_ok(d))
+  if (quad_ok(d) && !leaf_v1_) {
+    const int quads = int(d.nt / 2) * int(d.nt / 2);
+    // quads per lane: fewest lane slots (passes x R), ties to fewer passes; R <= 4
+    // keeps 4 CTAs/SM (R = 6 needs 208 registers and measured slower at config 2)
+    const int rmax = std::getenv("HFMM_C2M_RMAX") ? std::atoi(std::getenv("HFMM_C2M_RMAX")) : 4;
+    int r = 1, best = INT32_MAX;
+    for (int rr = 1; rr <= std::min(std::max(rmax, 1), 6); ++rr) {
+      const int cost = (quads + 32 * rr - 1) / (32 * rr) * rr;
+      if (cost <= best) {
+        best = cost;
+        r = rr;
+      }
+    }
+    const unsigned g = unsigned((nl + 3) / 4);
+#define HFMM_C2M(RR) \
+  k_c2m_quad2<RR><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.nt, s_.k, d.mp)
+    switch (r) {
+      case 1: HFMM_C2M(1); break;
+      case 2: HFMM_C2M(2); break;
+      case 3: HFMM_C2M(3); break;
+      case 4: HFMM_C2M(4); break;
+      case 5: HFMM_C2M(5); break;
+      default: HFMM_C2M(6); break;
+    }
+#undef HFMM_C2M
+  } else if (quad_ok(d))
     k_c2m_quad<<<unsigned((nl + 3) / 4), 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,
                                                          d.dir, d.nt, s_.k, d.mp);
   else
@@ -781,8 +811,23 @@ void Engine::phase_l2t() {
     } else {
       if (smem > 48 * 1024)
         ck(cudaFuncSetAttribute(k_l2t_quad2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-      k_l2t_quad2<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,
-                                                               d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+      if (n_dense_ > 0 && !l2t_noobs_) {  // populous leaves: lane per observer, the rest: lanes over quads
+        const int quads = int(d.nt / 2) * int(d.nt / 2);
+        const size_t so = 4 * size_t(quads) * 5 * sizeof(double2);
+        if (so > 48 * 1024)
+          ck(cudaFuncSetAttribute(k_l2t_obs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(so)), "attr");
+        k_l2t_obs<<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y,
+                                                                   d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc,
+                                                                   d_pot);
+        ++launches_;
+        if (n_sparse_ > 0)
+          k_l2t_quad2<<<unsigned((n_sparse_ + 3) / 4), 128, smem, st_>>>(0, n_sparse_, d_sparse_leaves_,
+                                                                          d_leaf_start, d_x, d_y, d_z, d.centers,
+                                                                          d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+      } else {
+        k_l2t_quad2<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, nullptr, d_leaf_start, d_x, d_y, d_z,
+                                                                 d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+      }
     }
   } else {
     const size_t smem = size_t(d.S) * (sizeof(double2) + 3 * sizeof(double));

@@ -181,7 +181,10 @@ class Engine {
   int64_t* d_sym_rows_ = nullptr;
   int p2p_items_b_[4] = {0, 0, 0, 0}, p2p_items_n_[4] = {0, 0, 0, 0};
   bool p2p_v1_ = false;
-  bool leaf_v1_ = false;  // HFMM_LEAF_V1: the previous quad C2M / L2T kernels (A/B)  // HFMM_P2P_V1: the previous symmetric kernel (A/B)
+  bool leaf_v1_ = false;
+  int* d_sparse_leaves_ = nullptr;  // own leaves with <= 32 particles (L2T)
+  int n_sparse_ = 0;
+  bool l2t_noobs_ = false;  // HFMM_L2T_NOOBS: lanes-over-quads L2T for every leaf (A/B)  // HFMM_LEAF_V1: the previous quad C2M / L2T kernels (A/B)  // HFMM_P2P_V1: the previous symmetric kernel (A/B)
   double2* d_tmp = nullptr;  // interpolation temporaries
   size_t tmp_elems_ = 0;
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range

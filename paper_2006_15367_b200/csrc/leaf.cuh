@@ -56,6 +56,9 @@ __device__ __forceinline__ void sincos_q(double x, double& sp, double& cp) {
 
 constexpr int kQuadP2 = 16;  // particles per table chunk
 
+// R quads per lane: the launch picks R = ceil(quads / 32) (<= 6), so a leaf
+// is one pass and its (Q+, Q-) table is built once.
+template <int R>
 __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
                                                    const double* __restrict__ z, const double2* __restrict__ q,
@@ -71,13 +74,13 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   double4 (*Qt)[kQuadHalfMax] = sQ[warp];
-  for (int qc = 0; qc < quads; qc += 32 * kQuadR) {
-    double ax[kQuadR], ay[kQuadR];
-    int qi[kQuadR];
-    double upx[kQuadR], upy[kQuadR], vpx[kQuadR], vpy[kQuadR];
-    double umx[kQuadR], umy[kQuadR], vmx[kQuadR], vmy[kQuadR];
+  for (int qc = 0; qc < quads; qc += 32 * R) {
+    double ax[R], ay[R];
+    int qi[R];
+    double upx[R], upy[R], vpx[R], vpy[R];
+    double umx[R], umy[R], vmx[R], vmy[R];
 #pragma unroll
-    for (int r = 0; r < kQuadR; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int qd = qc + lane + 32 * r;
       const int i = qd < quads ? qd / half : 0, j = qd < quads ? qd - (qd / half) * half : 0;
       qi[r] = i;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
       for (int pp = 0; pp < np; ++pp) {
         const double rx = x[pc + pp] - cx, ry = y[pc + pp] - cy;
 #pragma unroll
-        for (int r = 0; r < kQuadR; ++r) {
+        for (int r = 0; r < R; ++r) {
           double sa, ca;
           sincos_q(fma(ax[r], rx, ay[r] * ry), sa, ca);
           const double4 Q = Qt[pp][qi[r]];
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
       }
     }
 #pragma unroll
-    for (int r = 0; r < kQuadR; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int qd = qc + lane + 32 * r;
       if (qd < quads) {
         const int i = qd / half, j = qd - i * half;
@@ -134,7 +137,9 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
 
 // L2T, one warp per leaf: lanes over quads, kQuadOB observers per pass
 // (warp-shuffle reduction per observer), e^{iB} table per particle and row.
-__global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
+// leaves != nullptr: warp w takes leaves[w] (a population class), else leaf_b + w.
+__global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
+                                                   const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
                                                    const double* __restrict__ z, const double* __restrict__ centers,
                                                    const double* __restrict__ dir, const double* __restrict__ wq,
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, c
   double2* Bt = qsm + warp * (kQuadP * half);  // e^{iB} table of this warp
   const int64_t li = int64_t(blockIdx.x) * 4 + warp;
   if (li >= nl) return;
-  const int64_t leaf = leaf_b + li;
+  const int64_t leaf = leaves ? int64_t(leaves[li]) : leaf_b + li;
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
@@ -209,6 +214,77 @@ __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, c
         if (lane == 0 && pb + o < np) pot[pc + pb + o] = make_double2(-c * ai[o], c * ar[o]);
       }
     }
+  }
+}
+
+// L2T for populous leaves (> 32 particles): one warp per leaf, one LANE per
+// observer, quads looped with their (G, G', H, H') and (dir_x, dir_y) staged
+// once per leaf in shared memory (warp broadcasts).  The e^{iB} factor is
+// taken out of the row sum: per row i, X = sum_j (cos A G + i sin A G') and
+// Y = sum_j (i cos A H - sin A H') (8 FMA per quad), then
+// acc += cos B_i X + sin B_i Y.  No cross-lane reduction.
+// Shared memory per warp: quads x (4 + 1) double2.
+__global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restrict__ leaves,
+                                                 const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
+                                                 const double* __restrict__ y, const double* __restrict__ z,
+                                                 const double* __restrict__ centers, const double* __restrict__ dir,
+                                                 const double* __restrict__ wq, int n, double k,
+                                                 const double2* __restrict__ loc, double2* __restrict__ pot) {
+  extern __shared__ double2 osm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = n / 2, quads = half * half, nphi = n;
+  const int64_t S = int64_t(n) * n;
+  double2* qt = osm + int64_t(warp) * quads * 5;  // per quad: G, G', H, H', (k dir_x, k dir_y)
+  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
+  if (li >= nl) return;
+  const int64_t leaf = leaves[li];
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
+  const double2* lc = loc + leaf * S;
+  for (int qd = lane; qd < quads; qd += 32) {
+    const int i = qd / half, j = qd - i * half;
+    const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
+    auto lw = [&](int64_t s) {
+      const double2 v = __ldg(lc + s);
+      const double w = __ldg(wq + s);
+      return make_double2(w * v.x, w * v.y);
+    };
+    const double2 l1 = lw(s1), l2 = lw(s2), l3 = lw(s1 + half), l4 = lw(s2 + half);
+    const double2 s12 = make_double2(l1.x + l2.x, l1.y + l2.y), s34 = make_double2(l3.x + l4.x, l3.y + l4.y);
+    const double2 d12 = make_double2(l2.x - l1.x, l2.y - l1.y), d34 = make_double2(l4.x - l3.x, l4.y - l3.y);
+    qt[5 * qd + 0] = make_double2(s12.x + s34.x, s12.y + s34.y);  // G
+    qt[5 * qd + 1] = make_double2(s34.x - s12.x, s34.y - s12.y);  // G'
+    qt[5 * qd + 2] = make_double2(d12.x + d34.x, d12.y + d34.y);  // H
+    qt[5 * qd + 3] = make_double2(d34.x - d12.x, d34.y - d12.y);  // H'
+    qt[5 * qd + 4] = make_double2(k * dir[3 * s1], k * dir[3 * s1 + 1]);
+  }
+  __syncwarp();
+  for (int64_t ob = p0; ob < p1; ob += 32) {
+    const int64_t o = ob + lane;
+    const bool valid = o < p1;
+    const int64_t oo = valid ? o : p0;
+    const double rx = x[oo] - cx, ry = y[oo] - cy, rz = z[oo] - cz;
+    double ar = 0.0, ai = 0.0;
+    for (int i = 0; i < half; ++i) {
+      double xr = 0.0, xi = 0.0, yr = 0.0, yi = 0.0;
+      const double2* q = qt + 5 * i * half;
+      for (int j = 0; j < half; ++j, q += 5) {
+        const double2 a = q[4];
+        double sa, ca;
+        sincos_q(fma(a.x, rx, a.y * ry), sa, ca);
+        const double2 G = q[0], Gp = q[1], H = q[2], Hp = q[3];
+        xr = fma(ca, G.x, fma(-sa, Gp.y, xr));
+        xi = fma(ca, G.y, fma(sa, Gp.x, xi));
+        yr = fma(-ca, H.y, fma(-sa, Hp.x, yr));
+        yi = fma(ca, H.x, fma(-sa, Hp.y, yi));
+      }
+      double sb, cb;
+      sincos_q(k * dir[3 * int64_t(i) * nphi + 2] * rz, sb, cb);
+      ar = fma(cb, xr, fma(sb, yr, ar));
+      ai = fma(cb, xi, fma(sb, yi, ai));
+    }
+    if (valid) pot[o] = make_double2(-c * ai, c * ar);
   }
 }
 

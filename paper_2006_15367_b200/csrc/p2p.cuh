@@ -182,8 +182,11 @@ __device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double
 // One CTA per work item {dense leaf index, pass}: the pass's observers
 // (ob = 128 pass, NC slots per lane) against the leaf's one-sided list and
 // its symmetric partners; pass p writes the scratch rows sym_scr + p rows.
+#ifndef HFMM_P2P_MINB
+#define HFMM_P2P_MINB 4  // CTAs per SM the register budget is sized for
+#endif
 template <int NC>
-__global__ void __launch_bounds__(128, 4) k_p2p_sym2(const int2* __restrict__ items, const int* __restrict__ leaves,
+__global__ void __launch_bounds__(128, HFMM_P2P_MINB) k_p2p_sym2(const int2* __restrict__ items, const int* __restrict__ leaves,
                                                      const int64_t* __restrict__ leaf_start,
                                                      const int* __restrict__ plain_off, const int* __restrict__ plain,
                                                      const int* __restrict__ sym_off, const int* __restrict__ sym,

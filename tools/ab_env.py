@@ -1,6 +1,6 @@
 """A/B of an engine switch read from the environment at engine creation (dev tool).
 
-usage: python tools/ab_env.py cfg2 HFMM_LEAF_V1 [HFMM_P2P_V1 ...]
+usage: python tools/ab_env.py cfg2 HFMM_LEAF_V1 [HFMM_P2P_V1 NAME=VALUE ...]
 For "baseline" (none of the variables set) and each variable set alone:
 builds an engine, runs sequential-phase evaluations (set_overlap off, so each
 phase's events time its own kernels), prints the median per-phase ms of 3
@@ -23,9 +23,10 @@ setup = hb.build_setup(pos, q, hb.RunConfig(digits=digits, setup_device=1))
 ref = None
 for var in [None] + envs:
     for e in envs:
-        os.environ.pop(e, None)
+        os.environ.pop(e.split("=")[0], None)
     if var:
-        os.environ[var] = "1"
+        name, _, val = var.partition("=")
+        os.environ[name] = val or "1"
     eng = hb.RankEngine(setup)
     eng.set_overlap(False)
     runs = []
