@@ -31,7 +31,7 @@ __device__ __forceinline__ double xor_sign(double v, unsigned s) {
   return __hiloint2double(__double2hiint(v) ^ int(s), __double2loint(v));
 }
 
-// sin, cos of |x| < 2^20 (same reduction and kernels as sincos_fast).
+// sin, cos of |x| < 2^20 (same reduction as sincos_fast; cos kernel kCos5).
 __device__ __forceinline__ void sincos_q(double x, double& sp, double& cp) {
   const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
   const double t = fma(x, kSinCos[12], kMagic);
@@ -44,9 +44,9 @@ __device__ __forceinline__ void sincos_q(double x, double& sp, double& cp) {
 #pragma unroll
   for (int i = 1; i < 6; ++i) ps = fma(ps, y2, kSinCos[i]);
   const double sn = fma(ps * y2, y, y);
-  double pc = kSinCos[6];
+  double pc = kCos5[0];
 #pragma unroll
-  for (int i = 7; i < 12; ++i) pc = fma(pc, y2, kSinCos[i]);
+  for (int i = 1; i < 5; ++i) pc = fma(pc, y2, kCos5[i]);
   const double cs = fma(pc, y2 * y2, fma(-0.5, y2, 1.0));
   const bool swap = quad & 1;
   const unsigned q30 = unsigned(quad) << 30;

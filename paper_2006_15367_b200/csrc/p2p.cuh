@@ -2,10 +2,10 @@
 // green kernel.cpp:9-14, driver traversal.cpp:768-786).  Same pair algebra
 // and leaf schedule as k_p2p_sym (kernels.cuh), organised for the FP64 pipe:
 //
-//  * the scaled kernel g' = exp(-i r') / r' (r' = k r) costs 42 FP64
+//  * the scaled kernel g' = exp(-i r') / r' (r' = k r) costs 41 FP64
 //    instructions: 6 for r'^2, 6 for 1/r' and r' (MUFU.RSQ64H + one cubic
-//    Newton step, no special-case branch: r'^2 > 0 here), 20 for sincos
-//    (Cody-Waite by pi/2 + fdlibm's degree 13/14 kernels), 2 for g' and 8
+//    Newton step, no special-case branch: r'^2 > 0 here), 19 for sincos
+//    (Cody-Waite by pi/2, fdlibm's degree-13 sin, a degree-12 cos fit), 2 for g' and 8
 //    for the two complex multiply-adds (A <- B and B <- A).  The quadrant
 //    swap is a select and the quadrant signs are XORed into 1/r' (integer
 //    pipe), so no FP64 negations;
