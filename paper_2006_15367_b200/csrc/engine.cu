@@ -259,6 +259,7 @@ void Engine::upload() {
       d_sparse_leaves_ = upload_vec(sp);
     }
     l2t_noobs_ = std::getenv("HFMM_L2T_NOOBS") != nullptr;
+    if (const char* e = std::getenv("HFMM_PHI_CTAS")) phi_ctas_ = std::max(1, std::atoi(e));
     // symmetric pair lists among own dense leaves (k_p2p_sym2 / k_p2p_gather).
     // k_p2p_sym2 runs one CTA per (leaf, pass of 128 observers): each pass
     // writes its own scratch rows (no read-modify-write across CTAs), and
@@ -610,7 +611,7 @@ void Engine::phase_m2m() {
     if (cl.n_par == 0) continue;
     if (use_rb_ && rb_pair(nc, np)) {
       const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
-      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_};
+      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_, phi_ctas_ * sms_};
       if (launch_m2m_rb(nc, np, rl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up, d_tmp)) {
         launches_ += 2;
         ck(cudaGetLastError(), "k_m2m_rb");
@@ -726,7 +727,7 @@ void Engine::phase_l2l(int lo, int hi) {
     if (cl.n_par == 0) continue;
     if (use_rb_ && rb_pair(nc, np)) {
       const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
-      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_};
+      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_, phi_ctas_ * sms_};
       if (launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn, d_tmp)) {
         launches_ += 2;
         ck(cudaGetLastError(), "k_l2l_rb");

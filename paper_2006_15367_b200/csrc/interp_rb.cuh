@@ -655,6 +655,7 @@ struct RbLaunch {
   const uint8_t* oct_c;
   int grid;              // persistent CTAs
   cudaStream_t st;
+  int phi_grid = 0;      // persistent CTAs of the (HBM-bound) phi passes; 0 = grid
 };
 
 template <int A, int B>
@@ -662,7 +663,8 @@ void m2m_rb(const RbLaunch& L, const double2* mp_c, double2* mp_p, const double*
             const double* Bth, const double* vth, const double2* shift_up, double2* F) {
   using D = rb::Dims<A, B>;
   if (L.nch > 0)
-    k_m2m_phi_rb<A, B><<<L.grid, rb::kThreads, 0, L.st>>>(L.nch, L.children, mp_c, Bphi, vphi, F);
+    k_m2m_phi_rb<A, B><<<L.phi_grid ? L.phi_grid : L.grid, rb::kThreads, 0, L.st>>>(L.nch, L.children, mp_c, Bphi,
+                                                                                    vphi, F);
   const int smem = D::UTH_K * D::UTH_LDB * 8;
   cudaFuncSetAttribute(k_m2m_theta_rb<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   k_m2m_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c, F,
@@ -678,7 +680,8 @@ void l2l_rb(const RbLaunch& L, const double2* loc_p, double2* loc_c, const doubl
   k_l2l_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c,
                                                             loc_p, Bth, vth, shift_dn, Nb);
   if (L.nch > 0)
-    k_l2l_phi_rb<A, B><<<L.grid, rb::kThreads, 0, L.st>>>(L.nch, L.children, Nb, Bphi, vphi, loc_c);
+    k_l2l_phi_rb<A, B><<<L.phi_grid ? L.phi_grid : L.grid, rb::kThreads, 0, L.st>>>(L.nch, L.children, Nb, Bphi,
+                                                                                    vphi, loc_c);
 }
 
 inline bool launch_l2l_rb(int nc, int np, const RbLaunch& L, const double2* loc_p, double2* loc_c, const double* Bth,

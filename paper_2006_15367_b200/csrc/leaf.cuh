@@ -55,6 +55,14 @@ __device__ __forceinline__ void sincos_q(double x, double& sp, double& cp) {
 }
 
 constexpr int kQuadP2 = 16;  // particles per table chunk
+#ifndef HFMM_C2M_UNROLL
+#define HFMM_C2M_UNROLL 1
+#endif
+#ifndef HFMM_L2T_UNROLL
+#define HFMM_L2T_UNROLL 1
+#endif
+constexpr int kC2MUnroll = HFMM_C2M_UNROLL;  // particle loop unroll (C2M)
+constexpr int kL2TUnroll = HFMM_L2T_UNROLL;  // quad loop unroll (populous-leaf L2T)
 
 // R quads per lane: the launch picks R = ceil(quads / 32) (<= 6), so a leaf
 // is one pass and its (Q+, Q-) table is built once.
@@ -101,6 +109,7 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
                                  fma(qq.x, cb, qq.y * sb), fma(qq.y, cb, -qq.x * sb));  // q e^{-iB}
       }
       __syncwarp();
+#pragma unroll kC2MUnroll
       for (int pp = 0; pp < np; ++pp) {
         const double rx = x[pc + pp] - cx, ry = y[pc + pp] - cy;
 #pragma unroll
@@ -269,6 +278,7 @@ __global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restri
     for (int i = 0; i < half; ++i) {
       double xr = 0.0, xi = 0.0, yr = 0.0, yi = 0.0;
       const double2* q = qt + 5 * i * half;
+#pragma unroll kL2TUnroll
       for (int j = 0; j < half; ++j, q += 5) {
         const double2 a = q[4];
         double sa, ca;
