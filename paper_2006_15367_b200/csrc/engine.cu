@@ -269,7 +269,7 @@ void Engine::upload() {
     use_sym_ = std::getenv("HFMM_P2P_NOSYM") == nullptr;
     p2p_v1_ = std::getenv("HFMM_P2P_V1") != nullptr;
     leaf_v1_ = std::getenv("HFMM_LEAF_V1") != nullptr;
-    const int obs_pass = 32 * kP2PObsPerLane;
+    const int obs_pass = 32 * kSymObs;
     auto pop = [&](int64_t lf) { return int64_t(s.leaf_start[size_t(lf) + 1] - s.leaf_start[size_t(lf)]); };
     std::vector<int> pos(s.num_leaves(), -1);
     for (size_t i = 0; i < dense.size(); ++i) pos[size_t(dense[i])] = int(i);
@@ -286,7 +286,8 @@ void Engine::upload() {
       const size_t sb = sl.size();
       for (uint64_t z2 = s.near_off[size_t(a)]; z2 < s.near_off[size_t(a) + 1]; ++z2) {
         const int b = int(s.near[z2]);
-        if (b > a && pos[size_t(b)] >= 0) {
+        // k_p2p_sym2 takes the self leaf as a symmetric entry (pairs o < t once)
+        if ((b > a || (b == a && !p2p_v1_)) && pos[size_t(b)] >= 0) {
           sl.push_back(b);
           sscr.push_back(scr + rows);
           rows += pop(b);

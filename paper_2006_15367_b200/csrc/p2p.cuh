@@ -22,19 +22,131 @@
 
 namespace hfmm_b200 {
 
+#ifndef HFMM_P2P_SYMOBS
+#define HFMM_P2P_SYMOBS 4
+#endif
+constexpr int kSymObs = HFMM_P2P_SYMOBS;  // observer slots per lane (pass = 32 kSymObs observers)
+
+
 // green_scaled (exp(-i r') / r') lives in kernels.cuh next to p2p_pair.
+
+// Sources [b0, b0 + nb) (staged kP2PChunk at a time, relative to the leaf
+// centre) against the lane's NC observers; both sides accumulate: A's in
+// ar/ai, each source's B-side sum (over the CTA's observers of this warp)
+// is reduced across the warp and written to scr[source - b0].
+// SELF: the sources are this leaf's particles from the pass's first
+// observer on (source index s relative to the pass; slot tile u = s / 32):
+// slots c < u are symmetric pairs, slot c == u only lanes with o < s (the
+// diagonal tile, exact-zero self pair excluded), slots c > u are skipped --
+// those pairs are taken when the roles are swapped.
+template <int NC, int M, bool SELF>
+__device__ __forceinline__ void sym_block(P2PShared& sh, double k, double cx, double cy, double cz, double qs,
+                                          int64_t b0, int64_t nbp, double2* __restrict__ scr,
+                                          const double* __restrict__ x, const double* __restrict__ y,
+                                          const double* __restrict__ z, const double2* __restrict__ q,
+                                          const double (&xo)[NC], const double (&yo)[NC], const double (&zo)[NC],
+                                          const double (&qr)[NC], const double (&qi)[NC], double (&ar)[NC],
+                                          double (&ai)[NC]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  for (int64_t cb = 0; cb < nbp; cb += kP2PChunk) {
+    const int n = int(nbp - cb < kP2PChunk ? nbp - cb : kP2PChunk);
+    const int npad = (n + M - 1) / M * M;
+    __syncthreads();
+    for (int t = threadIdx.x; t < npad; t += blockDim.x) {
+      if (t < n) {
+        const int64_t src = b0 + cb + t;
+        sh.sx[t] = k * (x[src] - cx);
+        sh.sy[t] = k * (y[src] - cy);
+        sh.sz[t] = k * (z[src] - cz);
+        const double2 qq = q[src];
+        sh.sq[t] = make_double2(qs * qq.x, qs * qq.y);
+      } else {  // padding source: far, zero charge
+        sh.sx[t] = -1.0e4;
+        sh.sy[t] = 0.0;
+        sh.sz[t] = 0.0;
+        sh.sq[t] = make_double2(0.0, 0.0);
+      }
+    }
+    __syncthreads();
+    for (int t = warp * M; t < npad; t += nwarp * M) {
+      double br[M], bi[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const double px = sh.sx[t + m], py = sh.sy[t + m], pz = sh.sz[t + m];
+        const double2 qq = sh.sq[t + m];
+        const int srel = int(cb) + t + m, u = srel >> 5;  // SELF: source's slot tile
+        br[m] = 0.0;
+        bi[m] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (SELF && c > u) continue;  // warp-uniform
+          const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
+          double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          const bool keep = !SELF || c < u || lane < (srel & 31);
+          if (SELF) r2 = keep ? r2 : 1.0;
+          double gr, gi;
+          green_scaled(r2, gr, gi);
+          if (SELF) {
+            gr = keep ? gr : 0.0;
+            gi = keep ? gi : 0.0;
+          }
+          ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
+          ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
+          br[m] = fma(gr, qr[c], fma(-gi, qi[c], br[m]));
+          bi[m] = fma(gr, qi[c], fma(gi, qr[c], bi[m]));
+        }
+      }
+      // split butterfly: after the first log2(M) steps lane group g holds
+      // the partial of source g, then a plain butterfly over the rest
+      int width = 16;
+      int cnt = M;
+#pragma unroll
+      for (int s = 0; (1 << s) < M; ++s) {
+        const bool hi = lane & width;
+        cnt >>= 1;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          if (m >= cnt) break;
+          const double sr = hi ? br[m] : br[m + cnt], si = hi ? bi[m] : bi[m + cnt];
+          const double kr = hi ? br[m + cnt] : br[m], ki = hi ? bi[m + cnt] : bi[m];
+          br[m] = kr + __shfl_xor_sync(0xffffffffu, sr, width);
+          bi[m] = ki + __shfl_xor_sync(0xffffffffu, si, width);
+        }
+        width >>= 1;
+      }
+      double vr = br[0], vi = bi[0];
+      for (int off = width; off > 0; off >>= 1) {
+        vr += __shfl_xor_sync(0xffffffffu, vr, off);
+        vi += __shfl_xor_sync(0xffffffffu, vi, off);
+      }
+      // lane group g (of 32 / M lanes) holds source index sidx(g): the
+      // split keeps the upper half's source in the upper lanes
+      if ((lane & (32 / M - 1)) == 0) {
+        int sidx = 0, w2 = 16;
+#pragma unroll
+        for (int s = 0, c2 = M; (1 << s) < M; ++s) {
+          c2 >>= 1;
+          if (lane & w2) sidx += c2;
+          w2 >>= 1;
+        }
+        const int tt = t + sidx;
+        if (tt < n) scr[cb + tt] = make_double2(vr, vi);
+      }
+    }
+  }
+}
 
 // Symmetric dense-leaf near field: as k_p2p_sym (same lists, scratch layout
 // and gather), with the pair loop above.  Block = 128 threads.
 template <int NC, int M>
 __device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double k, double cx, double cy,
-                                             double cz, double qs, int64_t p0, int64_t total,
+                                             double cz, double qs, int64_t leaf, int ob, int64_t p0, int64_t total,
                                              const int* __restrict__ sym, int j0, int j1,
                                              const int64_t* __restrict__ sym_scr, int64_t scr_pass,
                                              const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
                                              const double* __restrict__ y, const double* __restrict__ z,
                                              const double2* __restrict__ q, double2* __restrict__ pot,
-                                             double2* __restrict__ scratch, double2 (*red)[32 * kP2PObsPerLane]) {
+                                             double2* __restrict__ scratch, double2 (*red)[32 * kSymObs]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   double xo[NC], yo[NC], zo[NC], qr[NC], qi[NC], ar[NC], ai[NC];
 #pragma unroll
@@ -51,8 +163,8 @@ __device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double
     ar[c] = 0.0;
     ai[c] = 0.0;
   }
-  // one-sided part: self leaf + small / ghost neighbours (exact-zero
-  // separation masked, operators.cpp:118)
+  // one-sided part: small / ghost neighbours (and the self leaf under
+  // HFMM_P2P_V1's lists; exact-zero separation masked, operators.cpp:118)
   for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
     const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
     __syncthreads();
@@ -75,87 +187,20 @@ __device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double
       }
     }
   }
-  // symmetric part: dense partners B > A; M sources per warp iteration
+  // symmetric part: dense partners B > A, and the leaf itself (self pairs
+  // o < t, from this pass's first observer on); M sources per warp iteration
   for (int j = j0; j < j1; ++j) {
     const int lb = sym[j];
-    const int64_t b0 = leaf_start[lb], nbp = leaf_start[lb + 1] - b0;
     double2* scr = scratch + sym_scr[j] + scr_pass;
-    for (int64_t cb = 0; cb < nbp; cb += kP2PChunk) {
-      const int n = int(nbp - cb < kP2PChunk ? nbp - cb : kP2PChunk);
-      const int npad = (n + M - 1) / M * M;
-      __syncthreads();
-      for (int t = threadIdx.x; t < npad; t += blockDim.x) {
-        if (t < n) {
-          const int64_t src = b0 + cb + t;
-          sh.sx[t] = k * (x[src] - cx);
-          sh.sy[t] = k * (y[src] - cy);
-          sh.sz[t] = k * (z[src] - cz);
-          const double2 qq = q[src];
-          sh.sq[t] = make_double2(qs * qq.x, qs * qq.y);
-        } else {  // padding source: far, zero charge
-          sh.sx[t] = -1.0e4;
-          sh.sy[t] = 0.0;
-          sh.sz[t] = 0.0;
-          sh.sq[t] = make_double2(0.0, 0.0);
-        }
-      }
-      __syncthreads();
-      for (int t = warp * M; t < npad; t += nwarp * M) {
-        double br[M], bi[M];
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          const double px = sh.sx[t + m], py = sh.sy[t + m], pz = sh.sz[t + m];
-          const double2 qq = sh.sq[t + m];
-          br[m] = 0.0;
-          bi[m] = 0.0;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
-            double gr, gi;
-            green_scaled(fma(dz, dz, fma(dy, dy, dx * dx)), gr, gi);
-            ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
-            ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
-            br[m] = fma(gr, qr[c], fma(-gi, qi[c], br[m]));
-            bi[m] = fma(gr, qi[c], fma(gi, qr[c], bi[m]));
-          }
-        }
-        // split butterfly: after the first log2(M) steps lane group g holds
-        // the partial of source g, then a plain butterfly over the rest
-        int width = 16;
-        int cnt = M;
-#pragma unroll
-        for (int s = 0; (1 << s) < M; ++s) {
-          const bool hi = lane & width;
-          cnt >>= 1;
-#pragma unroll
-          for (int m = 0; m < M; ++m) {
-            if (m >= cnt) break;
-            const double sr = hi ? br[m] : br[m + cnt], si = hi ? bi[m] : bi[m + cnt];
-            const double kr = hi ? br[m + cnt] : br[m], ki = hi ? bi[m + cnt] : bi[m];
-            br[m] = kr + __shfl_xor_sync(0xffffffffu, sr, width);
-            bi[m] = ki + __shfl_xor_sync(0xffffffffu, si, width);
-          }
-          width >>= 1;
-        }
-        double vr = br[0], vi = bi[0];
-        for (int off = width; off > 0; off >>= 1) {
-          vr += __shfl_xor_sync(0xffffffffu, vr, off);
-          vi += __shfl_xor_sync(0xffffffffu, vi, off);
-        }
-        // lane group g (of 32 / M lanes) holds source index sidx(g): the
-        // split keeps the upper half's source in the upper lanes
-        if ((lane & (32 / M - 1)) == 0) {
-          int sidx = 0, w2 = 16;
-#pragma unroll
-          for (int s = 0, c2 = M; (1 << s) < M; ++s) {
-            c2 >>= 1;
-            if (lane & w2) sidx += c2;
-            w2 >>= 1;
-          }
-          const int tt = t + sidx;
-          if (tt < n) scr[cb + tt] = make_double2(vr, vi);
-        }
-      }
+    if (lb == leaf) {
+      for (int t = threadIdx.x; t < ob; t += blockDim.x) scr[t] = make_double2(0.0, 0.0);  // earlier passes' rows
+      const int64_t b0 = leaf_start[lb] + ob;
+      sym_block<NC, M, true>(sh, k, cx, cy, cz, qs, b0, leaf_start[lb + 1] - b0, scr + ob, x, y, z, q, xo, yo, zo, qr,
+                             qi, ar, ai);
+    } else {
+      const int64_t b0 = leaf_start[lb];
+      sym_block<NC, M, false>(sh, k, cx, cy, cz, qs, b0, leaf_start[lb + 1] - b0, scr, x, y, z, q, xo, yo, zo, qr,
+                              qi, ar, ai);
     }
   }
 #pragma unroll
@@ -197,7 +242,7 @@ __global__ void __launch_bounds__(128, HFMM_P2P_MINB) k_p2p_sym2(const int2* __r
                                                      const double2* __restrict__ q, double k,
                                                      double2* __restrict__ pot, double2* __restrict__ scratch) {
   __shared__ P2PShared sh;
-  __shared__ double2 red[4][32 * kP2PObsPerLane];
+  __shared__ double2 red[4][32 * kSymObs];
   const int2 item = items[blockIdx.x];
   const int i = item.x, pass = item.y;
   const int64_t leaf = leaves[i];
@@ -218,9 +263,9 @@ __global__ void __launch_bounds__(128, HFMM_P2P_MINB) k_p2p_sym2(const int2* __r
   }
   __syncthreads();
   const int64_t total = sh.pref[sh.nn];
-  const int ob = pass * 32 * kP2PObsPerLane;
-  const int no = min(int(p1 - p0) - ob, 32 * kP2PObsPerLane);
-  p2p_sym_pass<NC, HFMM_P2P_M>(sh, no, k, cx, cy, cz, qs, p0 + ob, total, sym, sym_off[i], sym_off[i + 1],
+  const int ob = pass * 32 * kSymObs;
+  const int no = min(int(p1 - p0) - ob, 32 * kSymObs);
+  p2p_sym_pass<NC, HFMM_P2P_M>(sh, no, k, cx, cy, cz, qs, leaf, ob, p0 + ob, total, sym, sym_off[i], sym_off[i + 1],
                                sym_scr, int64_t(pass) * sym_rows[i], leaf_start, x, y, z, q, pot, scratch, red);
 }
 
