@@ -67,6 +67,25 @@ __device__ __forceinline__ void rank1_inject(double (&are)[KS], double (&aim)[KS
   }
 }
 
+// Sum over the 8 child rows of a warp tile (lane bits 2..4 = g) of a chunk of
+// 4 n8 tiles: v[(2 jc + q) 2 + part] are the lane's 16 values (tile jc,
+// column 2 tq + q, re/im).  A reduce-scatter (8 + 4 + 2 shuffles instead of
+// 3 x 16) leaves lane (g, tq) with column n = 8 (g >> 1) + 2 tq + (g & 1) of
+// the chunk, returned as (re, im).
+__device__ __forceinline__ double2 child_sum_scatter(double (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int w = 16, h = 8; w >= 4; w >>= 1, h >>= 1) {
+    const bool hi = lane & w;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const double send = hi ? v[i] : v[i + h], keep = hi ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return make_double2(v[0], v[1]);
+}
+
 // C (8 complex rows x NT n8 tiles) += A (8 x K) B (K x 8 NT): 2 NT DMMA per k-step.
 template <int KS, int NT, int LDB>
 __device__ __forceinline__ void tile_mma(const double (&are)[KS], const double (&aim)[KS], const double* __restrict__ Bs,
@@ -184,9 +203,10 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, con
     }
     rb::rank1_inject<KS, 2 * NC>(are, aim, v);
     double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
-    // N in chunks of NTC n8 tiles (A stays in registers): shift factors of the
-    // chunk's outputs are loaded ahead of its DMMAs.
-    constexpr int NTC = 3;
+    // N in chunks of 4 n8 tiles (A stays in registers): shift factors of the
+    // chunk's outputs are loaded ahead of its DMMAs; the child sum is one
+    // reduce-scatter per chunk (child_sum_scatter).
+    constexpr int NTC = 4;
 #pragma unroll
     for (int j0 = 0; j0 < NT; j0 += NTC) {
       double2 shv[NTC][2];
@@ -209,25 +229,21 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, con
             dmma884(cre[jc][0], cre[jc][1], are[kk], b);
             dmma884(cim[jc][0], cim[jc][1], aim[kk], b);
           }
+      double v[16];
 #pragma unroll
       for (int jc = 0; jc < NTC; ++jc)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          if (j0 + jc >= NT) continue;
           const double2 f = shv[jc][q];
-          double vr = cre[jc][q] * f.x - cim[jc][q] * f.y;
-          double vi = cre[jc][q] * f.y + cim[jc][q] * f.x;
-#pragma unroll
-          for (int off = 4; off < 32; off <<= 1) {  // sum over the 8 child slots (g)
-            vr += __shfl_xor_sync(0xffffffffu, vr, off);
-            vi += __shfl_xor_sync(0xffffffffu, vi, off);
-          }
-          const int n = 8 * (j0 + jc) + 2 * tq + q;
-          if (g == 0 && n < 2 * NP) {
-            const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
-            out[s] = make_double2(vr, vi);
-          }
+          v[(2 * jc + q) * 2] = cre[jc][q] * f.x - cim[jc][q] * f.y;
+          v[(2 * jc + q) * 2 + 1] = cre[jc][q] * f.y + cim[jc][q] * f.x;
         }
+      const double2 val = rb::child_sum_scatter(v);
+      const int jt = j0 + (g >> 1), n = 8 * jt + 2 * tq + (g & 1);
+      if (jt < NT && n < 2 * NP) {
+        const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
+        out[s] = val;
+      }
     }
   }
 }
@@ -510,24 +526,22 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
         }
       double cre[CH][2] = {}, cim[CH][2] = {};
       rb::chunk_mma<false, CH>(ks, 2 * nc, ia, fetch, Bsh, ldb, 0, nt - j0, cre, cim);
+      static_assert(CH == 4, "child_sum_scatter takes 4 n8 tiles");
+      double v[16];
 #pragma unroll
       for (int jc = 0; jc < CH; ++jc)
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const double2 f = shv[jc][q];
-          double vr = cre[jc][q] * f.x - cim[jc][q] * f.y;
-          double vi = cre[jc][q] * f.y + cim[jc][q] * f.x;
-#pragma unroll
-          for (int off = 4; off < 32; off <<= 1) {
-            vr += __shfl_xor_sync(0xffffffffu, vr, off);
-            vi += __shfl_xor_sync(0xffffffffu, vi, off);
-          }
-          const int n = 8 * (j0 + jc) + 2 * tq + q;
-          if (g == 0 && j0 + jc < nt && n < 2 * np) {
-            const int64_t s = n < np ? int64_t(n) * np + p : int64_t(2 * np - 1 - n) * np + p + half;
-            out[s] = make_double2(vr, vi);
-          }
+          v[(2 * jc + q) * 2] = cre[jc][q] * f.x - cim[jc][q] * f.y;
+          v[(2 * jc + q) * 2 + 1] = cre[jc][q] * f.y + cim[jc][q] * f.x;
         }
+      const double2 val = rb::child_sum_scatter(v);
+      const int jt = j0 + (g >> 1), n = 8 * jt + 2 * tq + (g & 1);
+      if (jt < nt && n < 2 * np) {
+        const int64_t s = n < np ? int64_t(n) * np + p : int64_t(2 * np - 1 - n) * np + p + half;
+        out[s] = val;
+      }
     }
   }
 }
