@@ -199,6 +199,9 @@ std::vector<uint64_t> scan(const std::vector<uint32_t>& cnt) {
 void device_keys_sort(const double* xyz, const double* q, size_t n, const double corner[3], double root_side,
                       double inv, uint32_t cells, int L, std::vector<uint64_t>& sorted_keys,
                       std::vector<uint64_t>& order, std::vector<double>& xyz_s, std::vector<double>& q_s) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw std::runtime_error("setup_device: no CUDA device (use setup_device = 0 for the host build)");
   DevBuf<double> dxyz(3 * n), dq(2 * n), dxyz_s(3 * n), dq_s(2 * n);
   DevBuf<uint64_t> keys(n), keys_s(n), idx(n), idx_s(n);
   DevBuf<int> bad(1);

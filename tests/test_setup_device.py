@@ -52,3 +52,19 @@ def test_device_setup_evaluates_like_host():
     a = hb.RankEngine(hb.build_setup(pos, q, hb.RunConfig(digits=4.0))).evaluate().potentials
     b = hb.RankEngine(hb.build_setup(pos, q, hb.RunConfig(digits=4.0, setup_device=1))).evaluate().potentials
     assert np.array_equal(a, b)
+
+
+def test_device_setup_without_device_fails_loudly(native):
+    """No silent host fallback: setup_device=1 without a CUDA device raises
+    NoDeviceError (CPU-only check; on a GPU box the device build runs)."""
+    import paper_2006_15367_b200 as hb
+    from paper_2006_15367_b200 import _native
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a CUDA device is present")
+    except ImportError:
+        pass
+    pos, q = hb.generate_inputs("cube", 2_000, 2.0, 1)
+    with pytest.raises(_native.NoDeviceError):
+        hb.build_setup(pos, q, hb.RunConfig(setup_device=1))
