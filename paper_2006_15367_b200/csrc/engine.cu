@@ -90,6 +90,8 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   ck(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
   ck(cudaEventCreate(&ev_near0_), "event");
   ck(cudaEventCreate(&ev_near1_), "event");
+  ck(cudaStreamCreateWithFlags(&st_cp_, cudaStreamNonBlocking), "copy stream");
+  ck(cudaEventCreateWithFlags(&ev_q_, cudaEventDisableTiming), "event");
   upload();
   if (dist_) upload_rank_plan();
   ck(cudaStreamSynchronize(st_), "upload sync");
@@ -97,15 +99,16 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
-  for (cudaStream_t s : {st_, st2_, st_hi_, st_lo_})  // every stream idle before the buffers go
+  for (cudaStream_t s : {st_, st2_, st_hi_, st_lo_, st_cp_})  // every stream idle before the buffers go
     if (s) cudaStreamSynchronize(s);
   for (void* p : allocs_) cudaFree(p);
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (st_ && owns_stream_) cudaStreamDestroy(st_);
   if (st2_) cudaStreamDestroy(st2_);
-  for (cudaStream_t s : {st_hi_, st_lo_})
+  for (cudaStream_t s : {st_hi_, st_lo_, st_cp_})
     if (s) cudaStreamDestroy(s);
+  if (ev_q_) cudaEventDestroy(ev_q_);
   for (cudaEvent_t e : {ev_ofork_, ev_ojoin_, ev_c2m_, ev_m2l_leaf_, ev_lf0_, ev_lf1_, ev_la_, ev_lb_})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {ev_fork_, ev_join_, ev_near0_, ev_near1_})
@@ -991,10 +994,18 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
     ck(cudaStreamWaitEvent(st_hi_, ev_ofork_, 0), "fork wait");
     st_ = st_hi_;
   }
+  // Charges still in flight on the copy stream (evaluate_host): the T build,
+  // which does not read them, goes first.
+  const bool t_first = q_pending_;
+  if (t_first) {
+    build_T();
+    ck(cudaStreamWaitEvent(st_, ev_q_, 0), "q wait");
+    q_pending_ = false;
+  }
   // Near field: side stream, overlapped with the far-field chain; in the
   // sequential mode (set_overlap off) it runs after L2T, inside phase_near.
   if (overlap_) near_start();
-  build_T();
+  if (!t_first) build_T();
   cudaEventRecord(ev_[1], st_);
   phase_c2m();
   cudaEventRecord(ev_[2], st_);
@@ -1047,7 +1058,17 @@ void Engine::evaluate_host(const double* q_in, double* pot_out, double* ms) {
     throw std::logic_error(
         "evaluate: num_ranks > 1 needs the exchanges of the distributed driver "
         "(paper_2006_15367_b200.distributed)");
-  if (q_in) set_charges(q_in);
+  if (q_in) {
+    // charges H2D + Morton gather on the copy stream; evaluate_device builds
+    // T meanwhile and joins before the first phase that reads them
+    const int64_t n = int64_t(s_.n);
+    ck(cudaMemcpyAsync(d_q_in, q_in, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, st_cp_), "H2D q");
+    k_gather_q<<<unsigned((n + 255) / 256), 256, 0, st_cp_>>>(n, d_orig, d_q_in, d_q);
+    ++launches_;
+    ck(cudaGetLastError(), "k_gather_q");
+    ck(cudaEventRecord(ev_q_, st_cp_), "q ready");
+    q_pending_ = true;
+  }
   evaluate_device(nullptr, nullptr, nullptr);
   const int64_t cnt = part_e_ - part_b_;
   if (cnt > 0) {

@@ -193,6 +193,9 @@ class Engine {
   cudaEvent_t ev_[8] = {};
   // near field on a side stream, overlapped with the far-field chain
   cudaStream_t st2_ = nullptr;
+  cudaStream_t st_cp_ = nullptr;  // host charges in (evaluate_host), beside the T build
+  cudaEvent_t ev_q_ = nullptr;
+  bool q_pending_ = false;
   // evaluate_device overlap: far chain (high priority) + leaf M2L (low priority)
   cudaStream_t st_hi_ = nullptr, st_lo_ = nullptr;
   cudaEvent_t ev_ofork_ = nullptr, ev_ojoin_ = nullptr, ev_c2m_ = nullptr, ev_m2l_leaf_ = nullptr;
