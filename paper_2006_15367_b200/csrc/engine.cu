@@ -561,16 +561,22 @@ void Engine::phase_c2m() {
       }
     }
     const unsigned g = unsigned((nl + 3) / 4);
-#define HFMM_C2M(RR) \
-  k_c2m_quad2<RR><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.nt, s_.k, d.mp)
-    switch (r) {
-      case 1: HFMM_C2M(1); break;
-      case 2: HFMM_C2M(2); break;
-      case 3: HFMM_C2M(3); break;
-      case 4: HFMM_C2M(4); break;
-      case 5: HFMM_C2M(5); break;
-      default: HFMM_C2M(6); break;
-    }
+#define HFMM_C2M(RR, HN)                                                                                      \
+  k_c2m_quad2<RR, HN><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.nt, \
+                                          s_.k, d.mp)
+    const int hn = int(d.nt / 2);
+    if (r == 3 && hn == 9) HFMM_C2M(3, 9);        // n = 18 (configs 1, 3, 4)
+    else if (r == 4 && hn == 11) HFMM_C2M(4, 11);  // n = 22 (config 5)
+    else if (r == 3 && hn == 13) HFMM_C2M(3, 13);  // n = 26 (config 2)
+    else
+      switch (r) {
+        case 1: HFMM_C2M(1, 0); break;
+        case 2: HFMM_C2M(2, 0); break;
+        case 3: HFMM_C2M(3, 0); break;
+        case 4: HFMM_C2M(4, 0); break;
+        case 5: HFMM_C2M(5, 0); break;
+        default: HFMM_C2M(6, 0); break;
+      }
 #undef HFMM_C2M
   } else if (quad_ok(d))
     k_c2m_quad<<<unsigned((nl + 3) / 4), 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,
@@ -814,24 +820,39 @@ void Engine::phase_l2t() {
       k_l2t_quad<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,
                                                               d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
     } else {
-      if (smem > 48 * 1024)
-        ck(cudaFuncSetAttribute(k_l2t_quad2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+      // (n / 2 <= kQuadHalfMax keeps the table under 48 KB: no attribute needed)
+      auto l2t_quads = [&](unsigned grid, int64_t lb, int64_t cnt, const int* list) {
+        const int hn = int(d.nt / 2);
+#define HFMM_L2TQ(HN)                                                                                          \
+  k_l2t_quad2<HN><<<grid, 128, smem, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, \
+                                            d.nt, s_.k, d.loc, d_pot)
+        if (hn == 9) HFMM_L2TQ(9);
+        else if (hn == 11) HFMM_L2TQ(11);
+        else if (hn == 13) HFMM_L2TQ(13);
+        else HFMM_L2TQ(0);
+#undef HFMM_L2TQ
+      };
       if (n_dense_ > 0 && !l2t_noobs_) {  // populous leaves: lane per observer, the rest: lanes over quads
         const int quads = int(d.nt / 2) * int(d.nt / 2);
         const size_t so = 4 * size_t(quads) * 5 * sizeof(double2);
-        if (so > 48 * 1024)
-          ck(cudaFuncSetAttribute(k_l2t_obs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(so)), "attr");
-        k_l2t_obs<<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y,
-                                                                   d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc,
-                                                                   d_pot);
+        const int hn = int(d.nt / 2);
+#define HFMM_L2TO(HN)                                                                                          \
+  do {                                                                                                         \
+    if (so > 48 * 1024)                                                                                        \
+      ck(cudaFuncSetAttribute(k_l2t_obs<HN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(so)), "attr");   \
+    k_l2t_obs<HN><<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(n_dense_, d_dense_leaves_, d_leaf_start, d_x, \
+                                                                  d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, \
+                                                                  d.loc, d_pot);                                \
+  } while (0)
+        if (hn == 9) HFMM_L2TO(9);
+        else if (hn == 11) HFMM_L2TO(11);
+        else if (hn == 13) HFMM_L2TO(13);
+        else HFMM_L2TO(0);
+#undef HFMM_L2TO
         ++launches_;
-        if (n_sparse_ > 0)
-          k_l2t_quad2<<<unsigned((n_sparse_ + 3) / 4), 128, smem, st_>>>(0, n_sparse_, d_sparse_leaves_,
-                                                                          d_leaf_start, d_x, d_y, d_z, d.centers,
-                                                                          d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+        if (n_sparse_ > 0) l2t_quads(unsigned((n_sparse_ + 3) / 4), 0, n_sparse_, d_sparse_leaves_);
       } else {
-        k_l2t_quad2<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, nullptr, d_leaf_start, d_x, d_y, d_z,
-                                                                 d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
+        l2t_quads(unsigned((nl + 3) / 4), leaf_b_, nl, nullptr);
       }
     }
   } else {

@@ -66,7 +66,9 @@ constexpr int kL2TUnroll = HFMM_L2T_UNROLL;  // quad loop unroll (populous-leaf 
 
 // R quads per lane: the launch picks R = ceil(quads / 32) (<= 6), so a leaf
 // is one pass and its (Q+, Q-) table is built once.
-template <int R>
+// HN > 0: n / 2 known at compile time (the BASELINE leaf grids n = 18, 22, 26),
+// so quad indices and table rows need no integer division at run time.
+template <int R, int HN = 0>
 __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
                                                    const double* __restrict__ z, const double2* __restrict__ q,
@@ -77,7 +79,7 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
   const int64_t li = int64_t(blockIdx.x) * 4 + warp;
   if (li >= nl) return;  // whole warp
   const int64_t leaf = leaf_b + li;
-  const int half = n / 2, quads = half * half, nphi = n;
+  const int half = HN > 0 ? HN : n / 2, quads = half * half, nphi = HN > 0 ? 2 * HN : n;
   const int64_t S = int64_t(n) * n;
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
@@ -147,6 +149,8 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
 // L2T, one warp per leaf: lanes over quads, kQuadOB observers per pass
 // (warp-shuffle reduction per observer), e^{iB} table per particle and row.
 // leaves != nullptr: warp w takes leaves[w] (a population class), else leaf_b + w.
+// HN as in k_c2m_quad2.
+template <int HN = 0>
 __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
                                                    const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, c
                                                    double2* __restrict__ pot) {
   extern __shared__ double2 qsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = n / 2, quads = half * half, nphi = n;
+  const int half = HN > 0 ? HN : n / 2, quads = half * half, nphi = HN > 0 ? 2 * HN : n;
   const int64_t S = int64_t(n) * n;
   double2* Bt = qsm + warp * (kQuadP * half);  // e^{iB} table of this warp
   const int64_t li = int64_t(blockIdx.x) * 4 + warp;
@@ -233,6 +237,7 @@ __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, c
 // Y = sum_j (i cos A H - sin A H') (8 FMA per quad), then
 // acc += cos B_i X + sin B_i Y.  No cross-lane reduction.
 // Shared memory per warp: quads x (4 + 1) double2.
+template <int HN = 0>
 __global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restrict__ leaves,
                                                  const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
                                                  const double* __restrict__ y, const double* __restrict__ z,
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restri
                                                  const double2* __restrict__ loc, double2* __restrict__ pot) {
   extern __shared__ double2 osm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = n / 2, quads = half * half, nphi = n;
+  const int half = HN > 0 ? HN : n / 2, quads = half * half, nphi = HN > 0 ? 2 * HN : n;
   const int64_t S = int64_t(n) * n;
   double2* qt = osm + int64_t(warp) * quads * 5;  // per quad: G, G', H, H', (k dir_x, k dir_y)
   const int64_t li = int64_t(blockIdx.x) * 4 + warp;
