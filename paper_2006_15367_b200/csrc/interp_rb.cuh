@@ -388,7 +388,15 @@ constexpr int kChunk = HFMM_RBL_CHUNK;
 #ifndef HFMM_M2M_RBL_CHUNK
 #define HFMM_M2M_RBL_CHUNK 4
 #endif
-constexpr int kChunkM2M = HFMM_M2M_RBL_CHUNK;  // M2M theta: B column block per CTA (n8 tiles)
+constexpr int kChunkM2M = HFMM_M2M_RBL_CHUNK;
+#ifndef HFMM_RBL_UNROLL_G
+#define HFMM_RBL_UNROLL_G 8
+#endif
+constexpr int kRblUnrollG = HFMM_RBL_UNROLL_G;  // k-step unroll of the global-B chunk GEMM (L2L theta)
+#ifndef HFMM_RBL_UNROLL_S
+#define HFMM_RBL_UNROLL_S 8
+#endif
+constexpr int kRblUnrollS = HFMM_RBL_UNROLL_S;  // same, shared-memory B (M2M theta)  // M2M theta: B column block per CTA (n8 tiles)
 
 // Rows [0, K) x columns [c0, c0 + nc) of a row-major K x N matrix -> shared
 // rows of stride ldb (cp.async 16 B; nc and c0 even).
@@ -431,7 +439,8 @@ __device__ __forceinline__ void chunk_mma(int ks, int kin, double2 ia, Fetch fet
                                           int j0, int nt, double (&cre)[CH][2], double (&cim)[CH][2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const double* bp = B + tq * N + 8 * j0 + g;
-#pragma unroll 2
+  // deeper unroll with B from global (L2): more loads in flight per warp
+#pragma unroll(GLOBAL_B ? kRblUnrollG : kRblUnrollS)
   for (int kk = 0; kk < ks; ++kk) {
     const int k = 4 * kk + tq;
     const double2 x = k < kin ? fetch(k) : (k == kin ? ia : make_double2(0.0, 0.0));
