@@ -707,17 +707,24 @@ void Engine::phase_m2l(int lo, int hi) {
   ck(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
   for (int l = lo; l <= hi; ++l) {
     DevLevel& d = lv_[size_t(l)];
+    // distributed mode: only the observers this rank holds (the multipole
+    // exchange completed exactly their far sources)
     if (d.dense) {
       const int nb = (d.G + m2l::MB - 1) / m2l::MB;
-      const int ppc = m2l_pairs_per_cta(nb * nb * nb, d.S, sms_);
-      dim3 grid(unsigned(nb * nb * nb), unsigned((d.S / 2 + ppc - 1) / ppc));
+      const int nblk = dist_ && dmma ? d.m2l_nblk : nb * nb * nb;
+      if (nblk == 0) continue;
+      const int ppc = m2l_pairs_per_cta(nblk, d.S, sms_);
+      dim3 grid(unsigned(nblk), unsigned((d.S / 2 + ppc - 1) / ppc));
       if (dmma)
-        k_m2l_dmma<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, d.lookup, d.T, d.mp, d.loc);
+        k_m2l_dmma<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, dist_ ? d.m2l_blk : nullptr, d.lookup,
+                                                        d.T, d.mp, d.loc);
       else
         k_m2l_dense<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, d.lookup, d.T, d.mp, d.loc);
     } else {
-      dim3 grid(unsigned(d.n_nodes), unsigned((d.S + 127) / 128));
-      k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, d.far_off, d.far, d.T, d.mp, d.loc);
+      const int nobs = dist_ ? held_cnt_[size_t(l)] : int(d.n_nodes);
+      if (nobs == 0) continue;
+      dim3 grid(unsigned(nobs), unsigned((d.S + 127) / 128));
+      k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, dist_ ? held_[size_t(l)] : nullptr, d.far_off, d.far, d.T, d.mp, d.loc);
     }
     ++launches_;
   }
@@ -1140,6 +1147,20 @@ void Engine::upload_rank_plan() {
   for (int l = s.top; l <= L; ++l) {
     held_cnt_[size_t(l)] = int(rp.held[size_t(l)].size());
     held_[size_t(l)] = upload_vec(rp.held[size_t(l)]);
+    DevLevel& d = lv_[size_t(l)];
+    if (d.dense) {  // the 8^3 observer blocks (Morton subtrees) holding held nodes
+      const int nb = (d.G + m2l::MB - 1) / m2l::MB;
+      std::vector<int> blk;
+      for (int node : rp.held[size_t(l)]) {
+        const uint64_t c = s.levels[size_t(l)].codes[size_t(node)];
+        blk.push_back((int(cell_axis(c, l, 2)) / m2l::MB * nb + int(cell_axis(c, l, 1)) / m2l::MB) * nb +
+                      int(cell_axis(c, l, 0)) / m2l::MB);
+      }
+      std::sort(blk.begin(), blk.end());
+      blk.erase(std::unique(blk.begin(), blk.end()), blk.end());
+      d.m2l_nblk = int(blk.size());
+      d.m2l_blk = upload_vec(blk);
+    }
   }
   halo_nodes_.assign(size_t(L + 1), nullptr);
   halo_cnt_.assign(size_t(L + 1), 0);

@@ -34,6 +34,8 @@ struct DevLevel {
   int G = 0;                  // cells per axis = 2^(level-1)
   int* lookup = nullptr;      // dense row-major cell -> node index (-1 empty), dense levels only
   bool dense = false;         // M2L as a stencil over the cell grid (m2l.cuh)
+  int* m2l_blk = nullptr;     // distributed mode: observer blocks holding held nodes (dense levels)
+  int m2l_nblk = 0;
   int* child_off = nullptr;   // n_nodes+1 (children at level+1)
   int* children = nullptr;
   int* parent = nullptr;      // n_nodes, parent index at level-1 (or -1)

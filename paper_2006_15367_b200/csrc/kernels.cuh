@@ -253,10 +253,11 @@ __global__ void __launch_bounds__(256) k_m2m_theta(int n_c, int n_p, int CP, int
 
 // ---------------------------------------------------------------------------
 // M2L (operators.cpp:82-87, traversal.cpp:443-581): L_o[s] = sum_far T[o-src][s] M_src[s].
-__global__ void k_m2l(int64_t S, int64_t node_b, const int64_t* __restrict__ far_off,
+// nodes != nullptr (distributed mode): blockIdx.x indexes the held observers.
+__global__ void k_m2l(int64_t S, int64_t node_b, const int* __restrict__ nodes, const int64_t* __restrict__ far_off,
                       const int2* __restrict__ far, const double2* __restrict__ T,
                       const double2* __restrict__ mp, double2* __restrict__ loc) {
-  const int64_t o = node_b + blockIdx.x;
+  const int64_t o = nodes ? int64_t(nodes[blockIdx.x]) : node_b + blockIdx.x;
   const int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
   if (s >= S) return;
   double2 acc = make_double2(0.0, 0.0);

@@ -23,7 +23,10 @@
 
 namespace hfmm_b200 {
 
+// blist != nullptr (distributed mode): blockIdx.x indexes a list of the 8^3
+// observer blocks holding this rank's held nodes.
 __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, int ppc,
+                                                     const int* __restrict__ blist,
                                                      const int* __restrict__ lookup,
                                                      const double2* __restrict__ T,
                                                      const double2* __restrict__ mp,
@@ -35,7 +38,7 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, i
   int* nodes = reinterpret_cast<int*>(Ts + kSlots * 2);
   const double* Md = reinterpret_cast<const double*>(Ms);
   const double* Td = reinterpret_cast<const double*>(Ts);
-  const int blk = blockIdx.x;
+  const int blk = blist ? blist[blockIdx.x] : int(blockIdx.x);
   const int bx = (blk % nb) * MB, by = ((blk / nb) % nb) * MB, bz = (blk / (nb * nb)) * MB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
