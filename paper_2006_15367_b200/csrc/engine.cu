@@ -262,6 +262,19 @@ void Engine::upload() {
       d_sparse_leaves_ = upload_vec(sp);
     }
     l2t_noobs_ = std::getenv("HFMM_L2T_NOOBS") != nullptr;
+    // Near-field phase table (green_tab): r' = k r <= k 2 sqrt(3) leaf side
+    // between particles of adjacent leaves; HFMM_P2P_POLY keeps the sincos
+    // polynomials.
+    {
+      const double rmax = s.k * 2.0 * std::sqrt(3.0) * s.leaf_side;
+      const int ntab = int(std::ceil(rmax * 128.0)) + 2;
+      if (ntab <= kPhaseTabMax && std::getenv("HFMM_P2P_POLY") == nullptr) {
+        std::vector<double2> tab(static_cast<size_t>(ntab));
+        for (int i = 0; i < ntab; ++i) tab[size_t(i)] = make_double2(std::cos(i / 128.0), -std::sin(i / 128.0));
+        d_ptab_ = upload_vec(tab);
+        ptab_max_ = ntab - 1;
+      }
+    }
     if (const char* e = std::getenv("HFMM_PHI_CTAS")) phi_ctas_ = std::max(1, std::atoi(e));
     // symmetric pair lists among own dense leaves (k_p2p_sym2 / k_p2p_gather).
     // k_p2p_sym2 runs one CTA per (leaf, pass of 128 observers): each pass
@@ -904,11 +917,17 @@ void Engine::near_start() {
         if (p2p_items_n_[c] == 0) continue;
         const int2* itm = d_p2p_items_ + p2p_items_b_[c];
         const unsigned g = unsigned(p2p_items_n_[c]);
-#define HFMM_SYM2(NC)                                                                                               \
-  k_p2p_sym2<NC><<<g, 128, 0, st2_>>>(itm, d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_, d_sym_off_, d_sym_, \
-                                      d_sym_scr_, d_sym_rows_, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near,     \
-                                      d_p2p_scratch_)
-        if (c == 3) HFMM_SYM2(4); else if (c == 2) HFMM_SYM2(3); else if (c == 1) HFMM_SYM2(2); else HFMM_SYM2(1);
+#define HFMM_SYM2(NC, TB)                                                                                          \
+  k_p2p_sym2<NC, TB><<<g, 128, 0, st2_>>>(itm, d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_, d_sym_off_,     \
+                                          d_sym_, d_sym_scr_, d_sym_rows_, d.centers, d_x, d_y, d_z, d_q, s_.k,      \
+                                          d_pot_near, d_p2p_scratch_, d_ptab_, ptab_max_)
+        if (d_ptab_) {
+          if (c == 3) HFMM_SYM2(4, true); else if (c == 2) HFMM_SYM2(3, true);
+          else if (c == 1) HFMM_SYM2(2, true); else HFMM_SYM2(1, true);
+        } else {
+          if (c == 3) HFMM_SYM2(4, false); else if (c == 2) HFMM_SYM2(3, false);
+          else if (c == 1) HFMM_SYM2(2, false); else HFMM_SYM2(1, false);
+        }
 #undef HFMM_SYM2
         ++launches_;
       }

@@ -602,6 +602,35 @@ __device__ __forceinline__ void green_scaled(double r2, double& gr, double& gi) 
   gi = mi * __hiloint2double(rhi ^ int(si), rlo);
 }
 
+// exp(-i r') / r' with a table instead of the sincos polynomials, for the
+// bounded near-field range r' <= k 2 sqrt(3) leaf side: tab[n] = (cos(n/128),
+// -sin(n/128)) (host libm), n = round(128 r') (magic add), and the residual
+// d = r' - n/128 (exact, |d| <= 1/256) through short Taylor kernels (omitted
+// terms < 1e-17): 21 FP64 instructions instead of 27.  Indices are clamped
+// to [0, tmax] (idle slots sit at far points with zero charge).
+constexpr int kPhaseTabMax = 1024;
+__device__ __forceinline__ void green_tab(double r2, const double2* __restrict__ tab, int tmax, double& gr,
+                                          double& gi) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double t = r2 * y0;
+  const double e = fma(-t, y0, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  const double ri = fma(y0 * e, p, y0);  // 1 / r'
+  const double x = r2 * ri;             // r'
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+  const double tq = fma(x, 128.0, kMagic);
+  const int n = min(max(__double2loint(tq), 0), tmax);
+  const double d = fma(tq - kMagic, -0.0078125, x);  // r' - n / 128, exact
+  const double d2 = d * d;
+  const double sn = fma(d * d2, fma(d2, 8.3333333333333333e-3, -1.6666666666666667e-1), d);
+  const double cs = fma(d2, fma(d2, 4.1666666666666667e-2, -0.5), 1.0);
+  const double2 c0 = tab[n];  // (cos x0, -sin x0)
+  // exp(-i (x0 + d)) = (cos x0 - i sin x0)(cos d - i sin d)
+  gr = fma(c0.x, cs, c0.y * sn) * ri;
+  gi = fma(c0.y, cs, -(c0.x * sn)) * ri;
+}
+
 __device__ __forceinline__ void p2p_pair(double xo, double yo, double zo, double sx, double sy, double sz,
                                          double2 qq, double& ar, double& ai) {
   const double dx = xo - sx, dy = yo - sy, dz = zo - sz;

@@ -39,8 +39,9 @@ constexpr int kSymObs = HFMM_P2P_SYMOBS;  // observer slots per lane (pass = 32 
 // slots c < u are symmetric pairs, slot c == u only lanes with o < s (the
 // diagonal tile, exact-zero self pair excluded), slots c > u are skipped --
 // those pairs are taken when the roles are swapped.
-template <int NC, int M, bool SELF>
-__device__ __forceinline__ void sym_block(P2PShared& sh, double k, double cx, double cy, double cz, double qs,
+template <int NC, int M, bool SELF, bool TAB>
+__device__ __forceinline__ void sym_block(P2PShared& sh, const double2* __restrict__ tab, int tmax, double k,
+                                          double cx, double cy, double cz, double qs,
                                           int64_t b0, int64_t nbp, double2* __restrict__ scr,
                                           const double* __restrict__ x, const double* __restrict__ y,
                                           const double* __restrict__ z, const double2* __restrict__ q,
@@ -85,7 +86,7 @@ __device__ __forceinline__ void sym_block(P2PShared& sh, double k, double cx, do
           const bool keep = !SELF || c < u || lane < (srel & 31);
           if (SELF) r2 = keep ? r2 : 1.0;
           double gr, gi;
-          green_scaled(r2, gr, gi);
+          if constexpr (TAB) green_tab(r2, tab, tmax, gr, gi); else green_scaled(r2, gr, gi);
           if (SELF) {
             gr = keep ? gr : 0.0;
             gi = keep ? gi : 0.0;
@@ -138,8 +139,9 @@ __device__ __forceinline__ void sym_block(P2PShared& sh, double k, double cx, do
 
 // Symmetric dense-leaf near field: as k_p2p_sym (same lists, scratch layout
 // and gather), with the pair loop above.  Block = 128 threads.
-template <int NC, int M>
-__device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double k, double cx, double cy,
+template <int NC, int M, bool TAB>
+__device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, const double2* __restrict__ tab, int tmax, int n_o_pass,
+                                             double k, double cx, double cy,
                                              double cz, double qs, int64_t leaf, int ob, int64_t p0, int64_t total,
                                              const int* __restrict__ sym, int j0, int j1,
                                              const int64_t* __restrict__ sym_scr, int64_t scr_pass,
@@ -179,7 +181,7 @@ __device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const bool self = r2 == 0.0;
         double gr, gi;
-        green_scaled(self ? 1.0 : r2, gr, gi);
+        if constexpr (TAB) green_tab(self ? 1.0 : r2, tab, tmax, gr, gi); else green_scaled(self ? 1.0 : r2, gr, gi);
         gr = self ? 0.0 : gr;
         gi = self ? 0.0 : gi;
         ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
@@ -195,11 +197,11 @@ __device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double
     if (lb == leaf) {
       for (int t = threadIdx.x; t < ob; t += blockDim.x) scr[t] = make_double2(0.0, 0.0);  // earlier passes' rows
       const int64_t b0 = leaf_start[lb] + ob;
-      sym_block<NC, M, true>(sh, k, cx, cy, cz, qs, b0, leaf_start[lb + 1] - b0, scr + ob, x, y, z, q, xo, yo, zo, qr,
+      sym_block<NC, M, true, TAB>(sh, tab, tmax, k, cx, cy, cz, qs, b0, leaf_start[lb + 1] - b0, scr + ob, x, y, z, q, xo, yo, zo, qr,
                              qi, ar, ai);
     } else {
       const int64_t b0 = leaf_start[lb];
-      sym_block<NC, M, false>(sh, k, cx, cy, cz, qs, b0, leaf_start[lb + 1] - b0, scr, x, y, z, q, xo, yo, zo, qr,
+      sym_block<NC, M, false, TAB>(sh, tab, tmax, k, cx, cy, cz, qs, b0, leaf_start[lb + 1] - b0, scr, x, y, z, q, xo, yo, zo, qr,
                               qi, ar, ai);
     }
   }
@@ -230,7 +232,7 @@ __device__ __forceinline__ void p2p_sym_pass(P2PShared& sh, int n_o_pass, double
 #ifndef HFMM_P2P_MINB
 #define HFMM_P2P_MINB 4  // CTAs per SM the register budget is sized for
 #endif
-template <int NC>
+template <int NC, bool TAB>
 __global__ void __launch_bounds__(128, HFMM_P2P_MINB) k_p2p_sym2(const int2* __restrict__ items, const int* __restrict__ leaves,
                                                      const int64_t* __restrict__ leaf_start,
                                                      const int* __restrict__ plain_off, const int* __restrict__ plain,
@@ -240,9 +242,14 @@ __global__ void __launch_bounds__(128, HFMM_P2P_MINB) k_p2p_sym2(const int2* __r
                                                      const double* __restrict__ centers, const double* __restrict__ x,
                                                      const double* __restrict__ y, const double* __restrict__ z,
                                                      const double2* __restrict__ q, double k,
-                                                     double2* __restrict__ pot, double2* __restrict__ scratch) {
+                                                     double2* __restrict__ pot, double2* __restrict__ scratch,
+                                                     const double2* __restrict__ ptab, int tmax) {
   __shared__ P2PShared sh;
   __shared__ double2 red[4][32 * kSymObs];
+  __shared__ double2 stab[TAB ? kPhaseTabMax : 1];
+  if constexpr (TAB) {
+    for (int t = threadIdx.x; t <= tmax; t += blockDim.x) stab[t] = ptab[t];  // visible after the next barrier
+  }
   const int2 item = items[blockIdx.x];
   const int i = item.x, pass = item.y;
   const int64_t leaf = leaves[i];
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(128, HFMM_P2P_MINB) k_p2p_sym2(const int2* __r
   const int64_t total = sh.pref[sh.nn];
   const int ob = pass * 32 * kSymObs;
   const int no = min(int(p1 - p0) - ob, 32 * kSymObs);
-  p2p_sym_pass<NC, HFMM_P2P_M>(sh, no, k, cx, cy, cz, qs, leaf, ob, p0 + ob, total, sym, sym_off[i], sym_off[i + 1],
+  p2p_sym_pass<NC, HFMM_P2P_M, TAB>(sh, stab, tmax, no, k, cx, cy, cz, qs, leaf, ob, p0 + ob, total, sym, sym_off[i], sym_off[i + 1],
                                sym_scr, int64_t(pass) * sym_rows[i], leaf_start, x, y, z, q, pot, scratch, red);
 }
 
