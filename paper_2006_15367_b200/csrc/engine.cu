@@ -262,6 +262,18 @@ void Engine::upload() {
       d_sparse_leaves_ = upload_vec(sp);
     }
     l2t_noobs_ = std::getenv("HFMM_L2T_NOOBS") != nullptr;
+    // Leaf phase table (sincos_l): |A| <= k side / sqrt 2, |B| <= k side / 2
+    // for particles in their leaf; HFMM_LEAF_POLY keeps the polynomials.
+    {
+      const double amax = s.k * s.leaf_side / std::sqrt(2.0);
+      const int nh = int(std::ceil(amax * 128.0)) + 2;
+      if (nh <= kLeafTabMax && std::getenv("HFMM_LEAF_POLY") == nullptr) {
+        std::vector<double2> tab(static_cast<size_t>(2 * nh + 1));
+        for (int i = -nh; i <= nh; ++i) tab[size_t(i + nh)] = make_double2(std::cos(i / 128.0), std::sin(i / 128.0));
+        d_ltab_ = upload_vec(tab);
+        ltab_half_ = nh;
+      }
+    }
     // Near-field phase table (green_tab): r' = k r <= k 2 sqrt(3) leaf side
     // between particles of adjacent leaves; HFMM_P2P_POLY keeps the sincos
     // polynomials.
@@ -574,9 +586,12 @@ void Engine::phase_c2m() {
       }
     }
     const unsigned g = unsigned((nl + 3) / 4);
-#define HFMM_C2M(RR, HN)                                                                                      \
-  k_c2m_quad2<RR, HN><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.nt, \
-                                          s_.k, d.mp)
+#define HFMM_C2M(RR, HN)                                                                                       \
+  do {                                                                                                          \
+    /* the phase table measured slower in C2M (a dependent load in its inner loop): polynomials */             \
+    k_c2m_quad2<RR, HN, false><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,      \
+                                                   d.dir, d.nt, s_.k, d.mp);                                    \
+  } while (0)
     const int hn = int(d.nt / 2);
     if (r == 3 && hn == 9) HFMM_C2M(3, 9);        // n = 18 (configs 1, 3, 4)
     else if (r == 4 && hn == 11) HFMM_C2M(4, 11);  // n = 22 (config 5)
@@ -844,8 +859,14 @@ void Engine::phase_l2t() {
       auto l2t_quads = [&](unsigned grid, int64_t lb, int64_t cnt, const int* list) {
         const int hn = int(d.nt / 2);
 #define HFMM_L2TQ(HN)                                                                                          \
-  k_l2t_quad2<HN><<<grid, 128, smem, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, \
-                                            d.nt, s_.k, d.loc, d_pot)
+  do {                                                                                                          \
+    if (d_ltab_)                                                                                                \
+      k_l2t_quad2<HN, true><<<grid, 128, smem, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers,      \
+                                                      d.dir, d.wq, d.nt, s_.k, d.loc, d_pot, d_ltab_, ltab_half_);\
+    else                                                                                                        \
+      k_l2t_quad2<HN, false><<<grid, 128, smem, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers,     \
+                                                       d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);                  \
+  } while (0)
         if (hn == 9) HFMM_L2TQ(9);
         else if (hn == 11) HFMM_L2TQ(11);
         else if (hn == 13) HFMM_L2TQ(13);
@@ -858,11 +879,17 @@ void Engine::phase_l2t() {
         const int hn = int(d.nt / 2);
 #define HFMM_L2TO(HN)                                                                                          \
   do {                                                                                                         \
-    if (so > 48 * 1024)                                                                                        \
-      ck(cudaFuncSetAttribute(k_l2t_obs<HN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(so)), "attr");   \
-    k_l2t_obs<HN><<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(n_dense_, d_dense_leaves_, d_leaf_start, d_x, \
-                                                                  d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, \
-                                                                  d.loc, d_pot);                                \
+    if (so > 24 * 1024) {                                                                                      \
+      ck(cudaFuncSetAttribute(k_l2t_obs<HN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(so)), "a"); \
+      ck(cudaFuncSetAttribute(k_l2t_obs<HN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(so)), "a"); \
+    }                                                                                                          \
+    if (d_ltab_)                                                                                               \
+      k_l2t_obs<HN, true><<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(                                      \
+          n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot, \
+          d_ltab_, ltab_half_);                                                                                \
+    else                                                                                                       \
+      k_l2t_obs<HN, false><<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(                                     \
+          n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot); \
   } while (0)
         if (hn == 9) HFMM_L2TO(9);
         else if (hn == 11) HFMM_L2TO(11);
@@ -897,14 +924,23 @@ void Engine::near_start() {
   if (cnt > 0)
     ck(cudaMemsetAsync(d_pot_near + part_b_, 0, size_t(cnt) * sizeof(double2), st2_), "memset near");
   if (n_tiny_ > 0) {
-    k_p2p_small_w<<<unsigned((n_tiny_ + 3) / 4), 128, 0, st2_>>>(n_tiny_, d_tiny_leaves_, d_leaf_start, d_near_off,
-                                                                 d_near, d.centers, d_x, d_y, d_z, d_q, s_.k,
-                                                                 d_pot_near);
+    if (d_ptab_)
+      k_p2p_small_w<true><<<unsigned((n_tiny_ + 3) / 4), 128, 0, st2_>>>(
+          n_tiny_, d_tiny_leaves_, d_leaf_start, d_near_off, d_near, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near,
+          d_ptab_, ptab_max_);
+    else
+      k_p2p_small_w<false><<<unsigned((n_tiny_ + 3) / 4), 128, 0, st2_>>>(
+          n_tiny_, d_tiny_leaves_, d_leaf_start, d_near_off, d_near, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near);
     ++launches_;
   }
   if (n_small_ > 0) {
-    k_p2p<false><<<unsigned(n_small_), 128, 0, st2_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
-                                                       d_x, d_y, d_z, d_q, s_.k, d_pot_near);
+    if (d_ptab_)
+      k_p2p<false, true><<<unsigned(n_small_), 128, 0, st2_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near,
+                                                               d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near,
+                                                               d_ptab_, ptab_max_);
+    else
+      k_p2p<false><<<unsigned(n_small_), 128, 0, st2_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near,
+                                                         d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near);
     ++launches_;
   }
   if (n_dense_ > 0 && use_sym_) {

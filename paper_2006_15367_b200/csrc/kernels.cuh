@@ -625,19 +625,21 @@ __device__ __forceinline__ void green_tab(double r2, const double2* __restrict__
   const double d2 = d * d;
   const double sn = fma(d * d2, fma(d2, 8.3333333333333333e-3, -1.6666666666666667e-1), d);
   const double cs = fma(d2, fma(d2, 4.1666666666666667e-2, -0.5), 1.0);
-  const double2 c0 = tab[n];  // (cos x0, -sin x0)
+  const double2 c0 = tab[n];  // (cos x0, -sin x0); shared (symmetric kernel) or global (small leaves)
   // exp(-i (x0 + d)) = (cos x0 - i sin x0)(cos d - i sin d)
   gr = fma(c0.x, cs, c0.y * sn) * ri;
   gi = fma(c0.y, cs, -(c0.x * sn)) * ri;
 }
 
+template <bool TAB = false>
 __device__ __forceinline__ void p2p_pair(double xo, double yo, double zo, double sx, double sy, double sz,
-                                         double2 qq, double& ar, double& ai) {
+                                         double2 qq, double& ar, double& ai, const double2* __restrict__ tab = nullptr,
+                                         int tmax = 0) {
   const double dx = xo - sx, dy = yo - sy, dz = zo - sz;
   const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
   const bool self = r2 == 0.0;  // exact-zero separation (operators.cpp:118)
   double gr, gi;
-  green_scaled(self ? 1.0 : r2, gr, gi);
+  if constexpr (TAB) green_tab(self ? 1.0 : r2, tab, tmax, gr, gi); else green_scaled(self ? 1.0 : r2, gr, gi);
   gr = self ? 0.0 : gr;
   gi = self ? 0.0 : gi;
   ar = fma(gr, qq.x, fma(-gi, qq.y, ar));
@@ -693,13 +695,15 @@ __device__ __forceinline__ void p2p_stage(P2PShared& sh, int64_t cb, int n, cons
   }
 }
 
-template <bool DENSE>
+template <bool DENSE, bool TAB = false>
 __global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
                                              const int64_t* __restrict__ near_off, const int* __restrict__ near,
                                              const double* __restrict__ centers, const double* __restrict__ x,
                                              const double* __restrict__ y, const double* __restrict__ z,
-                                             const double2* __restrict__ q, double k, double2* __restrict__ pot) {
+                                             const double2* __restrict__ q, double k, double2* __restrict__ pot,
+                                             const double2* __restrict__ ptab = nullptr, int tmax = 0) {
   __shared__ P2PShared sh;
+  const double2* stab = ptab;  // small CTAs: the table is read through L1 (no staging)
   const int64_t leaf = leaves[blockIdx.x];
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const int n_o = int(p1 - p0);
@@ -721,7 +725,8 @@ __global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, con
       p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
       __syncthreads();
       if (valid)
-        for (int t = j; t < n; t += G) p2p_pair(xo, yo, zo, sh.sx[t], sh.sy[t], sh.sz[t], sh.sq[t], ar, ai);
+        for (int t = j; t < n; t += G)
+          p2p_pair<TAB>(xo, yo, zo, sh.sx[t], sh.sy[t], sh.sz[t], sh.sq[t], ar, ai, stab, tmax);
     }
     for (int off = G >> 1; off > 0; off >>= 1) {
       ar += __shfl_down_sync(0xffffffffu, ar, off, G);
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, con
         const double2 qq = sh.sq[t];
 #pragma unroll
         for (int c = 0; c < kP2PObsPerLane; ++c)
-          if (c < nc) p2p_pair(xo[c], yo[c], zo[c], px, py, pz, qq, ar[c], ai[c]);
+          if (c < nc) p2p_pair<TAB>(xo[c], yo[c], zo[c], px, py, pz, qq, ar[c], ai[c], stab, tmax);
       }
     }
 #pragma unroll
@@ -787,15 +792,18 @@ __global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, con
 // sums come from a warp scan, sources are staged kSW at a time in warp-private
 // shared memory (__syncwarp only), G = 32 / n_o lanes share an observer.
 constexpr int kSW = 64;
+template <bool TAB = false>
 __global__ void __launch_bounds__(128) k_p2p_small_w(int n_small, const int* __restrict__ leaves,
                                                      const int64_t* __restrict__ leaf_start,
                                                      const int64_t* __restrict__ near_off, const int* __restrict__ near,
                                                      const double* __restrict__ centers, const double* __restrict__ x,
                                                      const double* __restrict__ y, const double* __restrict__ z,
-                                                     const double2* __restrict__ q, double k, double2* __restrict__ pot) {
+                                                     const double2* __restrict__ q, double k, double2* __restrict__ pot,
+                                                     const double2* __restrict__ ptab = nullptr, int tmax = 0) {
   __shared__ double sx[4][kSW], sy[4][kSW], sz[4][kSW];
   __shared__ double2 sq[4][kSW];
   __shared__ int64_t spref[4][32], sbeg[4][32];
+  const double2* stab = ptab;  // small CTAs: the table is read through L1 (no staging)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * 4 + warp;
   if (i >= n_small) return;  // whole warp
@@ -848,7 +856,8 @@ __global__ void __launch_bounds__(128) k_p2p_small_w(int n_small, const int* __r
     }
     __syncwarp();
     if (valid)
-      for (int t = sub; t < n; t += G) p2p_pair(xo, yo, zo, sx[warp][t], sy[warp][t], sz[warp][t], sq[warp][t], ar, ai);
+      for (int t = sub; t < n; t += G)
+        p2p_pair<TAB>(xo, yo, zo, sx[warp][t], sy[warp][t], sz[warp][t], sq[warp][t], ar, ai, stab, tmax);
   }
   for (int off = G >> 1; off > 0; off >>= 1) {
     ar += __shfl_xor_sync(0xffffffffu, ar, off);

@@ -54,6 +54,30 @@ __device__ __forceinline__ void sincos_q(double x, double& sp, double& cp) {
   cp = xor_sign(swap ? sn : cs, (q30 + 0x40000000u) & 0x80000000u);  // cos < 0 for quad 1, 2
 }
 
+// sin, cos for the bounded leaf-level phases (|x| <= k side / sqrt 2 for A,
+// k side / 2 for B) from a table tab[n] = (cos(n/128), sin(n/128)),
+// n in [-nh, nh] (tab points at n = 0), with the exact residual
+// |d| <= 1/256 through short Taylor kernels: 13 FP64 instructions instead
+// of 19.  TAB = false: the polynomial sincos_q.
+constexpr int kLeafTabMax = 256;  // |phase| <= 2 (leaf side <= 0.45 wavelengths)
+template <bool TAB>
+__device__ __forceinline__ void sincos_l(double x, const double2* __restrict__ tab, int nh, double& sp, double& cp) {
+  if constexpr (!TAB) {
+    sincos_q(x, sp, cp);
+  } else {
+    const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    const double tq = fma(x, 128.0, kMagic);
+    const int n = min(max(__double2loint(tq), -nh), nh);
+    const double d = fma(tq - kMagic, -0.0078125, x);  // x - n / 128, exact
+    const double d2 = d * d;
+    const double sd = fma(d * d2, fma(d2, 8.3333333333333333e-3, -1.6666666666666667e-1), d);
+    const double cd = fma(d2, fma(d2, 4.1666666666666667e-2, -0.5), 1.0);
+    const double2 c0 = __ldg(tab + n);
+    sp = fma(c0.y, cd, c0.x * sd);
+    cp = fma(c0.x, cd, -(c0.y * sd));
+  }
+}
+
 constexpr int kQuadP2 = 16;  // particles per table chunk
 #ifndef HFMM_C2M_UNROLL
 #define HFMM_C2M_UNROLL 1
@@ -68,13 +92,15 @@ constexpr int kL2TUnroll = HFMM_L2T_UNROLL;  // quad loop unroll (populous-leaf 
 // is one pass and its (Q+, Q-) table is built once.
 // HN > 0: n / 2 known at compile time (the BASELINE leaf grids n = 18, 22, 26),
 // so quad indices and table rows need no integer division at run time.
-template <int R, int HN = 0>
+template <int R, int HN = 0, bool TAB = false>
 __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
                                                    const double* __restrict__ z, const double2* __restrict__ q,
                                                    const double* __restrict__ centers, const double* __restrict__ dir,
-                                                   int n, double k, double2* __restrict__ mp) {
+                                                   int n, double k, double2* __restrict__ mp,
+                                                   const double2* __restrict__ ltab = nullptr, int nh = 0) {
   __shared__ double4 sQ[4][kQuadP2][kQuadHalfMax];  // (Q+, Q-) per particle and theta row
+  const double2* tb = TAB ? ltab + nh : nullptr;  // read through L1 (small CTAs: no staging)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t li = int64_t(blockIdx.x) * 4 + warp;
   if (li >= nl) return;  // whole warp
@@ -105,7 +131,7 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
       for (int t = lane; t < np * half; t += 32) {
         const int pp = t / half, i = t - pp * half;
         double sb, cb;
-        sincos_q(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), sb, cb);
+        sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sb, cb);
         const double2 qq = q[pc + pp];
         Qt[pp][i] = make_double4(fma(qq.x, cb, -qq.y * sb), fma(qq.x, sb, qq.y * cb),   // q e^{iB}
                                  fma(qq.x, cb, qq.y * sb), fma(qq.y, cb, -qq.x * sb));  // q e^{-iB}
@@ -117,7 +143,7 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           double sa, ca;
-          sincos_q(fma(ax[r], rx, ay[r] * ry), sa, ca);
+          sincos_l<TAB>(fma(ax[r], rx, ay[r] * ry), tb, nh, sa, ca);
           const double4 Q = Qt[pp][qi[r]];
           upx[r] = fma(Q.x, ca, upx[r]);
           upy[r] = fma(Q.x, sa, upy[r]);
@@ -150,15 +176,17 @@ __global__ void __launch_bounds__(128) k_c2m_quad2(int64_t leaf_b, int64_t nl, c
 // (warp-shuffle reduction per observer), e^{iB} table per particle and row.
 // leaves != nullptr: warp w takes leaves[w] (a population class), else leaf_b + w.
 // HN as in k_c2m_quad2.
-template <int HN = 0>
+template <int HN = 0, bool TAB = false>
 __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
                                                    const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
                                                    const double* __restrict__ z, const double* __restrict__ centers,
                                                    const double* __restrict__ dir, const double* __restrict__ wq,
                                                    int n, double k, const double2* __restrict__ loc,
-                                                   double2* __restrict__ pot) {
+                                                   double2* __restrict__ pot, const double2* __restrict__ ltab = nullptr,
+                                                   int nh = 0) {
   extern __shared__ double2 qsm[];
+  const double2* tb = TAB ? ltab + nh : nullptr;  // read through L1 (small CTAs: no staging)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = HN > 0 ? HN : n / 2, quads = half * half, nphi = HN > 0 ? 2 * HN : n;
   const int64_t S = int64_t(n) * n;
@@ -176,7 +204,7 @@ __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, c
     for (int t = lane; t < np * half; t += 32) {
       const int pp = t / half, i = t - pp * half;
       double sn, cs;
-      sincos_q(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), sn, cs);
+      sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sn, cs);
       Bt[pp * half + i] = make_double2(cs, sn);
     }
     __syncwarp();
@@ -210,7 +238,7 @@ __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, c
         for (int o = 0; o < kQuadOB; ++o) {
           const int pp = pb + o < np ? pb + o : pb;
           double sa, ca;
-          sincos_q(fma(dxs, rx[o], dys * ry[o]), sa, ca);
+          sincos_l<TAB>(fma(dxs, rx[o], dys * ry[o]), tb, nh, sa, ca);
           const double2 eb = Bt[pp * half + i];
           const double u = eb.x * ca, v = eb.x * sa, w = eb.y * ca, zz = eb.y * sa;
           ar[o] = fma(u, G.x, fma(-v, Gp.y, fma(-w, H.y, fma(-zz, Hp.x, ar[o]))));
@@ -237,14 +265,16 @@ __global__ void __launch_bounds__(128) k_l2t_quad2(int64_t leaf_b, int64_t nl, c
 // Y = sum_j (i cos A H - sin A H') (8 FMA per quad), then
 // acc += cos B_i X + sin B_i Y.  No cross-lane reduction.
 // Shared memory per warp: quads x (4 + 1) double2.
-template <int HN = 0>
+template <int HN = 0, bool TAB = false>
 __global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restrict__ leaves,
                                                  const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
                                                  const double* __restrict__ y, const double* __restrict__ z,
                                                  const double* __restrict__ centers, const double* __restrict__ dir,
                                                  const double* __restrict__ wq, int n, double k,
-                                                 const double2* __restrict__ loc, double2* __restrict__ pot) {
+                                                 const double2* __restrict__ loc, double2* __restrict__ pot,
+                                                 const double2* __restrict__ ltab = nullptr, int nh = 0) {
   extern __shared__ double2 osm[];
+  const double2* tb = TAB ? ltab + nh : nullptr;  // read through L1 (small CTAs: no staging)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = HN > 0 ? HN : n / 2, quads = half * half, nphi = HN > 0 ? 2 * HN : n;
   const int64_t S = int64_t(n) * n;
@@ -287,7 +317,7 @@ __global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restri
       for (int j = 0; j < half; ++j, q += 5) {
         const double2 a = q[4];
         double sa, ca;
-        sincos_q(fma(a.x, rx, a.y * ry), sa, ca);
+        sincos_l<TAB>(fma(a.x, rx, a.y * ry), tb, nh, sa, ca);
         const double2 G = q[0], Gp = q[1], H = q[2], Hp = q[3];
         xr = fma(ca, G.x, fma(-sa, Gp.y, xr));
         xi = fma(ca, G.y, fma(sa, Gp.x, xi));
@@ -295,7 +325,7 @@ __global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restri
         yi = fma(ca, H.x, fma(-sa, Hp.y, yi));
       }
       double sb, cb;
-      sincos_q(k * dir[3 * int64_t(i) * nphi + 2] * rz, sb, cb);
+      sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * rz, tb, nh, sb, cb);
       ar = fma(cb, xr, fma(sb, yr, ar));
       ai = fma(cb, xi, fma(sb, yi, ai));
     }

@@ -191,3 +191,19 @@ def test_full_size_configs_vs_direct(cfg, bound, hb, refo):
     res2 = eng.evaluate(1j * q)
     assert rel_l2(res2.potentials, 1j * res.potentials) < 1e-10  # re/im swap: rounding differs (2.6e-12 at cfg2)
     assert np.array_equal(eng.evaluate(q).potentials, res.potentials)  # deterministic
+
+
+def test_phase_tables_match_polynomials(hb, monkeypatch):
+    """The near-field and leaf phase tables (green_tab, sincos_l) against the
+    sincos polynomials they replace (HFMM_P2P_POLY, HFMM_LEAF_POLY): a sphere
+    (dense and small leaves, populous-leaf L2T) and a cube (quad L2T)."""
+    for shape, n, ext, seed in (("sphere", 60_000, 2.0, 71), ("cube", 40_000, 3.0, 72)):
+        pos, q = hb.generate_inputs(shape, n, ext, seed)
+        setup = hb.build_setup(pos, q, hb.RunConfig(digits=4.0))
+        tab = hb.RankEngine(setup).evaluate().potentials
+        monkeypatch.setenv("HFMM_P2P_POLY", "1")
+        monkeypatch.setenv("HFMM_LEAF_POLY", "1")
+        poly = hb.RankEngine(setup).evaluate().potentials
+        monkeypatch.delenv("HFMM_P2P_POLY")
+        monkeypatch.delenv("HFMM_LEAF_POLY")
+        assert rel_l2(tab, poly) < 1e-12, (shape, rel_l2(tab, poly))
