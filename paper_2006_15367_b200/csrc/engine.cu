@@ -262,6 +262,9 @@ void Engine::upload() {
       d_sparse_leaves_ = upload_vec(sp);
     }
     l2t_noobs_ = std::getenv("HFMM_L2T_NOOBS") != nullptr;
+    near_seq_ = std::getenv("HFMM_NEAR_SEQ") != nullptr;  // near field after L2T even in overlap mode
+    m2l_seq_ = std::getenv("HFMM_M2L_SEQ") != nullptr;    // leaf M2L inside the chain even in overlap mode
+    tune_ = !m2l_seq_ && std::getenv("HFMM_NO_TUNE") == nullptr;
     // Leaf phase table (sincos_l): |A| <= k side / sqrt 2, |B| <= k side / 2
     // for particles in their leaf; HFMM_LEAF_POLY keeps the polynomials.
     {
@@ -1064,12 +1067,33 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
   const int64_t n = int64_t(s_.n);
   if (d_q_sorted && d_q_sorted != reinterpret_cast<const double*>(d_q))
     ck(cudaMemcpyAsync(d_q, d_q_sorted, size_t(n) * sizeof(double2), cudaMemcpyDeviceToDevice, st_), "q");
+  // Schedule autotune (overlap mode): the leaf-level M2L beside the chain
+  // helps configs 2 and 3 and costs configs 4 and 5 (measured); evaluation 1
+  // runs it beside the chain, evaluation 2 inside it, and from evaluation 3
+  // on the faster of the two (each timed by its own ev_[0] -> ev_[7]).
+  if (overlap_ && tune_ && !tune_done_) {
+    if (tune_evals_ == 2 || tune_evals_ == 3) {
+      float f = 0.f;
+      ck(cudaEventSynchronize(ev_[7]), "tune sync");
+      ck(cudaEventElapsedTime(&f, ev_[0], ev_[7]), "tune time");
+      tune_ms_[tune_evals_ - 2] = f;
+    }
+    if (tune_evals_ == 1) {
+      m2l_seq_ = false;
+    } else if (tune_evals_ == 2) {
+      m2l_seq_ = true;
+    } else if (tune_evals_ == 3) {
+      m2l_seq_ = tune_ms_[1] < tune_ms_[0];
+      tune_done_ = true;
+    }
+    ++tune_evals_;
+  }
   cudaEventRecord(ev_[0], st_);
   // The far-field chain runs on a high-priority stream; the leaf-level M2L
   // (it needs only C2M's multipoles and is consumed only by the last L2L
   // step) runs beside it on a low-priority stream and fills the SMs that the
   // small upper-level kernels leave idle.  Dependencies are unchanged.
-  const bool overlap = overlap_ && s_.L > s_.top;
+  const bool overlap = overlap_ && s_.L > s_.top && !m2l_seq_;
   cudaStream_t user = st_;
   overlapped_ = overlap;
   if (overlap) {
@@ -1087,7 +1111,7 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
   }
   // Near field: side stream, overlapped with the far-field chain; in the
   // sequential mode (set_overlap off) it runs after L2T, inside phase_near.
-  if (overlap_) near_start();
+  if (overlap_ && !near_seq_) near_start();
   if (!t_first) build_T();
   cudaEventRecord(ev_[1], st_);
   phase_c2m();

@@ -188,6 +188,10 @@ class Engine {
   int n_sparse_ = 0;
   bool l2t_noobs_ = false;
   int phi_ctas_ = 2;
+  bool near_seq_ = false, m2l_seq_ = false;  // schedule knobs (HFMM_NEAR_SEQ, HFMM_M2L_SEQ)
+  bool tune_ = true, tune_done_ = false;     // leaf-M2L placement autotune (evaluate_device)
+  int tune_evals_ = 0;
+  float tune_ms_[2] = {0.f, 0.f};
   double2* d_ptab_ = nullptr;  // near-field phase table (green_tab), nullptr: sincos polynomials
   int ptab_max_ = 0;
   double2* d_ltab_ = nullptr;  // leaf phase table (sincos_l), centred; nullptr: polynomials
