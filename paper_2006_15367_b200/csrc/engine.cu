@@ -263,6 +263,7 @@ void Engine::upload() {
     }
     l2t_noobs_ = std::getenv("HFMM_L2T_NOOBS") != nullptr;
     near_seq_ = std::getenv("HFMM_NEAR_SEQ") != nullptr;  // near field after L2T even in overlap mode
+    c2m_tab_ = std::getenv("HFMM_C2M_TAB") != nullptr;
     m2l_seq_ = std::getenv("HFMM_M2L_SEQ") != nullptr;    // leaf M2L inside the chain even in overlap mode
     tune_ = !m2l_seq_ && std::getenv("HFMM_NO_TUNE") == nullptr;
     // Leaf phase table (sincos_l): |A| <= k side / sqrt 2, |B| <= k side / 2
@@ -591,9 +592,12 @@ void Engine::phase_c2m() {
     const unsigned g = unsigned((nl + 3) / 4);
 #define HFMM_C2M(RR, HN)                                                                                       \
   do {                                                                                                          \
-    /* the phase table measured slower in C2M (a dependent load in its inner loop): polynomials */             \
-    k_c2m_quad2<RR, HN, false><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,      \
-                                                   d.dir, d.nt, s_.k, d.mp);                                    \
+    if (d_ltab_ && c2m_tab_)                                                                                   \
+      k_c2m_quad2<RR, HN, true><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,     \
+                                                    d.dir, d.nt, s_.k, d.mp, d_ltab_, ltab_half_);              \
+    else                                                                                                        \
+      k_c2m_quad2<RR, HN, false><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,    \
+                                                     d.dir, d.nt, s_.k, d.mp);                                  \
   } while (0)
     const int hn = int(d.nt / 2);
     if (r == 3 && hn == 9) HFMM_C2M(3, 9);        // n = 18 (configs 1, 3, 4)

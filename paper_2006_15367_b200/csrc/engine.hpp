@@ -195,7 +195,8 @@ class Engine {
   double2* d_ptab_ = nullptr;  // near-field phase table (green_tab), nullptr: sincos polynomials
   int ptab_max_ = 0;
   double2* d_ltab_ = nullptr;  // leaf phase table (sincos_l), centred; nullptr: polynomials
-  int ltab_half_ = 0;  // persistent CTAs per SM of the streaming phi passes (HFMM_PHI_CTAS)  // HFMM_L2T_NOOBS: lanes-over-quads L2T for every leaf (A/B)  // HFMM_LEAF_V1: the previous quad C2M / L2T kernels (A/B)  // HFMM_P2P_V1: the previous symmetric kernel (A/B)
+  int ltab_half_ = 0;
+  bool c2m_tab_ = false;  // C2M on the leaf phase table (HFMM_C2M_TAB)  // persistent CTAs per SM of the streaming phi passes (HFMM_PHI_CTAS)  // HFMM_L2T_NOOBS: lanes-over-quads L2T for every leaf (A/B)  // HFMM_LEAF_V1: the previous quad C2M / L2T kernels (A/B)  // HFMM_P2P_V1: the previous symmetric kernel (A/B)
   double2* d_tmp = nullptr;  // interpolation temporaries
   size_t tmp_elems_ = 0;
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range
