@@ -78,8 +78,12 @@ __device__ __forceinline__ void sincos_l(double x, const double2* __restrict__ t
   }
 }
 
-#ifndef HFMM_LEAF_MINB
-#define HFMM_LEAF_MINB 1  // CTAs per SM the register budget is sized for (quad C2M / L2T)
+// HFMM_LEAF_MINB (dev knob): CTAs per SM the register budget of the quad C2M /
+// L2T kernels is sized for; unset = the compiler's choice (measured best).
+#ifdef HFMM_LEAF_MINB
+#define HFMM_LEAF_LB __launch_bounds__(128, HFMM_LEAF_MINB)
+#else
+#define HFMM_LEAF_LB __launch_bounds__(128)
 #endif
 constexpr int kQuadP2 = 16;  // particles per table chunk
 #ifndef HFMM_C2M_UNROLL
@@ -96,7 +100,7 @@ constexpr int kL2TUnroll = HFMM_L2T_UNROLL;  // quad loop unroll (populous-leaf 
 // HN > 0: n / 2 known at compile time (the BASELINE leaf grids n = 18, 22, 26),
 // so quad indices and table rows need no integer division at run time.
 template <int R, int HN = 0, bool TAB = false>
-__global__ void __launch_bounds__(128, HFMM_LEAF_MINB) k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
+__global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
                                                    const double* __restrict__ z, const double2* __restrict__ q,
                                                    const double* __restrict__ centers, const double* __restrict__ dir,
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(128, HFMM_LEAF_MINB) k_c2m_quad2(int64_t leaf_
 // leaves != nullptr: warp w takes leaves[w] (a population class), else leaf_b + w.
 // HN as in k_c2m_quad2.
 template <int HN = 0, bool TAB = false>
-__global__ void __launch_bounds__(128, HFMM_LEAF_MINB) k_l2t_quad2(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
+__global__ void HFMM_LEAF_LB k_l2t_quad2(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
                                                    const int64_t* __restrict__ leaf_start,
                                                    const double* __restrict__ x, const double* __restrict__ y,
                                                    const double* __restrict__ z, const double* __restrict__ centers,
