@@ -619,7 +619,10 @@ __device__ __forceinline__ void green_tab(double r2, const double2* __restrict__
   const double ri = fma(y0 * e, p, y0);  // 1 / r'
   const double x = r2 * ri;             // r'
   const double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-  const double tq = fma(x, 128.0, kMagic);
+  // table index from the unrefined r' (t = r2 y0, relative error ~2^-22): the
+  // table load does not wait for the Newton step; |d| <= 1/256 + 2e-6 still
+  // keeps the omitted Taylor terms below 1e-17
+  const double tq = fma(t, 128.0, kMagic);
   const int n = min(max(__double2loint(tq), 0), tmax);
   const double d = fma(tq - kMagic, -0.0078125, x);  // r' - n / 128, exact
   const double d2 = d * d;
