@@ -124,7 +124,10 @@ typedef struct hfmm_gpu_timing {
 /* Creates an engine on CUDA device `device` for logical rank `rank` of the
  * setup's partition.  Uploads the setup (sorted particles, level tables,
  * lists, samplings, interpolation matrices, translation coefficients).
- * Replaces RankEngine's constructor (traversal.cpp:242-288). */
+ * Replaces RankEngine's constructor (traversal.cpp:242-288).  The engine
+ * shares ownership of the setup: the caller may hfmm_setup_destroy() the
+ * setup handle at any time; the data stays alive until the last engine made
+ * from it is destroyed. */
 hfmm_status hfmm_gpu_create(const hfmm_setup* s, int device, int rank,
                             hfmm_gpu** out);
 void hfmm_gpu_destroy(hfmm_gpu* g);

@@ -15,7 +15,9 @@
 #include "setup.hpp"
 
 struct hfmm_setup {
-  hfmm_b200::Setup s;
+  // shared with every engine created from it (hfmm_gpu_create)
+  std::shared_ptr<hfmm_b200::Setup> sp = std::make_shared<hfmm_b200::Setup>();
+  hfmm_b200::Setup& s = *sp;
 };
 struct hfmm_gpu {
   std::unique_ptr<hfmm_b200::Engine> eng;
@@ -120,7 +122,7 @@ hfmm_status hfmm_gpu_create(const hfmm_setup* s, int device, int rank, hfmm_gpu*
     need(s, "hfmm_gpu_create(setup)");
     need(out, "hfmm_gpu_create(out)");
     auto g = std::make_unique<hfmm_gpu>();
-    g->eng = std::make_unique<hfmm_b200::Engine>(s->s, device, rank);
+    g->eng = std::make_unique<hfmm_b200::Engine>(s->sp, device, rank);
     *out = g.release();
   });
 }
@@ -278,7 +280,7 @@ hfmm_status hfmm_evaluate_potential(const double* positions, const double* charg
     need(pot_out, "hfmm_evaluate_potential(pot_out)");
     if (cfg->num_ranks != 1)
       throw std::invalid_argument("hfmm_evaluate_potential: one device evaluates num_ranks == 1");
-    hfmm_b200::Setup s = hfmm_b200::build_setup(positions, charges, n, *cfg);
+    auto s = std::make_shared<hfmm_b200::Setup>(hfmm_b200::build_setup(positions, charges, n, *cfg));
     hfmm_b200::Engine e(s, device, 0);
     e.evaluate_host(nullptr, pot_out, nullptr);
   });

@@ -15,8 +15,6 @@
 #include "leaf.cuh"
 #include "m2l_tc.cuh"
 #include "interp_rb.cuh"
-#include "interp_tc.cuh"
-#include "interp_ct.cuh"
 #include "interp_big.cuh"
 
 namespace hfmm_b200 {
@@ -56,7 +54,9 @@ T* Engine::upload_vec(const std::vector<T>& v) {
   return d;
 }
 
-Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank_(rank) {
+Engine::Engine(std::shared_ptr<const Setup> sp, int device, int rank)
+    : keep_(std::move(sp)), s_(*keep_), dev_(device), rank_(rank) {
+  const Setup& s = s_;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
@@ -65,12 +65,11 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   dist_ = s.P > 1;
   ck(cudaSetDevice(device), "cudaSetDevice");
   ck(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
-  use_ct_ = std::getenv("HFMM_NO_CT") == nullptr;
-  use_rb_ = std::getenv("HFMM_NO_RB") == nullptr;  // debugging aid: compile-time fused kernels instead  // debugging aid: runtime-shaped kernels only
-  // debugging aid: large-level path 0 = two-stage (default), 1 = fused runtime, 2 = legacy two-pass
-  if (const char* p = std::getenv("HFMM_BIG_PATH")) path_ = std::atoi(p);
-  l2l_ct_ = std::getenv("HFMM_L2L_BIG") == nullptr;  // debugging aid: two-stage L2L everywhere
-  if (const char* p = std::getenv("HFMM_BIG_THREADS")) big_threads_ = std::atoi(p);
+  // Test hooks (tests/test_gpu_paths.py): route every level pair through the
+  // general kernels that otherwise serve only the largest grids or leaves.
+  hook_no_rb_ = std::getenv("HFMM_NO_RB") != nullptr;    // no compile-time-shaped M2M/L2L pairs
+  hook_no_rbl_ = std::getenv("HFMM_NO_RBL") != nullptr;  // no runtime-shaped streaming M2M/L2L
+  hook_no_quad_ = std::getenv("HFMM_NO_QUAD") != nullptr;  // generic C2M / L2T instead of quad kernels
   ck(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
   for (auto& e : ev_) ck(cudaEventCreate(&e), "event");
   // Side stream for the near field.  (Giving the far-field chain a higher
@@ -84,7 +83,6 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
     for (cudaEvent_t* e : {&ev_ofork_, &ev_ojoin_, &ev_c2m_, &ev_m2l_leaf_})
       ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     for (cudaEvent_t* e : {&ev_lf0_, &ev_lf1_, &ev_la_, &ev_lb_}) ck(cudaEventCreate(e), "event");
-    overlap_ = std::getenv("HFMM_NO_OVERLAP") == nullptr;  // debugging aid: strictly sequential phases
   }
   ck(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
@@ -92,6 +90,7 @@ Engine::Engine(const Setup& s, int device, int rank) : s_(s), dev_(device), rank
   ck(cudaEventCreate(&ev_near1_), "event");
   ck(cudaStreamCreateWithFlags(&st_cp_, cudaStreamNonBlocking), "copy stream");
   ck(cudaEventCreateWithFlags(&ev_q_, cudaEventDisableTiming), "event");
+  ck(cudaEventCreateWithFlags(&ev_cp_order_, cudaEventDisableTiming), "event");
   upload();
   if (dist_) upload_rank_plan();
   ck(cudaStreamSynchronize(st_), "upload sync");
@@ -109,6 +108,7 @@ Engine::~Engine() {
   for (cudaStream_t s : {st_hi_, st_lo_, st_cp_})
     if (s) cudaStreamDestroy(s);
   if (ev_q_) cudaEventDestroy(ev_q_);
+  if (ev_cp_order_) cudaEventDestroy(ev_cp_order_);
   for (cudaEvent_t e : {ev_ofork_, ev_ojoin_, ev_c2m_, ev_m2l_leaf_, ev_lf0_, ev_lf1_, ev_la_, ev_lb_})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {ev_fork_, ev_join_, ev_near0_, ev_near1_})
@@ -126,9 +126,9 @@ void set_dims(int* d, int K, int N, bool with_ldo) {
 PassDims to_dims(const int* d) { return PassDims{d[0], d[1], d[2], d[3]}; }
 }  // namespace
 
-// Real + rank-1 matrices for the fused tensor-core M2M / L2L of parent level P
-// over child level C, and the shared-memory plan (children per batch).
-void Engine::setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, const LevelData& tc) {
+// Real + rank-1 matrices of the DMMA M2M / L2L passes of parent level P over
+// child level C, and the launch plan of the two-stage large-grid kernels.
+void Engine::setup_interp(DevLevel& P, const DevLevel& C, const LevelData& tp, const LevelData& tc) {
   const int nc = C.nt, np = P.nt, half = np / 2;
   // M2M: phi n_c -> n_p (shift 0), theta 2 n_c -> 2 n_p (shift 0.5)
   RealRank1 uphi = real_rank1(nc, 0.0, np, 0.0);
@@ -152,32 +152,6 @@ void Engine::setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, co
   P.dn_th_v = upload_vec(dth.v);
   P.dn_phi_B = upload_vec(dphi.B);
   P.dn_phi_v = upload_vec(dphi.v);
-  // Shared-memory plans: children per batch CB and buffering; prefer two
-  // CTAs per SM, else one.  HFMM_FUSED_CB caps CB, HFMM_NO_FUSED disables
-  // the fused path (debugging aids).
-  const char* force_cb = std::getenv("HFMM_FUSED_CB");
-  const int max_cb = force_cb ? std::atoi(force_cb) : 4;
-  const bool allow = std::getenv("HFMM_NO_FUSED") == nullptr;
-  const std::pair<int, int> order[] = {{4, 1}, {2, 1}, {4, 0}, {2, 0}, {1, 1}, {1, 0}};
-  auto m2m_bytes = [&](int cb, int db) {
-    return (size_t(db ? 2 : 1) * cb * nc * P.up_phi[2] + size_t(cb) * half * P.up_th[2] + size_t(P.S)) *
-           sizeof(double2);
-  };
-  auto l2l_bytes = [&](int cb, int db) {
-    return (size_t(db ? P.S : 0) + size_t(cb) * half * P.dn_th[2] + size_t(cb) * nc * P.dn_phi[2]) *
-           sizeof(double2);
-  };
-  for (size_t budget : {size_t(113 * 1024), size_t(227 * 1024)}) {
-    if (P.m2m_fused || !allow) break;
-    for (auto [cb, db] : order)
-      if (cb <= max_cb && m2m_bytes(cb, db) <= budget) {
-        P.m2m_plan[0] = cb;
-        P.m2m_plan[1] = db;
-        P.m2m_plan[2] = int(m2m_bytes(cb, db));
-        P.m2m_fused = true;
-        break;
-      }
-  }
   // Two-stage large-grid plans.
   {
     const int ldf = P.up_th[2];
@@ -194,17 +168,6 @@ void Engine::setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, co
     P.big_smem[3] = size_t(P.big_rc[1]) * P.dn_phi[2] * sizeof(double2);
     P.big_ldn = P.dn_phi[2];
     tmp_need_ = std::max(tmp_need_, std::max(size_t(C.n_nodes) * half * ldf, size_t(C.n_nodes) * nc * P.big_ldn));
-  }
-  for (size_t budget : {size_t(113 * 1024), size_t(227 * 1024)}) {
-    if (P.l2l_fused || !allow) break;
-    for (auto [cb, db] : order)
-      if (cb <= max_cb && l2l_bytes(cb, db) <= budget) {
-        P.l2l_plan[0] = cb;
-        P.l2l_plan[1] = db;
-        P.l2l_plan[2] = int(l2l_bytes(cb, db));
-        P.l2l_fused = true;
-        break;
-      }
   }
 }
 
@@ -261,13 +224,9 @@ void Engine::upload() {
       n_sparse_ = int(sp.size());
       d_sparse_leaves_ = upload_vec(sp);
     }
-    l2t_noobs_ = std::getenv("HFMM_L2T_NOOBS") != nullptr;
-    near_seq_ = std::getenv("HFMM_NEAR_SEQ") != nullptr;  // near field after L2T even in overlap mode
-    c2m_tab_ = std::getenv("HFMM_C2M_TAB") != nullptr;
-    m2l_seq_ = std::getenv("HFMM_M2L_SEQ") != nullptr;    // leaf M2L inside the chain even in overlap mode
-    tune_ = !m2l_seq_ && std::getenv("HFMM_NO_TUNE") == nullptr;
     // Leaf phase table (sincos_l): |A| <= k side / sqrt 2, |B| <= k side / 2
-    // for particles in their leaf; HFMM_LEAF_POLY keeps the polynomials.
+    // for particles in their leaf; larger leaves (or the HFMM_LEAF_POLY test
+    // hook) use the sincos polynomials.
     {
       const double amax = s.k * s.leaf_side / std::sqrt(2.0);
       const int nh = int(std::ceil(amax * 128.0)) + 2;
@@ -279,8 +238,8 @@ void Engine::upload() {
       }
     }
     // Near-field phase table (green_tab): r' = k r <= k 2 sqrt(3) leaf side
-    // between particles of adjacent leaves; HFMM_P2P_POLY keeps the sincos
-    // polynomials.
+    // between particles of adjacent leaves; larger leaves (or the
+    // HFMM_P2P_POLY test hook) use the sincos polynomials.
     {
       const double rmax = s.k * 2.0 * std::sqrt(3.0) * s.leaf_side;
       const int ntab = int(std::ceil(rmax * 128.0)) + 2;
@@ -291,16 +250,11 @@ void Engine::upload() {
         ptab_max_ = ntab - 1;
       }
     }
-    if (const char* e = std::getenv("HFMM_PHI_CTAS")) phi_ctas_ = std::max(1, std::atoi(e));
     // symmetric pair lists among own dense leaves (k_p2p_sym2 / k_p2p_gather).
     // k_p2p_sym2 runs one CTA per (leaf, pass of 128 observers): each pass
     // writes its own scratch rows (no read-modify-write across CTAs), and
     // the gather adds them in (sender leaf, pass) order, so sums are
-    // deterministic.  HFMM_P2P_V1 selects the previous kernel (one CTA per
-    // leaf, one scratch row per pair) for A/B.
-    use_sym_ = std::getenv("HFMM_P2P_NOSYM") == nullptr;
-    p2p_v1_ = std::getenv("HFMM_P2P_V1") != nullptr;
-    leaf_v1_ = std::getenv("HFMM_LEAF_V1") != nullptr;
+    // deterministic.
     const int obs_pass = 32 * kSymObs;
     auto pop = [&](int64_t lf) { return int64_t(s.leaf_start[size_t(lf) + 1] - s.leaf_start[size_t(lf)]); };
     std::vector<int> pos(s.num_leaves(), -1);
@@ -313,13 +267,13 @@ void Engine::upload() {
     for (size_t i = 0; i < dense.size(); ++i) {
       const int a = dense[i];
       const int64_t na = pop(a);
-      const int npass = p2p_v1_ ? 1 : int((na + obs_pass - 1) / obs_pass);
+      const int npass = int((na + obs_pass - 1) / obs_pass);
       int64_t rows = 0, plain_src = 0;
       const size_t sb = sl.size();
       for (uint64_t z2 = s.near_off[size_t(a)]; z2 < s.near_off[size_t(a) + 1]; ++z2) {
         const int b = int(s.near[z2]);
         // k_p2p_sym2 takes the self leaf as a symmetric entry (pairs o < t once)
-        if ((b > a || (b == a && !p2p_v1_)) && pos[size_t(b)] >= 0) {
+        if (b >= a && pos[size_t(b)] >= 0) {
           sl.push_back(b);
           sscr.push_back(scr + rows);
           rows += pop(b);
@@ -493,27 +447,6 @@ void Engine::upload() {
     const LevelData& tc = s.levels[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
     if (C.np != nc || P.np != np) throw std::logic_error("non-square sampling");
-    auto transpose = [](const std::vector<double>& M, int rows, int cols) {
-      std::vector<double2> T2(size_t(rows) * size_t(cols));
-      for (int r = 0; r < rows; ++r)
-        for (int c = 0; c < cols; ++c)
-          T2[size_t(c) * rows + r] = make_double2(M[size_t(2 * (r * cols + c))], M[size_t(2 * (r * cols + c) + 1)]);
-      return T2;
-    };
-    P.PuT = upload_vec(transpose(resample_matrix(nc, 0.0, np, 0.0), np, nc));
-    P.TuT = upload_vec(transpose(resample_matrix(2 * nc, 0.5, 2 * np, 0.5), 2 * np, 2 * nc));
-    P.PdT = upload_vec(transpose(resample_matrix(np, 0.0, nc, 0.0), nc, np));
-    std::vector<double> Td = resample_matrix(2 * np, 0.5, 2 * nc, 0.5);  // 2nc x 2np
-    const double scale = (double(P.S) / double(C.S)) * tp.phi_w / tc.phi_w;
-    for (int j = 0; j < 2 * nc; ++j)
-      for (int i = 0; i < 2 * np; ++i) {
-        const double wp = tp.theta_w[size_t(i < np ? i : 2 * np - 1 - i)];
-        const double wc = tc.theta_w[size_t(j < nc ? j : 2 * nc - 1 - j)];
-        const double f = scale * wp / wc;
-        Td[size_t(2 * (j * 2 * np + i))] *= f;
-        Td[size_t(2 * (j * 2 * np + i) + 1)] *= f;
-      }
-    P.TdT = upload_vec(transpose(Td, 2 * nc, 2 * np));
     // Shift tables on the parent grid: disp = c_child - c_parent = (b - 1/2) side_c.
     const std::vector<double>& dir = hdir[size_t(l)];
     std::vector<double2> up(size_t(8 * P.S)), dn(size_t(8 * P.S));
@@ -531,7 +464,7 @@ void Engine::upload() {
     }
     P.shift_up = upload_vec(up);
     P.shift_dn = upload_vec(dn);
-    setup_fused(P, C, tp, tc);
+    setup_interp(P, C, tp, tc);
     tmp = std::max(tmp, size_t(C.n_nodes) * size_t(nc) * size_t(np));
     tmp = std::max(tmp, rb_m2m_scratch(C.n_nodes, nc, np));
     tmp = std::max(tmp, rb_l2l_scratch(C.n_nodes, nc, np));
@@ -568,21 +501,20 @@ void Engine::build_T() {
 
 namespace {
 // Quad-symmetric leaf kernels need an even, square grid with n/2 <= kQuadHalfMax.
-bool quad_ok(const DevLevel& d) {
-  return d.nt == d.np && d.nt % 2 == 0 && d.nt / 2 <= kQuadHalfMax && std::getenv("HFMM_NO_QUAD") == nullptr;
+bool quad_ok(const DevLevel& d, bool hook_generic) {
+  return d.nt == d.np && d.nt % 2 == 0 && d.nt / 2 <= kQuadHalfMax && !hook_generic;
 }
 }  // namespace
 
 void Engine::phase_c2m() {
   const DevLevel& d = lv_[size_t(s_.L)];
   const int64_t nl = leaf_e_ - leaf_b_;
-  if (quad_ok(d) && !leaf_v1_) {
+  if (quad_ok(d, hook_no_quad_)) {
     const int quads = int(d.nt / 2) * int(d.nt / 2);
     // quads per lane: fewest lane slots (passes x R), ties to fewer passes; R <= 4
     // keeps 4 CTAs/SM (R = 6 needs 208 registers and measured slower at config 2)
-    const int rmax = std::getenv("HFMM_C2M_RMAX") ? std::atoi(std::getenv("HFMM_C2M_RMAX")) : 4;
     int r = 1, best = INT32_MAX;
-    for (int rr = 1; rr <= std::min(std::max(rmax, 1), 6); ++rr) {
+    for (int rr = 1; rr <= 4; ++rr) {
       const int cost = (quads + 32 * rr - 1) / (32 * rr) * rr;
       if (cost <= best) {
         best = cost;
@@ -590,15 +522,9 @@ void Engine::phase_c2m() {
       }
     }
     const unsigned g = unsigned((nl + 3) / 4);
-#define HFMM_C2M(RR, HN)                                                                                       \
-  do {                                                                                                          \
-    if (d_ltab_ && c2m_tab_)                                                                                   \
-      k_c2m_quad2<RR, HN, true><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,     \
-                                                    d.dir, d.nt, s_.k, d.mp, d_ltab_, ltab_half_);              \
-    else                                                                                                        \
-      k_c2m_quad2<RR, HN, false><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,    \
-                                                     d.dir, d.nt, s_.k, d.mp);                                  \
-  } while (0)
+#define HFMM_C2M(RR, HN)                                                                                    \
+  k_c2m_quad2<RR, HN><<<g, 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.nt, \
+                                          s_.k, d.mp)
     const int hn = int(d.nt / 2);
     if (r == 3 && hn == 9) HFMM_C2M(3, 9);        // n = 18 (configs 1, 3, 4)
     else if (r == 4 && hn == 11) HFMM_C2M(4, 11);  // n = 22 (config 5)
@@ -608,27 +534,15 @@ void Engine::phase_c2m() {
         case 1: HFMM_C2M(1, 0); break;
         case 2: HFMM_C2M(2, 0); break;
         case 3: HFMM_C2M(3, 0); break;
-        case 4: HFMM_C2M(4, 0); break;
-        case 5: HFMM_C2M(5, 0); break;
-        default: HFMM_C2M(6, 0); break;
+        default: HFMM_C2M(4, 0); break;
       }
 #undef HFMM_C2M
-  } else if (quad_ok(d))
-    k_c2m_quad<<<unsigned((nl + 3) / 4), 128, 0, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d_q, d.centers,
-                                                         d.dir, d.nt, s_.k, d.mp);
-  else
+  } else  // leaf grids past kQuadHalfMax: generic kernel
     k_c2m<<<unsigned(nl), 128, 0, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d_q, d.centers, d.dir, d.S, s_.k,
                                          d.mp);
   ++launches_;
   ck(cudaGetLastError(), "k_c2m");
 }
-
-namespace {
-int theta_chunk(int half, int outs_per_circle, int threads) {
-  int cp = std::max(1, (kThetaE * threads) / outs_per_circle);
-  return std::min(cp, half);
-}
-}  // namespace
 
 namespace {
 // Runtime-shaped streaming kernels: any even grid pair (the host B layouts
@@ -638,7 +552,7 @@ bool rbl_ok(int nc, int np) {
   const int lim = 227 * 1024;
   const bool fits = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8 <= lim && rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8 <= lim &&
                     rb::r4(2 * np + 1) * rb::blk_ldb(8 * rb::kChunk) * 8 <= lim;
-  return nc % 2 == 0 && np % 2 == 0 && fits && std::getenv("HFMM_NO_RBL") == nullptr;
+  return nc % 2 == 0 && np % 2 == 0 && fits;
 }
 }  // namespace
 
@@ -651,94 +565,57 @@ void Engine::phase_m2m() {
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
     const RankLevel* R = dist_ ? &rl_[size_t(l)] : nullptr;
-    const CtLaunch cl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
-                      R ? R->children : P.children, oct_[size_t(l + 1)], st_};
-    if (cl.n_par == 0) continue;
-    if (use_rb_ && rb_pair(nc, np)) {
-      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
-      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_, phi_ctas_ * sms_};
-      if (launch_m2m_rb(nc, np, rl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up, d_tmp)) {
-        launches_ += 2;
-        ck(cudaGetLastError(), "k_m2m_rb");
-        continue;
-      }
+    const RbLaunch rl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
+                      R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
+                      oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
+    if (rl.n_par == 0) continue;
+    // 1. compile-time-shaped streaming pairs (the BASELINE leaf-side pairs)
+    if (!hook_no_rb_ && rb_pair(nc, np) &&
+        launch_m2m_rb(nc, np, rl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up, d_tmp)) {
+      launches_ += 2;
+      ck(cudaGetLastError(), "k_m2m_rb");
+      continue;
     }
-    if (use_rb_ && rbl_ok(nc, np)) {  // larger pairs: runtime-shaped streaming kernels
-      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+    // 2. runtime-shaped streaming kernels (B matrices fit shared memory)
+    if (!hook_no_rbl_ && rbl_ok(nc, np)) {
       const int s_phi = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8;
       const int nchunk = (rb::r8(2 * np) / 8 + rb::kChunkM2M - 1) / rb::kChunkM2M;
       const int s_th = rb::r4(2 * nc + 1) * rb::blk_ldb(8 * rb::kChunkM2M) * 8;
       ck(cudaFuncSetAttribute(k_m2m_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
       ck(cudaFuncSetAttribute(k_m2m_theta_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_th), "attr");
-      if (nch > 0)
-        k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, nch, cl.children, C.mp, P.up_phi_B, P.up_phi_v,
+      if (rl.nch > 0)
+        k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, C.mp, P.up_phi_B, P.up_phi_v,
                                                               d_tmp);
       const dim3 gth(unsigned(std::max(1, 2 * sms_ / nchunk)), unsigned(nchunk));
-      k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, cl.n_par, cl.plist, cl.child_off, cl.children,
-                                                        cl.oct_c, d_tmp, P.up_th_B, P.up_th_v, P.shift_up, P.mp);
+      k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, rl.n_par, rl.plist, rl.child_off, rl.children,
+                                                        rl.oct_c, d_tmp, P.up_th_B, P.up_th_v, P.shift_up, P.mp);
       launches_ += 2;
       ck(cudaGetLastError(), "k_m2m_rbl");
       continue;
     }
-    if (use_ct_ && launch_m2m_ct(nc, np, cl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v,
-                                 P.shift_up)) {
+    // 3. two-stage large-grid kernels (any grid; B streams from L2)
+    const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
+    const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
+    ck(cudaFuncSetAttribute(k_m2m_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[0])), "attr");
+    ck(cudaFuncSetAttribute(k_m2m_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[1])), "attr");
+    if (ncl > 0) {
+      dim3 g0(unsigned(ncl), unsigned((nc + P.big_rc[0] - 1) / P.big_rc[0]));
+      k_m2m_big_phi<<<g0, kBigThreads, P.big_smem[0], st_>>>(nc, np, to_dims(P.up_phi), P.up_th[2], P.big_rc[0], clist,
+                                                             C.mp, P.up_phi_B, P.up_phi_v, d_tmp);
       ++launches_;
-      ck(cudaGetLastError(), "k_m2m_ct");
-      continue;
     }
-    if (path_ == 0) {  // two-stage large-grid kernels
-      const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
-      const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
-      ck(cudaFuncSetAttribute(k_m2m_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[0])), "attr");
-      ck(cudaFuncSetAttribute(k_m2m_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[1])), "attr");
-      if (ncl > 0) {
-        dim3 g0(unsigned(ncl), unsigned((nc + P.big_rc[0] - 1) / P.big_rc[0]));
-        k_m2m_big_phi<<<g0, big_threads_, P.big_smem[0], st_>>>(nc, np, to_dims(P.up_phi), P.up_th[2], P.big_rc[0], clist, C.mp,
-                                                                 P.up_phi_B, P.up_phi_v, d_tmp);
-        ++launches_;
-      }
-      dim3 grid(unsigned(cl.n_par), unsigned((np / 2 + P.big_m2m_cp - 1) / P.big_m2m_cp));
-      k_m2m_big_theta<<<grid, big_threads_, P.big_smem[1], st_>>>(nc, np, P.big_m2m_cp, to_dims(P.up_th), cl.plist, cl.child_off,
-                                                         cl.children, oct_[size_t(l + 1)], d_tmp, P.up_th_B,
-                                                         P.up_th_v, P.shift_up, P.mp);
-      ++launches_;
-      ck(cudaGetLastError(), "m2m big");
-      continue;
-    }
-    if (P.m2m_fused && path_ == 1) {
-      const FusedPlan fp{P.m2m_plan[0], P.m2m_plan[1], P.m2m_plan[2]};
-      ck(cudaFuncSetAttribute(k_m2m_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
-      k_m2m_fused<<<unsigned(cl.n_par), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
-          nc, np, fp, cl.plist, to_dims(P.up_phi), to_dims(P.up_th), cl.child_off, cl.children, oct_[size_t(l + 1)],
-          C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up);
-      ++launches_;
-      ck(cudaGetLastError(), "k_m2m_fused");
-      continue;
-    }
-    const size_t smem0 = size_t(nc) * nc * sizeof(double2);
-    if (smem0 > 48 * 1024)
-      ck(cudaFuncSetAttribute(k_m2m_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem0)), "attr");
-    k_m2m_phi<<<unsigned(C.n_nodes), 256, size_t(nc) * nc * sizeof(double2), st_>>>(nc, np, 0, C.mp, P.PuT,
-                                                                                   d_tmp);
+    dim3 grid(unsigned(rl.n_par), unsigned((np / 2 + P.big_m2m_cp - 1) / P.big_m2m_cp));
+    k_m2m_big_theta<<<grid, kBigThreads, P.big_smem[1], st_>>>(nc, np, P.big_m2m_cp, to_dims(P.up_th), rl.plist,
+                                                               rl.child_off, rl.children, rl.oct_c, d_tmp, P.up_th_B,
+                                                               P.up_th_v, P.shift_up, P.mp);
     ++launches_;
-    const int half = np / 2;
-    const int CP = theta_chunk(half, 2 * np, 256);
-    dim3 grid(unsigned(P.n_nodes), unsigned((half + CP - 1) / CP));
-    const size_t smem = size_t(CP) * 2 * nc * sizeof(double2);
-    if (smem > 48 * 1024)
-      ck(cudaFuncSetAttribute(k_m2m_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-    k_m2m_theta<<<grid, 256, smem, st_>>>(nc, np, CP, 0, 0, P.child_off, P.children, oct_[size_t(l + 1)], d_tmp,
-                                          P.TuT, P.shift_up, P.mp);
-    ++launches_;
-    ck(cudaGetLastError(), "m2m");
+    ck(cudaGetLastError(), "m2m big");
   }
 }
 
 void Engine::phase_m2l(int lo, int hi) {
   if (lo < 0) lo = s_.top;
   if (hi < 0) hi = s_.L;
-  const bool dmma = std::getenv("HFMM_M2L_DFMA") == nullptr;  // debugging aid: the DFMA stencil
-  ck(cudaFuncSetAttribute(k_m2l_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
   ck(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
   for (int l = lo; l <= hi; ++l) {
     DevLevel& d = lv_[size_t(l)];
@@ -746,15 +623,12 @@ void Engine::phase_m2l(int lo, int hi) {
     // exchange completed exactly their far sources)
     if (d.dense) {
       const int nb = (d.G + m2l::MB - 1) / m2l::MB;
-      const int nblk = dist_ && dmma ? d.m2l_nblk : nb * nb * nb;
+      const int nblk = dist_ ? d.m2l_nblk : nb * nb * nb;
       if (nblk == 0) continue;
       const int ppc = m2l_pairs_per_cta(nblk, d.S, sms_);
       dim3 grid(unsigned(nblk), unsigned((d.S / 2 + ppc - 1) / ppc));
-      if (dmma)
-        k_m2l_dmma<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, dist_ ? d.m2l_blk : nullptr, d.lookup,
-                                                        d.T, d.mp, d.loc);
-      else
-        k_m2l_dense<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, d.lookup, d.T, d.mp, d.loc);
+      k_m2l_dmma<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, dist_ ? d.m2l_blk : nullptr, d.lookup, d.T,
+                                                      d.mp, d.loc);
     } else {
       const int nobs = dist_ ? held_cnt_[size_t(l)] : int(d.n_nodes);
       if (nobs == 0) continue;
@@ -774,94 +648,55 @@ void Engine::phase_l2l(int lo, int hi) {
     DevLevel& C = lv_[size_t(l + 1)];
     const int nc = C.nt, np = P.nt;
     const RankLevel* R = dist_ ? &rl_[size_t(l)] : nullptr;
-    const CtLaunch cl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
-                      R ? R->children : P.children, oct_[size_t(l + 1)], st_};
-    if (cl.n_par == 0) continue;
-    if (use_rb_ && rb_pair(nc, np)) {
-      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
-      const RbLaunch rl{cl.n_par, cl.plist, cl.child_off, cl.children, nch, cl.oct_c, 2 * sms_, st_, phi_ctas_ * sms_};
-      if (launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn, d_tmp)) {
-        launches_ += 2;
-        ck(cudaGetLastError(), "k_l2l_rb");
-        continue;
-      }
+    const RbLaunch rl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
+                      R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
+                      oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
+    if (rl.n_par == 0) continue;
+    // 1. compile-time-shaped streaming pairs
+    if (!hook_no_rb_ && rb_pair(nc, np) &&
+        launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn, d_tmp)) {
+      launches_ += 2;
+      ck(cudaGetLastError(), "k_l2l_rb");
+      continue;
     }
-    if (use_rb_ && rbl_ok(nc, np)) {
-      const int64_t nch = dist_ ? R->n_children : int64_t(C.n_nodes);
+    // 2. runtime-shaped streaming kernels
+    if (!hook_no_rbl_ && rbl_ok(nc, np)) {
       const int s_phi = rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8;
       ck(cudaFuncSetAttribute(k_l2l_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
-      k_l2l_theta_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, cl.n_par, cl.plist, cl.child_off, cl.children,
-                                                          cl.oct_c, P.loc, P.dn_th_B, P.dn_th_v, P.shift_dn, d_tmp);
-      if (nch > 0)
-        k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, nch, cl.children, d_tmp, P.dn_phi_B, P.dn_phi_v,
+      k_l2l_theta_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, rl.n_par, rl.plist, rl.child_off, rl.children,
+                                                          rl.oct_c, P.loc, P.dn_th_B, P.dn_th_v, P.shift_dn, d_tmp);
+      if (rl.nch > 0)
+        k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, d_tmp, P.dn_phi_B, P.dn_phi_v,
                                                               C.loc);
       launches_ += 2;
       ck(cudaGetLastError(), "k_l2l_rbl");
       continue;
     }
-    if (use_ct_ && l2l_ct_ && launch_l2l_ct(nc, np, cl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v,
-                                 P.shift_dn)) {
-      ++launches_;
-      ck(cudaGetLastError(), "k_l2l_ct");
-      continue;
-    }
-    if (path_ == 0) {  // two-stage large-grid kernels
-      const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
-      const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
-      if (ncl == 0) continue;
-      ck(cudaFuncSetAttribute(k_l2l_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[2])), "attr");
-      ck(cudaFuncSetAttribute(k_l2l_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[3])), "attr");
-      dim3 grid(unsigned(ncl), unsigned((np / 2 + P.big_l2l_cp - 1) / P.big_l2l_cp));
-      k_l2l_big_theta<<<grid, big_threads_, P.big_smem[2], st_>>>(nc, np, P.big_l2l_cp, to_dims(P.dn_th), P.big_ldn, clist,
-                                                         C.parent, oct_[size_t(l + 1)], P.loc, P.shift_dn, P.dn_th_B,
-                                                         P.dn_th_v, d_tmp);
-      ++launches_;
-      dim3 g3(unsigned(ncl), unsigned((nc + P.big_rc[1] - 1) / P.big_rc[1]));
-      k_l2l_big_phi<<<g3, big_threads_, P.big_smem[3], st_>>>(nc, np, to_dims(P.dn_phi), P.big_ldn, P.big_rc[1], clist, d_tmp,
-                                                               P.dn_phi_B, P.dn_phi_v, C.loc);
-      ++launches_;
-      ck(cudaGetLastError(), "l2l big");
-      continue;
-    }
-    if (P.l2l_fused && path_ == 1) {
-      const FusedPlan fp{P.l2l_plan[0], P.l2l_plan[1], P.l2l_plan[2]};
-      ck(cudaFuncSetAttribute(k_l2l_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, fp.smem_bytes), "attr");
-      k_l2l_fused<<<unsigned(cl.n_par), kFusedThreads, size_t(fp.smem_bytes), st_>>>(
-          nc, np, fp, cl.plist, to_dims(P.dn_th), to_dims(P.dn_phi), cl.child_off, cl.children, oct_[size_t(l + 1)],
-          P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn);
-      ++launches_;
-      ck(cudaGetLastError(), "k_l2l_fused");
-      continue;
-    }
-    const int half = np / 2;
-    const int CP = theta_chunk(half, 2 * nc, 256);
-    dim3 grid(unsigned(C.n_nodes), unsigned((half + CP - 1) / CP));
-    const size_t smem = size_t(CP) * 2 * np * sizeof(double2);
-    if (smem > 48 * 1024)
-      ck(cudaFuncSetAttribute(k_l2l_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-    k_l2l_theta<<<grid, 256, smem, st_>>>(nc, np, CP, 0, C.parent, oct_[size_t(l + 1)], P.loc, P.shift_dn, P.TdT,
-                                          d_tmp);
+    // 3. two-stage large-grid kernels
+    const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
+    const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
+    if (ncl == 0) continue;
+    ck(cudaFuncSetAttribute(k_l2l_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[2])), "attr");
+    ck(cudaFuncSetAttribute(k_l2l_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[3])), "attr");
+    dim3 grid(unsigned(ncl), unsigned((np / 2 + P.big_l2l_cp - 1) / P.big_l2l_cp));
+    k_l2l_big_theta<<<grid, kBigThreads, P.big_smem[2], st_>>>(nc, np, P.big_l2l_cp, to_dims(P.dn_th), P.big_ldn, clist,
+                                                               C.parent, rl.oct_c, P.loc, P.shift_dn, P.dn_th_B,
+                                                               P.dn_th_v, d_tmp);
     ++launches_;
-    const size_t smem2 = size_t(nc) * np * sizeof(double2);
-    if (smem2 > 48 * 1024)
-      ck(cudaFuncSetAttribute(k_l2l_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)), "attr");
-    k_l2l_phi<<<unsigned(C.n_nodes), 256, smem2, st_>>>(nc, np, 0, d_tmp, P.PdT, C.loc);
+    dim3 g3(unsigned(ncl), unsigned((nc + P.big_rc[1] - 1) / P.big_rc[1]));
+    k_l2l_big_phi<<<g3, kBigThreads, P.big_smem[3], st_>>>(nc, np, to_dims(P.dn_phi), P.big_ldn, P.big_rc[1], clist,
+                                                           d_tmp, P.dn_phi_B, P.dn_phi_v, C.loc);
     ++launches_;
-    ck(cudaGetLastError(), "l2l");
+    ck(cudaGetLastError(), "l2l big");
   }
 }
 
 void Engine::phase_l2t() {
   const DevLevel& d = lv_[size_t(s_.L)];
   const int64_t nl = leaf_e_ - leaf_b_;
-  if (quad_ok(d)) {
+  if (quad_ok(d, hook_no_quad_)) {
     const size_t smem = 4 * size_t(kQuadP * (d.nt / 2)) * sizeof(double2);
-    if (smem > 48 * 1024)
-      ck(cudaFuncSetAttribute(k_l2t_quad, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-    if (leaf_v1_) {
-      k_l2t_quad<<<unsigned((nl + 3) / 4), 128, smem, st_>>>(leaf_b_, nl, d_leaf_start, d_x, d_y, d_z, d.centers,
-                                                              d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);
-    } else {
+    {
       // (n / 2 <= kQuadHalfMax keeps the table under 48 KB: no attribute needed)
       auto l2t_quads = [&](unsigned grid, int64_t lb, int64_t cnt, const int* list) {
         const int hn = int(d.nt / 2);
@@ -880,7 +715,7 @@ void Engine::phase_l2t() {
         else HFMM_L2TQ(0);
 #undef HFMM_L2TQ
       };
-      if (n_dense_ > 0 && !l2t_noobs_) {  // populous leaves: lane per observer, the rest: lanes over quads
+      if (n_dense_ > 0) {  // populous leaves: lane per observer, the rest: lanes over quads
         const int quads = int(d.nt / 2) * int(d.nt / 2);
         const size_t so = 4 * size_t(quads) * 5 * sizeof(double2);
         const int hn = int(d.nt / 2);
@@ -909,7 +744,7 @@ void Engine::phase_l2t() {
         l2t_quads(unsigned((nl + 3) / 4), leaf_b_, nl, nullptr);
       }
     }
-  } else {
+  } else {  // leaf grids past kQuadHalfMax: generic kernel
     const size_t smem = size_t(d.S) * (sizeof(double2) + 3 * sizeof(double));
     if (smem > 48 * 1024)
       ck(cudaFuncSetAttribute(k_l2t, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
@@ -950,13 +785,8 @@ void Engine::near_start() {
                                                          d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near);
     ++launches_;
   }
-  if (n_dense_ > 0 && use_sym_) {
-    if (p2p_v1_)
-      k_p2p_sym<<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_plain_off_, d_plain_,
-                                                      d_sym_off_, d_sym_, d_sym_scr_, d.centers, d_x, d_y, d_z, d_q,
-                                                      s_.k, d_pot_near, d_p2p_scratch_);
-    else
-      for (int c = 3; c >= 0; --c) {
+  if (n_dense_ > 0) {
+    for (int c = 3; c >= 0; --c) {
         if (p2p_items_n_[c] == 0) continue;
         const int2* itm = d_p2p_items_ + p2p_items_b_[c];
         const unsigned g = unsigned(p2p_items_n_[c]);
@@ -976,10 +806,6 @@ void Engine::near_start() {
       }
     k_p2p_gather<<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_in_off_, d_in_scr_,
                                                        d_p2p_scratch_, d_pot_near);
-    launches_ += 2;
-  } else if (n_dense_ > 0) {
-    k_p2p<true><<<unsigned(n_dense_), 128, 0, st2_>>>(d_dense_leaves_, d_leaf_start, d_near_off, d_near, d.centers,
-                                                      d_x, d_y, d_z, d_q, s_.k, d_pot_near);
     ++launches_;
   }
   ck(cudaGetLastError(), "k_p2p");
@@ -1075,7 +901,7 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
   // helps configs 2 and 3 and costs configs 4 and 5 (measured); evaluation 1
   // runs it beside the chain, evaluation 2 inside it, and from evaluation 3
   // on the faster of the two (each timed by its own ev_[0] -> ev_[7]).
-  if (overlap_ && tune_ && !tune_done_) {
+  if (overlap_ && !tune_done_) {
     if (tune_evals_ == 2 || tune_evals_ == 3) {
       float f = 0.f;
       ck(cudaEventSynchronize(ev_[7]), "tune sync");
@@ -1115,7 +941,7 @@ void Engine::evaluate_device(const double* d_q_sorted, double* d_pot_sorted, cud
   }
   // Near field: side stream, overlapped with the far-field chain; in the
   // sequential mode (set_overlap off) it runs after L2T, inside phase_near.
-  if (overlap_ && !near_seq_) near_start();
+  if (overlap_) near_start();
   if (!t_first) build_T();
   cudaEventRecord(ev_[1], st_);
   phase_c2m();
@@ -1173,6 +999,10 @@ void Engine::evaluate_host(const double* q_in, double* pot_out, double* ms) {
     // charges H2D + Morton gather on the copy stream; evaluate_device builds
     // T meanwhile and joins before the first phase that reads them
     const int64_t n = int64_t(s_.n);
+    // d_q_in / d_q may still be in use by work already queued on st_ (and,
+    // through st_'s joins, on the side streams): order the copy after it.
+    ck(cudaEventRecord(ev_cp_order_, st_), "cp order");
+    ck(cudaStreamWaitEvent(st_cp_, ev_cp_order_, 0), "cp order wait");
     ck(cudaMemcpyAsync(d_q_in, q_in, size_t(n) * sizeof(double2), cudaMemcpyHostToDevice, st_cp_), "H2D q");
     k_gather_q<<<unsigned((n + 255) / 256), 256, 0, st_cp_>>>(n, d_orig, d_q_in, d_q);
     ++launches_;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "setup.hpp"
@@ -40,20 +41,13 @@ struct DevLevel {
   int* children = nullptr;
   int* parent = nullptr;      // n_nodes, parent index at level-1 (or -1)
   // As a parent level of level+1:
-  double2* PuT = nullptr;  // phi upsample, transposed [n_c][n_p]
-  double2* TuT = nullptr;  // theta upsample (folded), transposed [2n_c][2n_p]
-  double2* PdT = nullptr;  // phi downsample, transposed [n_p][n_c]
-  double2* TdT = nullptr;  // theta downsample with weights folded, transposed [2n_p][2n_c]
   double2* shift_up = nullptr;  // 8*S: exp(+i k khat.(c_child - c_parent)) on this grid
   double2* shift_dn = nullptr;  // 8*S: exp(+i k khat.(c_parent - c_child))
-  // Fused tensor-core M2M / L2L (interp_tc.cuh): real matrices + rank-1 vectors.
-  bool m2m_fused = false, l2l_fused = false;
-  // Two-stage large-grid kernels (interp_big.cuh): circles per CTA and smem bytes.
+  // DMMA M2M / L2L (dmma.cuh): real matrices + rank-1 vectors.  Two-stage large-grid kernels (interp_big.cuh): circles per CTA and smem bytes.
   int big_m2m_cp = 1, big_l2l_cp = 1;
   size_t big_smem[4] = {0, 0, 0, 0};  // m2m phi, m2m theta, l2l theta, l2l phi
   int big_ldn = 0;                    // narrow-row stride of the L2L temp
   int big_rc[2] = {1, 1};             // rows per CTA: m2m phi, l2l phi
-  int m2m_plan[3] = {1, 0, 0}, l2l_plan[3] = {1, 0, 0};  // FusedPlan {CB, dbuf, smem bytes}
   int up_phi[4] = {0, 0, 0, 0}, up_th[4] = {0, 0, 0, 0};  // PassDims {K, N, lda, ldo}
   int dn_th[4] = {0, 0, 0, 0}, dn_phi[4] = {0, 0, 0, 0};
   double* up_phi_B = nullptr;
@@ -89,7 +83,9 @@ struct PeerPlan {
 
 class Engine {
  public:
-  Engine(const Setup& s, int device, int rank);
+  // The engine shares ownership of the setup, so a C caller may destroy its
+  // hfmm_setup handle before the engine (include/hfmm_gpu.h).
+  Engine(std::shared_ptr<const Setup> s, int device, int rank);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -126,7 +122,7 @@ class Engine {
 
  private:
   void upload();
-  void setup_fused(DevLevel& P, const DevLevel& C, const LevelData& tp, const LevelData& tc);
+  void setup_interp(DevLevel& P, const DevLevel& C, const LevelData& tp, const LevelData& tc);
   void build_T();
   void phase_c2m();
   void phase_m2m();
@@ -139,6 +135,7 @@ class Engine {
   template <class T>
   T* upload_vec(const std::vector<T>& v);
 
+  std::shared_ptr<const Setup> keep_;
   const Setup& s_;
   int dev_ = 0, rank_ = 0;
   int sms_ = 148;  // multiprocessors of dev_
@@ -148,11 +145,10 @@ class Engine {
   std::vector<uint8_t*> oct_;  // per level: child octant (code & 7) of each node
   std::vector<void*> allocs_;
   int64_t launches_ = 0;
-  bool use_ct_ = true;
-  bool l2l_ct_ = true;
-  bool use_rb_ = true;
-  int big_threads_ = 256;  // block size of the two-stage large-grid kernels
-  int path_ = 0;           // large-level M2M/L2L path (see constructor)
+  // test hooks (HFMM_NO_RB, HFMM_NO_RBL, HFMM_NO_QUAD; tests/test_gpu_paths.py)
+  bool hook_no_rb_ = false, hook_no_rbl_ = false, hook_no_quad_ = false;
+  static constexpr int kBigThreads = 256;  // block size of the two-stage large-grid kernels
+  static constexpr int kPhiCtas = 2;       // persistent CTAs per SM of the streaming phi passes
   size_t tmp_need_ = 0;    // temp elements required by the large-level kernels
   // particles (sorted)
   double* d_x = nullptr;
@@ -178,25 +174,19 @@ class Engine {
   int* d_in_off_ = nullptr;
   int64_t* d_in_scr_ = nullptr;
   double2* d_p2p_scratch_ = nullptr;
-  bool use_sym_ = true;
   int2* d_p2p_items_ = nullptr;  // k_p2p_sym2 work items {dense leaf idx, pass}, grouped by slots per lane
   int64_t* d_sym_rows_ = nullptr;
   int p2p_items_b_[4] = {0, 0, 0, 0}, p2p_items_n_[4] = {0, 0, 0, 0};
-  bool p2p_v1_ = false;
-  bool leaf_v1_ = false;
   int* d_sparse_leaves_ = nullptr;  // own leaves with <= 32 particles (L2T)
   int n_sparse_ = 0;
-  bool l2t_noobs_ = false;
-  int phi_ctas_ = 2;
-  bool near_seq_ = false, m2l_seq_ = false;  // schedule knobs (HFMM_NEAR_SEQ, HFMM_M2L_SEQ)
-  bool tune_ = true, tune_done_ = false;     // leaf-M2L placement autotune (evaluate_device)
+  bool m2l_seq_ = false;                     // leaf M2L inside the chain (autotuned choice)
+  bool tune_done_ = false;                   // leaf-M2L placement autotune (evaluate_device)
   int tune_evals_ = 0;
   float tune_ms_[2] = {0.f, 0.f};
   double2* d_ptab_ = nullptr;  // near-field phase table (green_tab), nullptr: sincos polynomials
   int ptab_max_ = 0;
   double2* d_ltab_ = nullptr;  // leaf phase table (sincos_l), centred; nullptr: polynomials
   int ltab_half_ = 0;
-  bool c2m_tab_ = false;  // C2M on the leaf phase table (HFMM_C2M_TAB)  // persistent CTAs per SM of the streaming phi passes (HFMM_PHI_CTAS)  // HFMM_L2T_NOOBS: lanes-over-quads L2T for every leaf (A/B)  // HFMM_LEAF_V1: the previous quad C2M / L2T kernels (A/B)  // HFMM_P2P_V1: the previous symmetric kernel (A/B)
   double2* d_tmp = nullptr;  // interpolation temporaries
   size_t tmp_elems_ = 0;
   int64_t leaf_b_ = 0, leaf_e_ = 0;  // owned leaf range
@@ -206,6 +196,7 @@ class Engine {
   cudaStream_t st2_ = nullptr;
   cudaStream_t st_cp_ = nullptr;  // host charges in (evaluate_host), beside the T build
   cudaEvent_t ev_q_ = nullptr;
+  cudaEvent_t ev_cp_order_ = nullptr;  // st_ -> st_cp_: the host-charge copy waits for queued work
   bool q_pending_ = false;
   // evaluate_device overlap: far chain (high priority) + leaf M2L (low priority)
   cudaStream_t st_hi_ = nullptr, st_lo_ = nullptr;

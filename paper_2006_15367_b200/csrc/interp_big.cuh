@@ -13,7 +13,7 @@
 #ifndef HFMM_B200_INTERP_BIG_CUH
 #define HFMM_B200_INTERP_BIG_CUH
 
-#include "interp_tc.cuh"
+#include "dmma.cuh"
 
 namespace hfmm_b200 {
 

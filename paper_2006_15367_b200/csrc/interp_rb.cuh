@@ -19,7 +19,7 @@
 #ifndef HFMM_B200_INTERP_RB_CUH
 #define HFMM_B200_INTERP_RB_CUH
 
-#include "interp_tc.cuh"
+#include "dmma.cuh"
 
 namespace hfmm_b200 {
 namespace rb {

@@ -170,88 +170,6 @@ __global__ void __launch_bounds__(128) k_c2m(int64_t leaf_b, const int64_t* __re
 }
 
 // ---------------------------------------------------------------------------
-// M2M phi pass + fold (sphere_grid.cpp:164-171 then fold_transpose :72-83):
-// W[i][jj] = sum_j P_up[jj][j] X[i][j]; stored folded F[p][ii] (n_p/2 circles
-// of length 2 n_c).  One CTA per child.
-__global__ void k_m2m_phi(int n_c, int n_p, int64_t child_b, const double2* __restrict__ mp_c,
-                          const double2* __restrict__ PuT, double2* __restrict__ F) {
-  extern __shared__ double2 sX[];
-  const int64_t child = child_b + blockIdx.x;
-  const int Sc = n_c * n_c;
-  for (int t = threadIdx.x; t < Sc; t += blockDim.x) sX[t] = mp_c[child * Sc + t];
-  __syncthreads();
-  const int half = n_p / 2;
-  double2* Fc = F + (child - child_b) * int64_t(n_p) * n_c;
-  for (int e = threadIdx.x; e < n_c * n_p; e += blockDim.x) {
-    const int i = e / n_p, jj = e % n_p;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int j = 0; j < n_c; ++j) cmac(acc, PuT[j * n_p + jj], sX[i * n_c + j]);
-    const int p = jj < half ? jj : jj - half;
-    const int ii = jj < half ? i : 2 * n_c - 1 - i;
-    Fc[p * (2 * n_c) + ii] = acc;
-  }
-}
-
-// M2M theta pass + unfold + shift + ordered aggregation (sphere_grid.cpp:173-181,
-// :85-102; operators.cpp:28-37; traversal.cpp:392-425).  Grid (parent, circle
-// chunk); each thread keeps E parent samples in registers over the children.
-constexpr int kThetaE = 8;
-__global__ void __launch_bounds__(256) k_m2m_theta(int n_c, int n_p, int CP, int64_t par_b,
-                                                   int64_t child_b,
-                                                   const int* __restrict__ child_off,
-                                                   const int* __restrict__ children,
-                                                   const uint8_t* __restrict__ oct_c,
-                                                   const double2* __restrict__ F,
-                                                   const double2* __restrict__ TuT,
-                                                   const double2* __restrict__ shift_up,
-                                                   double2* __restrict__ mp_p) {
-  extern __shared__ double2 sF[];
-  const int64_t par = par_b + blockIdx.x;
-  const int half = n_p / 2, Lc = 2 * n_c, Lp = 2 * n_p;
-  const int64_t Sp = int64_t(n_p) * n_p;
-  const int p0 = blockIdx.y * CP, p1 = min(half, p0 + CP), ncirc = p1 - p0;
-  const int nout = ncirc * Lp;
-  double2 acc[kThetaE];
-  int sidx[kThetaE];
-#pragma unroll
-  for (int r = 0; r < kThetaE; ++r) {
-    acc[r] = make_double2(0.0, 0.0);
-    const int e = threadIdx.x + r * blockDim.x;
-    int s = -1;
-    if (e < nout) {
-      const int pl = e / Lp, j = e % Lp, p = p0 + pl;
-      s = j < n_p ? j * n_p + p : (Lp - 1 - j) * n_p + p + half;
-    }
-    sidx[r] = s;
-  }
-  for (int kk = child_off[par]; kk < child_off[par + 1]; ++kk) {
-    const int64_t ch = children[kk];
-    const int o = oct_c[ch];
-    const double2* Fc = F + (ch - child_b) * int64_t(n_p) * n_c + int64_t(p0) * Lc;
-    __syncthreads();
-    for (int t = threadIdx.x; t < ncirc * Lc; t += blockDim.x) sF[t] = Fc[t];
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kThetaE; ++r) {
-      const int e = threadIdx.x + r * blockDim.x;
-      if (e < nout) {
-        const int pl = e / Lp, j = e % Lp;
-        double2 g = make_double2(0.0, 0.0);
-        const double2* f = sF + pl * Lc;
-        for (int i = 0; i < Lc; ++i) cmac(g, TuT[i * Lp + j], f[i]);
-        const double2 sh = shift_up[o * Sp + sidx[r]];
-        const double2 v = cmul(g, sh);
-        acc[r].x += v.x;
-        acc[r].y += v.y;
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < kThetaE; ++r)
-    if (sidx[r] >= 0) mp_p[par * Sp + sidx[r]] = acc[r];
-}
-
-// ---------------------------------------------------------------------------
 // M2L (operators.cpp:82-87, traversal.cpp:443-581): L_o[s] = sum_far T[o-src][s] M_src[s].
 // nodes != nullptr (distributed mode): blockIdx.x indexes the held observers.
 __global__ void k_m2l(int64_t S, int64_t node_b, const int* __restrict__ nodes, const int64_t* __restrict__ far_off,
@@ -269,60 +187,6 @@ __global__ void k_m2l(int64_t S, int64_t node_b, const int* __restrict__ nodes, 
 }
 
 // ---------------------------------------------------------------------------
-// L2L theta pass (fold, weighted theta anterpolation 2n_p -> 2n_c, unfold;
-// traversal.cpp:648-661 with sphere_grid.cpp:194-214).  Grid (child, circle
-// chunk); parent samples are shifted (operators.cpp:28-37) while staged.
-__global__ void k_l2l_theta(int n_c, int n_p, int CP, int64_t child_b,
-                            const int* __restrict__ parent_c, const uint8_t* __restrict__ oct_c,
-                            const double2* __restrict__ loc_p, const double2* __restrict__ shift_dn,
-                            const double2* __restrict__ TdT, double2* __restrict__ Nb) {
-  extern __shared__ double2 sZ[];
-  const int64_t child = child_b + blockIdx.x;
-  const int64_t par = parent_c[child];
-  const int o = oct_c[child];
-  const int half = n_p / 2, Lc = 2 * n_c, Lp = 2 * n_p;
-  const int64_t Sp = int64_t(n_p) * n_p;
-  const int p0 = blockIdx.y * CP, p1 = min(half, p0 + CP), ncirc = p1 - p0;
-  for (int t = threadIdx.x; t < ncirc * Lp; t += blockDim.x) {
-    const int pl = t / Lp, i = t % Lp, p = p0 + pl;
-    const int64_t s = i < n_p ? int64_t(i) * n_p + p : int64_t(Lp - 1 - i) * n_p + p + half;
-    sZ[t] = cmul(loc_p[par * Sp + s], shift_dn[o * Sp + s]);
-  }
-  __syncthreads();
-  double2* Nc = Nb + (child - child_b) * int64_t(n_c) * n_p;
-  for (int e = threadIdx.x; e < ncirc * Lc; e += blockDim.x) {
-    const int pl = e / Lc, j = e % Lc, p = p0 + pl;
-    double2 g = make_double2(0.0, 0.0);
-    const double2* f = sZ + pl * Lp;
-    for (int i = 0; i < Lp; ++i) cmac(g, TdT[i * Lc + j], f[i]);
-    const int row = j < n_c ? j : Lc - 1 - j;
-    const int col = j < n_c ? p : p + half;
-    Nc[row * n_p + col] = g;
-  }
-}
-
-// L2L phi pass (n_p -> n_c per theta row) and accumulation into the child
-// locals (traversal.cpp:658-660).  One CTA per child.
-__global__ void k_l2l_phi(int n_c, int n_p, int64_t child_b, const double2* __restrict__ Nb,
-                          const double2* __restrict__ PdT, double2* __restrict__ loc_c) {
-  extern __shared__ double2 sN[];
-  const int64_t child = child_b + blockIdx.x;
-  const double2* Nc = Nb + (child - child_b) * int64_t(n_c) * n_p;
-  for (int t = threadIdx.x; t < n_c * n_p; t += blockDim.x) sN[t] = Nc[t];
-  __syncthreads();
-  const int64_t Sc = int64_t(n_c) * n_c;
-  for (int e = threadIdx.x; e < n_c * n_c; e += blockDim.x) {
-    const int r = e / n_c, jc = e % n_c;
-    double2 v = make_double2(0.0, 0.0);
-    for (int jp = 0; jp < n_p; ++jp) cmac(v, PdT[jp * n_c + jc], sN[r * n_p + jp]);
-    double2 cur = loc_c[child * Sc + e];
-    cur.x += v.x;
-    cur.y += v.y;
-    loc_c[child * Sc + e] = cur;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Quad-symmetric C2M / L2T.  The sample grid (sphere_grid.cpp:25-50) is
 // symmetric: theta_{n-1-i} = pi - theta_i and phi_{j+n/2} = phi_j + pi, so the
 // four samples (i, j), (n-1-i, j), (i, j+n/2), (n-1-i, j+n/2) of a quad have
@@ -333,176 +197,8 @@ __global__ void k_l2l_phi(int n_c, int n_p, int64_t child_b, const double2* __re
 // (a quarter of the direct sincos count); the phases equal the reference's
 // per-sample ones to rounding.  One warp per leaf.
 constexpr int kQuadHalfMax = 16;  // n/2 <= 16 (leaf grids of the BASELINE configs: n <= 26)
-constexpr int kQuadR = 3;  // quads per lane per pass (C2M; measured best of 2..4)
 constexpr int kQuadP = 32;        // particles per B-table chunk
 
-// exp(i(A+B)), exp(i(A-B)); the other two are their conjugates.
-__device__ __forceinline__ void quad_exp(double ca, double sa, double2 eb, double2& e1, double2& e2) {
-  const double P = ca * eb.x, Q = sa * eb.y, R = sa * eb.x, T = ca * eb.y;
-  e1 = make_double2(P - Q, R + T);
-  e2 = make_double2(P + Q, R - T);
-}
-
-__global__ void __launch_bounds__(128) k_c2m_quad(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
-                                                  const double* __restrict__ x, const double* __restrict__ y,
-                                                  const double* __restrict__ z, const double2* __restrict__ q,
-                                                  const double* __restrict__ centers, const double* __restrict__ dir,
-                                                  int n, double k, double2* __restrict__ mp) {
-  __shared__ double2 sB[4][kQuadP][kQuadHalfMax];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
-  if (li >= nl) return;  // whole warp
-  const int64_t leaf = leaf_b + li;
-  const int half = n / 2, quads = half * half, nphi = n;
-  const int64_t S = int64_t(n) * n;
-  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
-  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
-  double2 (*B)[kQuadHalfMax] = sB[warp];
-  for (int qc = 0; qc < quads; qc += 32 * kQuadR) {
-    double ax[kQuadR], ay[kQuadR];
-    int qi[kQuadR];
-    double2 acc[kQuadR][4];
-#pragma unroll
-    for (int r = 0; r < kQuadR; ++r) {
-      const int qd = qc + lane + 32 * r;
-      const int i = qd < quads ? qd / half : 0, j = qd < quads ? qd - (qd / half) * half : 0;
-      qi[r] = i;
-      const int64_t s1 = int64_t(i) * nphi + j;
-      ax[r] = k * dir[3 * s1];
-      ay[r] = k * dir[3 * s1 + 1];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[r][u] = make_double2(0.0, 0.0);
-    }
-    for (int64_t pc = p0; pc < p1; pc += kQuadP) {
-      const int np = int(p1 - pc < kQuadP ? p1 - pc : kQuadP);
-      __syncwarp();
-      for (int t = lane; t < np * half; t += 32) {  // B table: exp(i k z cos(theta_i))
-        const int pp = t / half, i = t - pp * half;
-        double sn, cs;
-        sincos_fast(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), &sn, &cs);
-        B[pp][i] = make_double2(cs, sn);
-      }
-      __syncwarp();
-      for (int pp = 0; pp < np; ++pp) {
-        const double rx = x[pc + pp] - cx, ry = y[pc + pp] - cy;
-        const double2 qq = q[pc + pp];
-#pragma unroll
-        for (int r = 0; r < kQuadR; ++r) {
-          double sa, ca;
-          sincos_fast(fma(ax[r], rx, ay[r] * ry), &sa, &ca);
-          double2 e1, e2;
-          quad_exp(ca, sa, B[pp][qi[r]], e1, e2);
-          // q * e (samples 1, 2) and q * conj(e) (samples 4, 3)
-          acc[r][0].x = fma(qq.x, e1.x, fma(-qq.y, e1.y, acc[r][0].x));
-          acc[r][0].y = fma(qq.x, e1.y, fma(qq.y, e1.x, acc[r][0].y));
-          acc[r][3].x = fma(qq.x, e1.x, fma(qq.y, e1.y, acc[r][3].x));
-          acc[r][3].y = fma(-qq.x, e1.y, fma(qq.y, e1.x, acc[r][3].y));
-          acc[r][1].x = fma(qq.x, e2.x, fma(-qq.y, e2.y, acc[r][1].x));
-          acc[r][1].y = fma(qq.x, e2.y, fma(qq.y, e2.x, acc[r][1].y));
-          acc[r][2].x = fma(qq.x, e2.x, fma(qq.y, e2.y, acc[r][2].x));
-          acc[r][2].y = fma(-qq.x, e2.y, fma(qq.y, e2.x, acc[r][2].y));
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kQuadR; ++r) {
-      const int qd = qc + lane + 32 * r;
-      if (qd < quads) {
-        const int i = qd / half, j = qd - i * half;
-        double2* m = mp + leaf * S;
-        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
-        m[s1] = acc[r][0];             // A + B
-        m[s2] = acc[r][1];             // A - B   (pi - theta)
-        m[s1 + half] = acc[r][2];      // -A + B  (phi + pi)
-        m[s2 + half] = acc[r][3];      // -A - B
-      }
-    }
-  }
-}
-
-// L2T: potentials of a leaf's observers from its local samples; lanes over
-// quads, kQuadOB observers per pass (the four samples w_s L_s of a quad are
-// read once, straight from L1 / global, for all of them -- their latency
-// overlaps the sincos chains, which interleave), one shuffle reduction each.
-constexpr int kQuadOB = 4;
-__global__ void __launch_bounds__(128) k_l2t_quad(int64_t leaf_b, int64_t nl, const int64_t* __restrict__ leaf_start,
-                                                  const double* __restrict__ x, const double* __restrict__ y,
-                                                  const double* __restrict__ z, const double* __restrict__ centers,
-                                                  const double* __restrict__ dir, const double* __restrict__ wq,
-                                                  int n, double k, const double2* __restrict__ loc,
-                                                  double2* __restrict__ pot) {
-  extern __shared__ double2 qsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = n / 2, quads = half * half, nphi = n;
-  const int64_t S = int64_t(n) * n;
-  double2* Bt = qsm + warp * (kQuadP * half);  // B table of this warp
-  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
-  if (li >= nl) return;
-  const int64_t leaf = leaf_b + li;
-  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
-  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
-  const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
-  for (int64_t pc = p0; pc < p1; pc += kQuadP) {
-    const int np = int(p1 - pc < kQuadP ? p1 - pc : kQuadP);
-    __syncwarp();
-    for (int t = lane; t < np * half; t += 32) {  // exp(i k z cos(theta_i)) (conjugated below)
-      const int pp = t / half, i = t - pp * half;
-      double sn, cs;
-      sincos_fast(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), &sn, &cs);
-      Bt[pp * half + i] = make_double2(cs, sn);
-    }
-    __syncwarp();
-    for (int pb = 0; pb < np; pb += kQuadOB) {
-      double rx[kQuadOB], ry[kQuadOB], ar[kQuadOB], ai[kQuadOB];
-#pragma unroll
-      for (int o = 0; o < kQuadOB; ++o) {
-        const int pp = pb + o < np ? pb + o : pb;  // idle slots repeat a live observer
-        rx[o] = k * (x[pc + pp] - cx);
-        ry[o] = k * (y[pc + pp] - cy);
-        ar[o] = 0.0;
-        ai[o] = 0.0;
-      }
-      for (int qd = lane; qd < quads; qd += 32) {
-        const int i = qd / half, j = qd - i * half;
-        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
-        const double dxs = dir[3 * s1], dys = dir[3 * s1 + 1];
-        const double2* lc = loc + leaf * S;
-        auto lw = [&](int64_t s) {
-          const double2 v = __ldg(lc + s);
-          const double w = __ldg(wq + s);
-          return make_double2(w * v.x, w * v.y);
-        };
-        const double2 l1 = lw(s1), l2 = lw(s2), l3 = lw(s1 + half), l4 = lw(s2 + half);
-#pragma unroll
-        for (int o = 0; o < kQuadOB; ++o) {
-          const int pp = pb + o < np ? pb + o : pb;
-          double sa, ca;
-          sincos_fast(fma(dxs, rx[o], dys * ry[o]), &sa, &ca);
-          double2 e1, e2;
-          quad_exp(ca, sa, Bt[pp * half + i], e1, e2);
-          // sum_s Lw_s exp(-i phase_s): conj(e1) at s1, conj(e2) at s2, e2 at s1 + half, e1 at s2 + half
-          ar[o] = fma(l1.x, e1.x, fma(l1.y, e1.y, ar[o]));
-          ai[o] = fma(l1.y, e1.x, fma(-l1.x, e1.y, ai[o]));
-          ar[o] = fma(l2.x, e2.x, fma(l2.y, e2.y, ar[o]));
-          ai[o] = fma(l2.y, e2.x, fma(-l2.x, e2.y, ai[o]));
-          ar[o] = fma(l3.x, e2.x, fma(-l3.y, e2.y, ar[o]));
-          ai[o] = fma(l3.y, e2.x, fma(l3.x, e2.y, ai[o]));
-          ar[o] = fma(l4.x, e1.x, fma(-l4.y, e1.y, ar[o]));
-          ai[o] = fma(l4.y, e1.x, fma(l4.x, e1.y, ai[o]));
-        }
-      }
-#pragma unroll
-      for (int o = 0; o < kQuadOB; ++o) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          ar[o] += __shfl_xor_sync(0xffffffffu, ar[o], off);
-          ai[o] += __shfl_xor_sync(0xffffffffu, ai[o], off);
-        }
-        if (lane == 0 && pb + o < np) pot[pc + pb + o] = make_double2(-c * ai[o], c * ar[o]);
-      }
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // L2T (operators.cpp:89-108, driver traversal.cpp:717-728): one CTA per leaf,
@@ -875,152 +571,6 @@ __global__ void __launch_bounds__(128) k_p2p_small_w(int n_small, const int* __r
 }
 
 // ---------------------------------------------------------------------------
-// Symmetric near field for dense leaves: g(r) is the same for (m <- n) and
-// (n <- m), so every unordered pair of dense own leaves (A, B), A < B, is
-// evaluated once by A's CTA: A's observers accumulate in registers, B's in a
-// per-pair scratch row (warp-reduced over A's observers), which
-// k_p2p_gather adds to B in a fixed order (deterministic).  The self leaf
-// and neighbours that are small or ghost leaves go through the one-sided
-// path (`plain` list).
-__global__ void __launch_bounds__(128) k_p2p_sym(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
-                                                 const int* __restrict__ plain_off, const int* __restrict__ plain,
-                                                 const int* __restrict__ sym_off, const int* __restrict__ sym,
-                                                 const int64_t* __restrict__ sym_scr,
-                                                 const double* __restrict__ centers, const double* __restrict__ x,
-                                                 const double* __restrict__ y, const double* __restrict__ z,
-                                                 const double2* __restrict__ q, double k, double2* __restrict__ pot,
-                                                 double2* __restrict__ scratch) {
-  __shared__ P2PShared sh;
-  __shared__ double2 red[4][32 * kP2PObsPerLane];
-  const int i = blockIdx.x;
-  const int64_t leaf = leaves[i];
-  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
-  const int n_o = int(p1 - p0);
-  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
-  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  // plain list as a concatenated source list (prefix sums as in p2p_prepare)
-  if (threadIdx.x == 0) {
-    const int b = plain_off[i], nn = plain_off[i + 1] - b;
-    int64_t run = 0;
-    for (int j = 0; j < nn; ++j) {
-      const int lf = plain[b + j];
-      sh.pref[j] = run;
-      sh.nbeg[j] = leaf_start[lf];
-      run += leaf_start[lf + 1] - leaf_start[lf];
-    }
-    sh.pref[nn] = run;
-    sh.nn = nn;
-  }
-  __syncthreads();
-  const int64_t total = sh.pref[sh.nn];
-  for (int ob = 0, pass = 0; ob < n_o; ob += 32 * kP2PObsPerLane, ++pass) {
-    const int no = min(n_o - ob, 32 * kP2PObsPerLane);
-    const int nc = (no + 31) >> 5;
-    double xo[kP2PObsPerLane], yo[kP2PObsPerLane], zo[kP2PObsPerLane];
-    double2 qo[kP2PObsPerLane];
-    double ar[kP2PObsPerLane], ai[kP2PObsPerLane];
-#pragma unroll
-    for (int c = 0; c < kP2PObsPerLane; ++c) {
-      const int o = lane + 32 * c;
-      const bool v = c < nc && o < no;
-      // invalid slots: far away but finite (zero charge, finite kernel value),
-      // so their terms in the partner leaf's reduction are exact zeros
-      xo[c] = v ? k * (x[p0 + ob + o] - cx) : 1.0e4;
-      yo[c] = v ? k * (y[p0 + ob + o] - cy) : 0.0;
-      zo[c] = v ? k * (z[p0 + ob + o] - cz) : 0.0;
-      const double2 qq = v ? q[p0 + ob + o] : make_double2(0.0, 0.0);
-      qo[c] = make_double2(qs * qq.x, qs * qq.y);
-      ar[c] = 0.0;
-      ai[c] = 0.0;
-    }
-    // one-sided part: self leaf + small / ghost neighbours
-    for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
-      const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
-      __syncthreads();
-      p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
-      __syncthreads();
-      for (int t = warp; t < n; t += nwarp) {
-        const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
-        const double2 qq = sh.sq[t];
-#pragma unroll
-        for (int c = 0; c < kP2PObsPerLane; ++c)
-          if (c < nc) p2p_pair(xo[c], yo[c], zo[c], px, py, pz, qq, ar[c], ai[c]);
-      }
-    }
-    // symmetric part: dense partners B > A
-    for (int j = sym_off[i]; j < sym_off[i + 1]; ++j) {
-      const int lb = sym[j];
-      const int64_t b0 = leaf_start[lb], nbp = leaf_start[lb + 1] - b0;
-      double2* scr = scratch + sym_scr[j];
-      for (int64_t cb = 0; cb < nbp; cb += kP2PChunk) {
-        const int n = int(nbp - cb < kP2PChunk ? nbp - cb : kP2PChunk);
-        __syncthreads();
-        for (int t = threadIdx.x; t < n; t += blockDim.x) {
-          const int64_t src = b0 + cb + t;
-          sh.sx[t] = k * (x[src] - cx);
-          sh.sy[t] = k * (y[src] - cy);
-          sh.sz[t] = k * (z[src] - cz);
-          const double2 qq = q[src];
-          sh.sq[t] = make_double2(qs * qq.x, qs * qq.y);
-        }
-        __syncthreads();
-        for (int t = warp; t < n; t += nwarp) {
-          const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
-          const double2 qq = sh.sq[t];
-          double br = 0.0, bi = 0.0;
-          // Branch- and mask-free: idle observer slots sit at a finite far
-          // point with zero charge (exact-zero terms), and two particles in
-          // different leaves are never coincident (equal positions share a
-          // Morton cell), so r2 > 0 here.
-#pragma unroll
-          for (int c = 0; c < kP2PObsPerLane; ++c) {
-            const double dx = xo[c] - px, dy = yo[c] - py, dz = zo[c] - pz;
-            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-            const double ri = rsqrt(r2);
-            double sn, cs;
-            sincos_fast(-(r2 * ri), &sn, &cs);
-            const double gr = cs * ri, gi = sn * ri;
-            ar[c] = fma(gr, qq.x, fma(-gi, qq.y, ar[c]));
-            ai[c] = fma(gr, qq.y, fma(gi, qq.x, ai[c]));
-            br = fma(gr, qo[c].x, fma(-gi, qo[c].y, br));
-            bi = fma(gr, qo[c].y, fma(gi, qo[c].x, bi));
-          }
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            br += __shfl_xor_sync(0xffffffffu, br, off);
-            bi += __shfl_xor_sync(0xffffffffu, bi, off);
-          }
-          if (lane == 0) {
-            double2 v = make_double2(br, bi);
-            if (pass > 0) {
-              const double2 old = scr[cb + t];
-              v.x += old.x;
-              v.y += old.y;
-            }
-            scr[cb + t] = v;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < kP2PObsPerLane; ++c) red[warp][lane + 32 * c] = make_double2(ar[c], ai[c]);
-    __syncthreads();
-    for (int o = threadIdx.x; o < no; o += blockDim.x) {
-      double2 sum = red[0][o];
-      for (int w = 1; w < nwarp; ++w) {
-        sum.x += red[w][o].x;
-        sum.y += red[w][o].y;
-      }
-      double2 cur = pot[p0 + ob + o];
-      cur.x += sum.x;
-      cur.y += sum.y;
-      pot[p0 + ob + o] = cur;
-    }
-    __syncthreads();
-  }
-}
-
 // Adds the scratch rows other dense leaves wrote for leaf B (fixed order).
 __global__ void k_p2p_gather(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
                              const int* __restrict__ in_off, const int64_t* __restrict__ in_scr,

@@ -179,6 +179,7 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
   }
 }
 
+constexpr int kQuadOB = 4;  // observers per L2T pass
 // L2T, one warp per leaf: lanes over quads, kQuadOB observers per pass
 // (warp-shuffle reduction per observer), e^{iB} table per particle and row.
 // leaves != nullptr: warp w takes leaves[w] (a population class), else leaf_b + w.

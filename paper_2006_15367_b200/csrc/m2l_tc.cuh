@@ -18,7 +18,7 @@
 #ifndef HFMM_B200_M2L_TC_CUH
 #define HFMM_B200_M2L_TC_CUH
 
-#include "interp_tc.cuh"
+#include "dmma.cuh"
 #include "m2l.cuh"
 
 namespace hfmm_b200 {
