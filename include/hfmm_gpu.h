@@ -109,8 +109,11 @@ typedef enum hfmm_phase {
   HFMM_PHASE_L2T = 5, /* l2o part of l2o_near_phase traversal.cpp:717-728 */
   HFMM_PHASE_NEAR = 6, /* near part of l2o_near_phase traversal.cpp:768-786: joins it into
                           the potentials (launching it first if not started) */
-  HFMM_PHASE_NEAR_START = 7 /* launches the near field on the engine's side stream
+  HFMM_PHASE_NEAR_START = 7, /* launches the near field on the engine's side stream
                                (overlaps the far-field phases; needs charges/ghosts) */
+  HFMM_PHASE_T_BUILD = 8 /* translation operators of every level (OperatorCache::build,
+                            operators.cpp:124-176); HFMM_PHASE_M2L includes it, the
+                            level-wise hfmm_gpu_run_level(M2L) needs it first */
 } hfmm_phase;
 
 /* Per-phase device milliseconds of the last hfmm_gpu_evaluate (CUDA events
@@ -169,22 +172,37 @@ hfmm_status hfmm_gpu_get_potentials_sorted(hfmm_gpu* g, double* out,
                                            size_t cap_doubles);
 
 /* ---------------- distributed mode (num_ranks > 1, one process per GPU) ----
- * Rank r holds the nodes whose leaf range meets its Morton leaf range; the
- * upward pass yields partial multipoles; one static exchange (kind 0) adds
- * the partials of every far source a held observer needs; ghost particles
- * of neighbouring ranks (kind 1, the reference near plan comm_plan.cpp:84-109)
- * feed the near field.  The caller moves the buffers (e.g. NCCL); the
- * engine packs / unpacks them on its stream.  Sequence per evaluation:
- *   set_charges | load_charges_device; ghosts: pack(1,q) -> send/recv -> unpack(1,q);
- *   run_phase(C2M), run_phase(M2M); exchange_begin(0); pack(0,q) -> send/recv ->
- *   unpack(0,q) for q in rank order; run_phase(M2L..NEAR).
+ * Rank r holds the nodes whose leaf range meets its Morton leaf range.  The
+ * upward pass (C2M, M2M) yields partial multipoles of held nodes; plural
+ * (shared) nodes are SLICED by theta rows (assign_sample_slices,
+ * tree.cpp:180-239): after the upward pass each user holds the full
+ * multipole on its own slice.  Exchange kinds (static plans, rows = flat
+ * sample ranges of a node):
+ *   0  M2L halo: the reference's M2L CommPlan (comm_plan.cpp:31-82), the
+ *      source rows (sender slice) x (receiver observer slice); per level;
+ *   1  ghost particles (x, y, z, re, im) of the reference near plan
+ *      (comm_plan.cpp:84-109);
+ *   2  plural multipole reduce-scatter among a node's users (partials of the
+ *      receiver's slice, added in the order unpack is called: call it in
+ *      ascending peer rank);
+ *   3  plural local all-gather among a node's users (each user's final slice
+ *      rows), per level, before the L2L from that level.
+ * The caller moves the buffers (e.g. NCCL); the engine packs / unpacks them on
+ * its stream.  `level` = -1 selects all levels laid out level-major (kinds 0,
+ * 2, 3; ignored for kind 1).  Sequence per evaluation (distributed.py):
+ *   set_charges | load_charges_device; kind 1; run_phase(NEAR_START, C2M, M2M);
+ *   kind 2 (all levels); run_phase(T_BUILD); for l = top..L: kind 0 (level l),
+ *   run_level(M2L, l); for l = top..L-1: kind 3 (level l), run_level(L2L, l);
+ *   run_phase(L2T), run_phase(NEAR).
  * In distributed mode hfmm_gpu_set_charges takes the full input-order array
  * and keeps this rank's particles only. */
-hfmm_status hfmm_gpu_exchange_sizes(hfmm_gpu* g, int kind, int peer, int64_t* send_doubles,
-                                    int64_t* recv_doubles);
-hfmm_status hfmm_gpu_exchange_begin(hfmm_gpu* g, int kind);
-hfmm_status hfmm_gpu_pack(hfmm_gpu* g, int kind, int peer, double* d_send);
-hfmm_status hfmm_gpu_unpack(hfmm_gpu* g, int kind, int peer, const double* d_recv);
+hfmm_status hfmm_gpu_exchange_sizes(hfmm_gpu* g, int kind, int peer, int level,
+                                    int64_t* send_doubles, int64_t* recv_doubles);
+hfmm_status hfmm_gpu_pack(hfmm_gpu* g, int kind, int peer, int level, double* d_send);
+hfmm_status hfmm_gpu_unpack(hfmm_gpu* g, int kind, int peer, int level, const double* d_recv);
+/* One level of a phase: HFMM_PHASE_M2L (observer level, after HFMM_PHASE_T_BUILD)
+ * or HFMM_PHASE_L2L (parent level l -> children at l + 1). */
+hfmm_status hfmm_gpu_run_level(hfmm_gpu* g, int phase, int level);
 /* All engine work goes to `stream` (cudaStream_t; NULL = a private stream). */
 hfmm_status hfmm_gpu_set_stream(hfmm_gpu* g, void* stream);
 hfmm_status hfmm_gpu_synchronize(hfmm_gpu* g);

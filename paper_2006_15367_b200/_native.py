@@ -98,11 +98,11 @@ _SIG = {
     "hfmm_gpu_run_phase": (ctypes.c_int, [_P, ctypes.c_int]),
     "hfmm_gpu_get_expansion": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t]),
     "hfmm_gpu_get_potentials_sorted": (ctypes.c_int, [_P, _P, ctypes.c_size_t]),
-    "hfmm_gpu_exchange_sizes": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
-                                               ctypes.POINTER(ctypes.c_int64)]),
-    "hfmm_gpu_exchange_begin": (ctypes.c_int, [_P, ctypes.c_int]),
-    "hfmm_gpu_pack": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P]),
-    "hfmm_gpu_unpack": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P]),
+    "hfmm_gpu_exchange_sizes": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "hfmm_gpu_pack": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
+    "hfmm_gpu_unpack": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]),
+    "hfmm_gpu_run_level": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
     "hfmm_gpu_set_stream": (ctypes.c_int, [_P, _P]),
     "hfmm_gpu_synchronize": (ctypes.c_int, [_P]),
     "hfmm_gpu_load_charges_device": (ctypes.c_int, [_P, _P]),

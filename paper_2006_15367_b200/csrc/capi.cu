@@ -190,33 +190,34 @@ hfmm_status hfmm_gpu_get_potentials_sorted(hfmm_gpu* g, double* out, size_t cap)
   });
 }
 
-hfmm_status hfmm_gpu_exchange_sizes(hfmm_gpu* g, int kind, int peer, int64_t* send_d, int64_t* recv_d) {
+hfmm_status hfmm_gpu_exchange_sizes(hfmm_gpu* g, int kind, int peer, int level, int64_t* send_d,
+                                    int64_t* recv_d) {
   return guard([&] {
     need(g, "hfmm_gpu_exchange_sizes(gpu)");
     need(send_d, "hfmm_gpu_exchange_sizes(send)");
     need(recv_d, "hfmm_gpu_exchange_sizes(recv)");
-    g->eng->exchange_sizes(kind, peer, send_d, recv_d);
+    g->eng->exchange_sizes(kind, peer, level, send_d, recv_d);
   });
 }
 
-hfmm_status hfmm_gpu_exchange_begin(hfmm_gpu* g, int kind) {
-  return guard([&] {
-    need(g, "hfmm_gpu_exchange_begin(gpu)");
-    g->eng->exchange_begin(kind);
-  });
-}
-
-hfmm_status hfmm_gpu_pack(hfmm_gpu* g, int kind, int peer, double* d_send) {
+hfmm_status hfmm_gpu_pack(hfmm_gpu* g, int kind, int peer, int level, double* d_send) {
   return guard([&] {
     need(g, "hfmm_gpu_pack(gpu)");
-    g->eng->pack(kind, peer, d_send);
+    g->eng->pack(kind, peer, level, d_send);
   });
 }
 
-hfmm_status hfmm_gpu_unpack(hfmm_gpu* g, int kind, int peer, const double* d_recv) {
+hfmm_status hfmm_gpu_unpack(hfmm_gpu* g, int kind, int peer, int level, const double* d_recv) {
   return guard([&] {
     need(g, "hfmm_gpu_unpack(gpu)");
-    g->eng->unpack(kind, peer, d_recv);
+    g->eng->unpack(kind, peer, level, d_recv);
+  });
+}
+
+hfmm_status hfmm_gpu_run_level(hfmm_gpu* g, int phase, int level) {
+  return guard([&] {
+    need(g, "hfmm_gpu_run_level(gpu)");
+    g->eng->run_level(phase, level);
   });
 }
 

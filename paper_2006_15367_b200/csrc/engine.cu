@@ -22,8 +22,10 @@ namespace hfmm_b200 {
 namespace {
 
 void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess)
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // a non-sticky error must not resurface at the next launch check
     throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
 }
 
 inline int slot_of(long ox, long oy, long oz) {
@@ -557,9 +559,6 @@ bool rbl_ok(int nc, int np) {
 }  // namespace
 
 void Engine::phase_m2m() {
-  // Distributed mode: halo rows still hold last evaluation's full multipoles;
-  // the upward pass must see zeros there (they are summed again after it).
-  if (dist_) exchange_begin(0);
   for (int l = s_.L - 1; l >= s_.top; --l) {
     DevLevel& P = lv_[size_t(l)];
     DevLevel& C = lv_[size_t(l + 1)];
@@ -745,11 +744,8 @@ void Engine::phase_l2t() {
       }
     }
   } else {  // leaf grids past kQuadHalfMax: generic kernel
-    const size_t smem = size_t(d.S) * (sizeof(double2) + 3 * sizeof(double));
-    if (smem > 48 * 1024)
-      ck(cudaFuncSetAttribute(k_l2t, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-    k_l2t<<<unsigned(nl), 128, smem, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.S,
-                                            s_.k, d.loc, d_pot);
+    k_l2t<<<unsigned(nl), 128, 0, st_>>>(leaf_b_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.S, s_.k,
+                                         d.loc, d_pot);
   }
   ++launches_;
   ck(cudaGetLastError(), "k_l2t");
@@ -851,6 +847,9 @@ void Engine::run_phase(int phase) {
       break;
     case HFMM_PHASE_NEAR_START:
       near_start();
+      break;
+    case HFMM_PHASE_T_BUILD:
+      build_T();
       break;
     default:
       throw std::invalid_argument("hfmm_gpu_run_phase: unknown phase");
@@ -1075,32 +1074,32 @@ void Engine::upload_rank_plan() {
       d.m2l_blk = upload_vec(blk);
     }
   }
-  halo_nodes_.assign(size_t(L + 1), nullptr);
-  halo_cnt_.assign(size_t(L + 1), 0);
-  for (int l = s.top; l <= L; ++l) {
-    halo_cnt_[size_t(l)] = int(rp.halo[size_t(l)].size());
-    halo_nodes_[size_t(l)] = upload_vec(rp.halo[size_t(l)]);
-  }
   peers_.assign(size_t(P), PeerPlan{});
   for (int q = 0; q < P; ++q) {
     if (q == rank_) continue;
     PeerPlan& pp = peers_[size_t(q)];
-    pp.mp_send_nodes.assign(size_t(L + 1), nullptr);
-    pp.mp_recv_nodes.assign(size_t(L + 1), nullptr);
-    pp.mp_send_cnt.assign(size_t(L + 1), 0);
-    pp.mp_recv_cnt.assign(size_t(L + 1), 0);
-    for (int dir = 0; dir < 2; ++dir) {
-      const auto& items = dir == 0 ? rp.mp_send[size_t(q)] : rp.mp_recv[size_t(q)];
-      std::vector<std::vector<int>> per(size_t(L + 1));
-      for (auto [l, n] : items) per[size_t(l)].push_back(n);
-      int64_t total = 0;
-      for (int l = s.top; l <= L; ++l) {
-        (dir == 0 ? pp.mp_send_cnt : pp.mp_recv_cnt)[size_t(l)] = int(per[size_t(l)].size());
-        (dir == 0 ? pp.mp_send_nodes : pp.mp_recv_nodes)[size_t(l)] = upload_vec(per[size_t(l)]);
-        total += int64_t(per[size_t(l)].size()) * lv_[size_t(l)].S * 2;
+    for (int kind : {int(kXHalo), int(kXReduce), int(kXGather)})
+      for (int dir = 0; dir < 2; ++dir) {
+        const std::vector<RowItem>& items = dir == 0 ? rp.send[kind][size_t(q)] : rp.recv[kind][size_t(q)];
+        RowXfer& x = dir == 0 ? pp.send[kind] : pp.recv[kind];
+        x.items.assign(size_t(L + 1), nullptr);
+        x.cnt.assign(size_t(L + 1), 0);
+        x.len.assign(size_t(L + 1), 0);
+        x.maxlen.assign(size_t(L + 1), 0);
+        std::vector<std::vector<int64_t>> per(size_t(L + 1));
+        for (const RowItem& it : items) {  // (level, node, begin) order
+          auto& v = per[size_t(it.level)];
+          const int64_t len = it.end - it.begin;
+          v.insert(v.end(), {int64_t(it.node), it.begin, len, x.len[size_t(it.level)]});
+          x.len[size_t(it.level)] += len;
+          x.maxlen[size_t(it.level)] = std::max(x.maxlen[size_t(it.level)], len);
+        }
+        for (int l = s.top; l <= L; ++l) {
+          x.cnt[size_t(l)] = int(per[size_t(l)].size() / 4);
+          if (x.cnt[size_t(l)]) x.items[size_t(l)] = upload_vec(per[size_t(l)]);
+          x.total += x.len[size_t(l)];
+        }
       }
-      (dir == 0 ? pp.mp_send : pp.mp_recv) = total;
-    }
     // ghosts: leaves r owns that q needs, and leaves q owns that r needs (comm_plan.cpp:84-109)
     for (int dir = 0; dir < 2; ++dir) {
       const auto& leaves = dir == 0 ? s.near_send[size_t(rank_) * P + size_t(q)] : s.near_send[size_t(q) * P + size_t(rank_)];
@@ -1113,83 +1112,98 @@ void Engine::upload_rank_plan() {
   }
 }
 
-void Engine::exchange_sizes(int kind, int peer, int64_t* send_d, int64_t* recv_d) const {
+namespace {
+void check_level(int level, int top, int L) {
+  if (level != -1 && (level < top || level > L)) throw std::out_of_range("exchange: level not computed");
+}
+}  // namespace
+
+void Engine::exchange_sizes(int kind, int peer, int level, int64_t* send_d, int64_t* recv_d) const {
   if (!dist_) throw std::logic_error("exchange: single-rank engine");
-  if (peer < 0 || peer >= s_.P) throw std::out_of_range("exchange: bad peer");
+  if (peer < 0 || peer >= s_.P || peer == rank_) throw std::out_of_range("exchange: bad peer");
   const PeerPlan& pp = peers_[size_t(peer)];
-  if (kind == 0) {
-    *send_d = pp.mp_send;
-    *recv_d = pp.mp_recv;
-  } else if (kind == 1) {
+  if (kind == kXGhost) {
     *send_d = 5 * pp.n_gh_send;
     *recv_d = 5 * pp.n_gh_recv;
-  } else {
-    throw std::invalid_argument("exchange: bad kind");
+    return;
   }
+  if (kind != kXHalo && kind != kXReduce && kind != kXGather) throw std::invalid_argument("exchange: bad kind");
+  check_level(level, s_.top, s_.L);
+  const RowXfer& sx = pp.send[kind];
+  const RowXfer& rx = pp.recv[kind];
+  *send_d = 2 * (level < 0 ? sx.total : sx.len[size_t(level)]);
+  *recv_d = 2 * (level < 0 ? rx.total : rx.len[size_t(level)]);
 }
 
-void Engine::exchange_begin(int kind) {
-  ck(cudaSetDevice(dev_), "cudaSetDevice");
-  if (!dist_) throw std::logic_error("exchange: single-rank engine");
-  if (kind != 0) return;
-  for (int l = s_.top; l <= s_.L; ++l) {  // halo sources start from zero before the partial sums
-    if (halo_cnt_[size_t(l)] == 0) continue;
-    const DevLevel& d = lv_[size_t(l)];
-    dim3 grid(unsigned(halo_cnt_[size_t(l)]), unsigned(std::min<int64_t>((d.S + 255) / 256, 64)));
-    k_zero_rows<<<grid, 256, 0, st_>>>(d.mp, halo_nodes_[size_t(l)], d.S);
-    ++launches_;
-  }
-  ck(cudaGetLastError(), "exchange_begin");
-}
-
-void Engine::pack(int kind, int peer, double* d_buf) {
+void Engine::pack(int kind, int peer, int level, double* d_buf) {
   ck(cudaSetDevice(dev_), "cudaSetDevice");
   int64_t sd = 0, rd = 0;
-  exchange_sizes(kind, peer, &sd, &rd);
+  exchange_sizes(kind, peer, level, &sd, &rd);
   const PeerPlan& pp = peers_[size_t(peer)];
-  if (kind == 0) {
-    int64_t off = 0;
-    for (int l = s_.top; l <= s_.L; ++l) {
-      const int cnt = pp.mp_send_cnt[size_t(l)];
-      if (cnt == 0) continue;
-      const DevLevel& d = lv_[size_t(l)];
-      dim3 grid(unsigned(cnt), unsigned(std::min<int64_t>((d.S + 255) / 256, 64)));
-      k_pack_rows<<<grid, 256, 0, st_>>>(d.mp, pp.mp_send_nodes[size_t(l)], d.S,
-                                         reinterpret_cast<double2*>(d_buf + off));
+  if (kind == kXGhost) {
+    if (pp.n_gh_send > 0) {
+      k_pack_particles<<<unsigned((pp.n_gh_send + 255) / 256), 256, 0, st_>>>(pp.n_gh_send, pp.gh_send_idx, d_x, d_y,
+                                                                             d_z, d_q, d_buf);
       ++launches_;
-      off += int64_t(cnt) * d.S * 2;
     }
-  } else if (pp.n_gh_send > 0) {
-    k_pack_particles<<<unsigned((pp.n_gh_send + 255) / 256), 256, 0, st_>>>(pp.n_gh_send, pp.gh_send_idx, d_x, d_y,
-                                                                           d_z, d_q, d_buf);
-    ++launches_;
+  } else {
+    const RowXfer& x = pp.send[kind];
+    double2* buf = reinterpret_cast<double2*>(d_buf);
+    for (int l = level < 0 ? s_.top : level; l <= (level < 0 ? s_.L : level); ++l) {
+      if (x.cnt[size_t(l)] > 0) {
+        const DevLevel& d = lv_[size_t(l)];
+        dim3 grid(unsigned(x.cnt[size_t(l)]), unsigned(std::min<int64_t>((x.maxlen[size_t(l)] + 255) / 256, 64)));
+        k_pack_items<<<grid, 256, 0, st_>>>(kind == kXGather ? d.loc : d.mp, d.S, x.items[size_t(l)], buf);
+        ++launches_;
+      }
+      buf += x.len[size_t(l)];
+    }
   }
   ck(cudaGetLastError(), "pack");
 }
 
-void Engine::unpack(int kind, int peer, const double* d_buf) {
+void Engine::unpack(int kind, int peer, int level, const double* d_buf) {
   ck(cudaSetDevice(dev_), "cudaSetDevice");
   int64_t sd = 0, rd = 0;
-  exchange_sizes(kind, peer, &sd, &rd);
+  exchange_sizes(kind, peer, level, &sd, &rd);
   const PeerPlan& pp = peers_[size_t(peer)];
-  if (kind == 0) {
-    int64_t off = 0;
-    for (int l = s_.top; l <= s_.L; ++l) {
-      const int cnt = pp.mp_recv_cnt[size_t(l)];
-      if (cnt == 0) continue;
-      const DevLevel& d = lv_[size_t(l)];
-      dim3 grid(unsigned(cnt), unsigned(std::min<int64_t>((d.S + 255) / 256, 64)));
-      k_add_rows<<<grid, 256, 0, st_>>>(d.mp, pp.mp_recv_nodes[size_t(l)], d.S,
-                                        reinterpret_cast<const double2*>(d_buf + off));
+  if (kind == kXGhost) {
+    if (pp.n_gh_recv > 0) {
+      k_unpack_particles<<<unsigned((pp.n_gh_recv + 255) / 256), 256, 0, st_>>>(pp.n_gh_recv, pp.gh_recv_idx, d_buf,
+                                                                               d_x, d_y, d_z, d_q);
       ++launches_;
-      off += int64_t(cnt) * d.S * 2;
     }
-  } else if (pp.n_gh_recv > 0) {
-    k_unpack_particles<<<unsigned((pp.n_gh_recv + 255) / 256), 256, 0, st_>>>(pp.n_gh_recv, pp.gh_recv_idx, d_buf,
-                                                                             d_x, d_y, d_z, d_q);
-    ++launches_;
+  } else {
+    const RowXfer& x = pp.recv[kind];
+    const double2* buf = reinterpret_cast<const double2*>(d_buf);
+    for (int l = level < 0 ? s_.top : level; l <= (level < 0 ? s_.L : level); ++l) {
+      if (x.cnt[size_t(l)] > 0) {
+        DevLevel& d = lv_[size_t(l)];
+        dim3 grid(unsigned(x.cnt[size_t(l)]), unsigned(std::min<int64_t>((x.maxlen[size_t(l)] + 255) / 256, 64)));
+        if (kind == kXReduce)  // partial sums of the peer, added in the caller's (rank) order
+          k_unpack_items<true><<<grid, 256, 0, st_>>>(d.mp, d.S, x.items[size_t(l)], buf);
+        else
+          k_unpack_items<false><<<grid, 256, 0, st_>>>(kind == kXGather ? d.loc : d.mp, d.S, x.items[size_t(l)], buf);
+        ++launches_;
+      }
+      buf += x.len[size_t(l)];
+    }
   }
   ck(cudaGetLastError(), "unpack");
+}
+
+void Engine::run_level(int phase, int level) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  if (phase == HFMM_PHASE_M2L) {
+    if (level < s_.top || level > s_.L) throw std::out_of_range("run_level: M2L level not computed");
+    phase_m2l(level, level);
+  } else if (phase == HFMM_PHASE_L2L) {
+    if (level < s_.top || level >= s_.L) throw std::out_of_range("run_level: L2L parent level not computed");
+    phase_l2l(level, level);
+  } else {
+    throw std::invalid_argument("run_level: phase must be M2L or L2L");
+  }
+  ck(cudaGetLastError(), "run_level");
 }
 
 void Engine::set_stream(cudaStream_t st) {

@@ -69,12 +69,21 @@ struct RankLevel {
   int64_t n_children = 0;    // entries of children
 };
 
+// One direction of a row exchange (kinds 0, 2, 3 of setup.hpp) with one
+// peer: per level, device items {node, begin, length, offset} with offsets
+// in double2 from the level's start in the buffer; levels are laid out
+// level-major in the peer buffer.
+struct RowXfer {
+  std::vector<int64_t*> items;  // [level]
+  std::vector<int> cnt;         // [level]
+  std::vector<int64_t> len;     // [level] double2 elements
+  std::vector<int64_t> maxlen;  // [level] longest item (grid sizing)
+  int64_t total = 0;            // double2 elements over all levels
+};
+
 // Static exchange plan with one peer (distributed mode).
 struct PeerPlan {
-  // multipole partials: per level, the node rows sent / received
-  std::vector<int*> mp_send_nodes, mp_recv_nodes;  // [level]
-  std::vector<int> mp_send_cnt, mp_recv_cnt;       // [level]
-  int64_t mp_send = 0, mp_recv = 0;                // doubles
+  RowXfer send[4], recv[4];  // by exchange kind (index 1 = ghosts: below)
   // ghost particles (x, y, z, re, im) by sorted particle index
   int64_t* gh_send_idx = nullptr;
   int64_t* gh_recv_idx = nullptr;
@@ -102,11 +111,14 @@ class Engine {
 
   void get_expansion(int kind, int level, double* out, size_t cap_doubles);
   // Distributed mode (P > 1): exchange buffers are driven by the caller
-  // (torch.distributed over NCCL); kind 0 = multipole partials, 1 = ghosts.
-  void exchange_sizes(int kind, int peer, int64_t* send_doubles, int64_t* recv_doubles) const;
-  void exchange_begin(int kind);
-  void pack(int kind, int peer, double* d_buf);
-  void unpack(int kind, int peer, const double* d_buf);
+  // (torch.distributed over NCCL); kinds as in setup.hpp (0 M2L halo,
+  // 1 ghosts, 2 plural multipole reduce-scatter, 3 plural local gather).
+  // level -1 = all levels, laid out level-major (kinds 0, 2, 3).
+  void exchange_sizes(int kind, int peer, int level, int64_t* send_doubles, int64_t* recv_doubles) const;
+  void pack(int kind, int peer, int level, double* d_buf);
+  void unpack(int kind, int peer, int level, const double* d_buf);
+  // One level of M2L (observer level) or L2L (parent level) after the T build.
+  void run_level(int phase, int level);
   void set_stream(cudaStream_t st);
   void synchronize();
   void load_charges_device(const double* d_q_sorted);
@@ -213,8 +225,6 @@ class Engine {
   std::vector<int*> held_;                  // [level] held nodes (distributed mode)
   std::vector<int> held_cnt_;
   std::vector<PeerPlan> peers_;             // [peer]
-  std::vector<int*> halo_nodes_;            // [level]
-  std::vector<int> halo_cnt_;               // [level]
   void upload_rank_plan();
   int64_t last_launches_ = 0;
   bool timed_ = false;

@@ -203,6 +203,7 @@ constexpr int kQuadP = 32;        // particles per B-table chunk
 // ---------------------------------------------------------------------------
 // L2T (operators.cpp:89-108, driver traversal.cpp:717-728): one CTA per leaf,
 // one warp per observer, lanes over samples, warp-shuffle reduction.
+constexpr int kL2TChunk = 1024;  // samples staged per pass (40 KB of shared memory)
 __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __restrict__ leaf_start,
                                              const double* __restrict__ x, const double* __restrict__ y,
                                              const double* __restrict__ z,
@@ -211,38 +212,52 @@ __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __re
                                              const double* __restrict__ wq, int64_t S, double k,
                                              const double2* __restrict__ loc,
                                              double2* __restrict__ pot) {
-  extern __shared__ double2 sL[];
-  double* sd = reinterpret_cast<double*>(sL + S);
+  __shared__ double2 sL[kL2TChunk];
+  __shared__ double sd[3 * kL2TChunk];
   const int64_t leaf = leaf_b + blockIdx.x;
-  for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
-    const double2 v = loc[leaf * S + s];
-    const double w = wq[s];
-    sL[s] = make_double2(w * v.x, w * v.y);
-    sd[3 * s] = dir[3 * s];
-    sd[3 * s + 1] = dir[3 * s + 1];
-    sd[3 * s + 2] = dir[3 * s + 2];
-  }
-  __syncthreads();
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
-  for (int64_t p = p0 + warp; p < p1; p += nw) {
-    const double dx = x[p] - cx, dy = y[p] - cy, dz = z[p] - cz;
-    double ar = 0.0, ai = 0.0;
-    for (int64_t s = lane; s < S; s += 32) {
-      double sn, cs;
-      sincos_fast(-k * (sd[3 * s] * dx + sd[3 * s + 1] * dy + sd[3 * s + 2] * dz), &sn, &cs);
-      const double2 v = sL[s];
-      ar += v.x * cs - v.y * sn;
-      ai += v.x * sn + v.y * cs;
+  // Samples in chunks of kL2TChunk (any leaf grid); a particle stays with one
+  // warp, which adds the chunk sums in chunk order (deterministic).
+  for (int64_t sb = 0; sb < S; sb += kL2TChunk) {
+    const int ns = int(S - sb < kL2TChunk ? S - sb : kL2TChunk);
+    __syncthreads();
+    for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+      const double2 v = loc[leaf * S + sb + t];
+      const double w = wq[sb + t];
+      sL[t] = make_double2(w * v.x, w * v.y);
+      sd[3 * t] = dir[3 * (sb + t)];
+      sd[3 * t + 1] = dir[3 * (sb + t) + 1];
+      sd[3 * t + 2] = dir[3 * (sb + t) + 2];
     }
+    __syncthreads();
+    for (int64_t p = p0 + warp; p < p1; p += nw) {
+      const double dx = x[p] - cx, dy = y[p] - cy, dz = z[p] - cz;
+      double ar = 0.0, ai = 0.0;
+      for (int s = lane; s < ns; s += 32) {
+        double sn, cs;
+        sincos_fast(-k * (sd[3 * s] * dx + sd[3 * s + 1] * dy + sd[3 * s + 2] * dz), &sn, &cs);
+        const double2 v = sL[s];
+        ar += v.x * cs - v.y * sn;
+        ai += v.x * sn + v.y * cs;
+      }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      ar += __shfl_down_sync(0xffffffffu, ar, off);
-      ai += __shfl_down_sync(0xffffffffu, ai, off);
+      for (int off = 16; off > 0; off >>= 1) {
+        ar += __shfl_down_sync(0xffffffffu, ar, off);
+        ai += __shfl_down_sync(0xffffffffu, ai, off);
+      }
+      if (lane == 0) {
+        const double2 v = make_double2(-c * ai, c * ar);
+        if (sb == 0) {
+          pot[p] = v;
+        } else {
+          double2 cur = pot[p];
+          pot[p] = make_double2(cur.x + v.x, cur.y + v.y);
+        }
+      }
     }
-    if (lane == 0) pot[p] = make_double2(-c * ai, c * ar);
   }
 }
 
@@ -614,29 +629,32 @@ __global__ void k_scatter_pot(int64_t b, int64_t e, const int64_t* __restrict__ 
 
 // ---------------------------------------------------------------------------
 // Exchange packing (distributed mode): whole expansion rows and ghost particles.
-__global__ void k_pack_rows(const double2* __restrict__ src, const int* __restrict__ nodes, int64_t S,
-                            double2* __restrict__ dst) {
-  const int64_t i = blockIdx.x;
-  const int64_t node = nodes[i];
-  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.y) * blockDim.x)
-    dst[i * S + s] = src[node * S + s];
+// Row exchanges of the distributed mode (setup.hpp, RankPlan kinds 0, 2, 3):
+// item i = {node, begin, length, buffer offset} (int64, double2 units);
+// one CTA row per item, grid.y strides over its samples.
+__global__ void k_pack_items(const double2* __restrict__ src, int64_t S, const int64_t* __restrict__ items,
+                             double2* __restrict__ buf) {
+  const int64_t* it = items + 4 * int64_t(blockIdx.x);
+  const int64_t node = it[0], b = it[1], len = it[2], off = it[3];
+  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < len; s += int64_t(gridDim.y) * blockDim.x)
+    buf[off + s] = src[node * S + b + s];
 }
-__global__ void k_add_rows(double2* __restrict__ dst, const int* __restrict__ nodes, int64_t S,
-                           const double2* __restrict__ src) {
-  const int64_t i = blockIdx.x;
-  const int64_t node = nodes[i];
-  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.y) * blockDim.x) {
-    double2 a = dst[node * S + s];
-    const double2 b = src[i * S + s];
-    a.x += b.x;
-    a.y += b.y;
-    dst[node * S + s] = a;
+template <bool ADD>
+__global__ void k_unpack_items(double2* __restrict__ dst, int64_t S, const int64_t* __restrict__ items,
+                               const double2* __restrict__ buf) {
+  const int64_t* it = items + 4 * int64_t(blockIdx.x);
+  const int64_t node = it[0], b = it[1], len = it[2], off = it[3];
+  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < len; s += int64_t(gridDim.y) * blockDim.x) {
+    const double2 v = buf[off + s];
+    if (ADD) {
+      double2 a = dst[node * S + b + s];
+      a.x += v.x;
+      a.y += v.y;
+      dst[node * S + b + s] = a;
+    } else {
+      dst[node * S + b + s] = v;
+    }
   }
-}
-__global__ void k_zero_rows(double2* __restrict__ dst, const int* __restrict__ nodes, int64_t S) {
-  const int64_t node = nodes[blockIdx.x];
-  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < S; s += int64_t(gridDim.y) * blockDim.x)
-    dst[node * S + s] = make_double2(0.0, 0.0);
 }
 __global__ void k_pack_particles(int64_t n, const int64_t* __restrict__ idx, const double* __restrict__ x,
                                  const double* __restrict__ y, const double* __restrict__ z,

@@ -604,6 +604,10 @@ RankPlan build_rank_plan(const Setup& s, int r) {
   rp.child_off.assign(size_t(L + 1), {});
   rp.children.assign(size_t(L + 1), {});
   rp.halo.assign(size_t(L + 1), {});
+  for (int k = 0; k < 4; ++k) {
+    rp.send[k].assign(size_t(P), {});
+    rp.recv[k].assign(size_t(P), {});
+  }
   std::vector<std::vector<uint8_t>> is_held(size_t(L + 1));
   for (int l = s.top; l <= L; ++l) {
     const LevelData& t = s.levels[size_t(l)];
@@ -626,31 +630,43 @@ RankPlan build_rank_plan(const Setup& s, int r) {
     }
   }
   rp.child_off[size_t(L)].assign(rp.held[size_t(L)].size() + 1, 0);
-  // need[q][n]: far source n is needed by an observer rank q holds (one pass
-  // over the far lists, each observer visited once per user)
-  rp.mp_send.assign(size_t(P), {});
-  rp.mp_recv.assign(size_t(P), {});
+  // kinds 2 and 3: plural nodes r holds, against each other user's slice
   for (int l = s.top; l <= L; ++l) {
     const LevelData& t = s.levels[size_t(l)];
-    const size_t nn = t.num_nodes();
-    std::vector<std::vector<uint8_t>> need(static_cast<size_t>(P));
-    for (size_t o = 0; o < nn; ++o)
-      for (int q = t.first_user[o]; q <= t.last_user[o]; ++q) {
-        if (need[size_t(q)].empty()) need[size_t(q)].assign(nn, 0);
-        for (uint64_t f = t.far_off[o]; f < t.far_off[o + 1]; ++f) need[size_t(q)][t.far[f]] = 1;
-      }
-    for (size_t n = 0; n < nn; ++n) {
-      const bool mine = is_held[size_t(l)][n] != 0;
-      if (!need[size_t(r)].empty() && need[size_t(r)][n]) {
-        if (!mine) rp.halo[size_t(l)].push_back(int(n));
-        for (int q = t.first_user[n]; q <= t.last_user[n]; ++q)
-          if (q != r) rp.mp_recv[size_t(q)].push_back({l, int(n)});
+    for (int n : rp.held[size_t(l)]) {
+      if (!t.plural[size_t(n)]) continue;
+      const SliceRec* mine = nullptr;
+      for (uint64_t z = t.slice_off[size_t(n)]; z < t.slice_off[size_t(n) + 1]; ++z)
+        if (t.slices[z].rank == r && t.slices[z].size() > 0) mine = &t.slices[z];
+      for (uint64_t z = t.slice_off[size_t(n)]; z < t.slice_off[size_t(n) + 1]; ++z) {
+        const SliceRec& sl = t.slices[z];
+        if (sl.rank == r || sl.size() == 0) continue;
+        rp.send[kXReduce][size_t(sl.rank)].push_back({l, n, sl.begin, sl.end});  // my partial of q's rows
+        rp.recv[kXGather][size_t(sl.rank)].push_back({l, n, sl.begin, sl.end});  // q's final rows
       }
       if (mine)
-        for (int q = 0; q < P; ++q)
-          if (q != r && !need[size_t(q)].empty() && need[size_t(q)][n]) rp.mp_send[size_t(q)].push_back({l, int(n)});
+        for (int q = t.first_user[size_t(n)]; q <= t.last_user[size_t(n)]; ++q) {
+          if (q == r) continue;
+          rp.recv[kXReduce][size_t(q)].push_back({l, n, mine->begin, mine->end});
+          rp.send[kXGather][size_t(q)].push_back({l, n, mine->begin, mine->end});
+        }
     }
   }
+  // kind 0: the reference's M2L CommPlan (comm_plan.cpp:31-82), items in
+  // (level, Morton, begin) order
+  std::vector<std::vector<uint8_t>> in_halo(size_t(L + 1));
+  for (int l = s.top; l <= L; ++l) in_halo[size_t(l)].assign(s.levels[size_t(l)].num_nodes(), 0);
+  for (const PairPlanRec& pp : s.m2l_plan) {
+    if (pp.src != r && pp.dst != r) continue;
+    auto& dst = pp.src == r ? rp.send[kXHalo][size_t(pp.dst)] : rp.recv[kXHalo][size_t(pp.src)];
+    for (const PlanItemRec& it : pp.items) {
+      dst.push_back({it.level, int(it.node), it.begin, it.end});
+      if (pp.dst == r && !is_held[size_t(it.level)][it.node]) in_halo[size_t(it.level)][it.node] = 1;
+    }
+  }
+  for (int l = s.top; l <= L; ++l)
+    for (size_t i = 0; i < in_halo[size_t(l)].size(); ++i)
+      if (in_halo[size_t(l)][i]) rp.halo[size_t(l)].push_back(int(i));
   return rp;
 }
 
@@ -739,11 +755,13 @@ std::vector<unsigned char> setup_array(const Setup& s, const std::string& name) 
         if (l < s.top || l > L) throw std::out_of_range("hfmm_setup_get: level not computed");
         return size_t(l);
       };
-      auto pairs = [&](const std::vector<std::pair<int, int>>& v) {
-        std::vector<int32_t> o;
-        for (auto& [l, n] : v) {
-          o.push_back(l);
-          o.push_back(n);
+      auto rows = [&](const std::vector<RowItem>& v) {
+        std::vector<int64_t> o;
+        for (const RowItem& it : v) {
+          o.push_back(it.level);
+          o.push_back(it.node);
+          o.push_back(it.begin);
+          o.push_back(it.end);
         }
         return bytes_of(o);
       };
@@ -751,10 +769,15 @@ std::vector<unsigned char> setup_array(const Setup& s, const std::string& name) 
       if (field == "child_off") return bytes_of(rp.child_off[level_of(arg)]);
       if (field == "children") return bytes_of(rp.children[level_of(arg)]);
       if (field == "halo") return bytes_of(rp.halo[level_of(arg)]);
-      if (field == "mp_send" || field == "mp_recv") {
+      // send<k>.<q> / recv<k>.<q>: exchange kind k items with peer q, int64
+      // quadruples (level, node, begin, end)
+      if ((field.rfind("send", 0) == 0 || field.rfind("recv", 0) == 0) && field.size() == 5) {
+        const int kind = field[4] - '0';
         const int q = std::atoi(arg.c_str());
+        if (kind != kXHalo && kind != kXReduce && kind != kXGather)
+          throw std::invalid_argument("hfmm_setup_get: bad exchange kind in " + name);
         if (q < 0 || q >= s.P) throw std::out_of_range("hfmm_setup_get: bad peer");
-        return pairs(field == "mp_send" ? rp.mp_send[size_t(q)] : rp.mp_recv[size_t(q)]);
+        return rows(field[0] == 's' ? rp.send[kind][size_t(q)] : rp.recv[kind][size_t(q)]);
       }
     }
   }

@@ -97,21 +97,35 @@ struct Setup {
 
 // Per-rank evaluation plan for one process per GPU.
 // Rank r "holds" every node whose leaf range meets its Morton leaf range
-// (first_user <= r <= last_user).  The upward pass runs on held nodes only
-// and yields PARTIAL multipoles (M2M is linear, so partials of a plural node
-// sum to the full one).  One static exchange then delivers, for every far
-// source a held observer needs, the partials of the source's other users;
-// the downward pass and L2T/P2P are rank-local except for ghost particles
-// (the reference's near plan, comm_plan.cpp:84-109).
+// (first_user <= r <= last_user).  The upward pass runs on held nodes and
+// yields PARTIAL multipoles (M2M is linear); plural (shared) nodes are then
+// SLICED: every user keeps the full multipole on its own theta-row slice
+// (assign_sample_slices, tree.cpp:180-239) after a reduce-scatter among the
+// node's users.  M2L runs per observer slice and receives the missing source
+// rows through the reference's M2L CommPlan (comm_plan.cpp:31-82); the
+// downward pass gathers the plural parents' local slices among their users
+// before anterpolating.  Ghost particles follow the reference's near plan
+// (comm_plan.cpp:84-109).
+//
+// Exchange kinds (rows = flat sample ranges [begin, end) of one node):
+//   0  M2L halo: the reference CommPlan items, overwrite (per level)
+//   1  ghost particles (x, y, z, re, im)
+//   2  plural multipole reduce-scatter: partial rows of the peer's slice, add
+//   3  plural local all-gather: own slice rows to the other users, overwrite
+struct RowItem {
+  int level;
+  int node;
+  int64_t begin, end;
+};
+enum ExchangeKind { kXHalo = 0, kXGhost = 1, kXReduce = 2, kXGather = 3 };
 struct RankPlan {
   int rank = 0;
   std::vector<std::vector<int>> held;       // [level] held node indices, sorted
   std::vector<std::vector<int>> child_off;  // [level] CSR over held[level] (held children only)
   std::vector<std::vector<int>> children;   // [level] indices at level + 1
-  std::vector<std::vector<int>> halo;       // [level] needed far sources not held
-  // multipole exchange, per peer q: (level, node) items in (level, node) order
-  std::vector<std::vector<std::pair<int, int>>> mp_send;  // what r sends q
-  std::vector<std::vector<std::pair<int, int>>> mp_recv;  // what r receives from q
+  std::vector<std::vector<int>> halo;       // [level] nodes received through kind 0 that r does not hold
+  // per kind (0, 2, 3) and peer q: items r sends q / receives from q, (level, node, begin) order
+  std::vector<std::vector<RowItem>> send[4], recv[4];
 };
 RankPlan build_rank_plan(const struct Setup& s, int r);
 

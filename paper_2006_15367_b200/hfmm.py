@@ -44,6 +44,7 @@ class Phase(enum.IntEnum):
     L2T = 5
     Near = 6
     NearStart = 7
+    TBuild = 8
 
 
 @dataclass
@@ -230,21 +231,23 @@ class RankEngine:
     def run_phase(self, phase: int) -> None:
         check(lib().hfmm_gpu_run_phase(self._h, int(phase)))
 
-    def exchange_sizes(self, kind: int, peer: int) -> tuple[int, int]:
+    def run_level(self, phase: int, level: int) -> None:
+        """One level of M2L (observer level) or L2L (parent level)."""
+        check(lib().hfmm_gpu_run_level(self._h, int(phase), int(level)))
+
+    def exchange_sizes(self, kind: int, peer: int, level: int = -1) -> tuple[int, int]:
+        """(send, recv) doubles of exchange `kind` with `peer` (level -1: all levels)."""
         s = ctypes.c_int64()
         r = ctypes.c_int64()
-        check(lib().hfmm_gpu_exchange_sizes(self._h, kind, peer, ctypes.byref(s), ctypes.byref(r)))
+        check(lib().hfmm_gpu_exchange_sizes(self._h, kind, peer, level, ctypes.byref(s), ctypes.byref(r)))
         return s.value, r.value
 
-    def exchange_begin(self, kind: int) -> None:
-        check(lib().hfmm_gpu_exchange_begin(self._h, kind))
-
-    def pack(self, kind: int, peer: int, buf) -> None:
+    def pack(self, kind: int, peer: int, buf, level: int = -1) -> None:
         """Packs this rank's outgoing data for `peer` into a device tensor (float64)."""
-        check(lib().hfmm_gpu_pack(self._h, kind, peer, ctypes.c_void_p(buf.data_ptr())))
+        check(lib().hfmm_gpu_pack(self._h, kind, peer, level, ctypes.c_void_p(buf.data_ptr())))
 
-    def unpack(self, kind: int, peer: int, buf) -> None:
-        check(lib().hfmm_gpu_unpack(self._h, kind, peer, ctypes.c_void_p(buf.data_ptr())))
+    def unpack(self, kind: int, peer: int, buf, level: int = -1) -> None:
+        check(lib().hfmm_gpu_unpack(self._h, kind, peer, level, ctypes.c_void_p(buf.data_ptr())))
 
     def set_stream(self, stream_ptr: int) -> None:
         check(lib().hfmm_gpu_set_stream(self._h, ctypes.c_void_p(stream_ptr)))

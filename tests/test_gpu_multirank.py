@@ -1,7 +1,8 @@
 """Distributed-mode device code on ONE GPU: all P ranks' engines run in one
-process, one after another (no kernel ever waits on another rank), and the
-exchange buffers move by device copies in the same order the NCCL driver
-uses.  Potentials must match the reference within 1e-10."""
+process, stage by stage through the same schedule as the NCCL driver (no
+kernel ever waits on another rank): ghosts, plural multipole reduce-scatter,
+sliced M2L halo (the reference CommPlan), plural local gather.  Potentials
+must match the reference within 1e-10."""
 import os
 
 import numpy as np
@@ -14,40 +15,14 @@ pytestmark = pytest.mark.gpu
 
 
 def _run_ranks(hb, setup, q, engs):
-    P = setup.num_ranks
+    """One evaluation of all P rank engines through the distributed schedule
+    (paper_2006_15367_b200.distributed.run_emulated); returns the assembled
+    sorted-order potentials."""
+    from paper_2006_15367_b200.distributed import run_emulated
     for e in engs:
         e.set_intensities(q)
-
-    def exchange(kind):
-        if kind == 0:
-            for e in engs:
-                e.exchange_begin(0)
-        bufs = {}
-        for r, e in enumerate(engs):
-            for p in range(P):
-                if p == r:
-                    continue
-                s, _ = e.exchange_sizes(kind, p)
-                if s:
-                    bufs[r, p] = torch.empty(s, dtype=torch.float64, device="cuda")
-                    e.pack(kind, p, bufs[r, p])
-            e.synchronize()
-        for p, e in enumerate(engs):
-            for r in range(P):  # senders in rank order
-                if (r, p) in bufs:
-                    assert e.exchange_sizes(kind, r)[1] == bufs[r, p].numel()
-                    e.unpack(kind, r, bufs[r, p])
-            e.synchronize()
-
-    exchange(1)
+    run_emulated(engs, lambda n: torch.empty(int(n), dtype=torch.float64, device="cuda"))
     for e in engs:
-        e.run_phase(hb.Phase.C2M)
-        e.run_phase(hb.Phase.M2M)
-        e.synchronize()
-    exchange(0)
-    for e in engs:
-        for ph in (hb.Phase.M2L, hb.Phase.L2L, hb.Phase.L2T, hb.Phase.Near):
-            e.run_phase(ph)
         e.synchronize()
     pot = np.full(setup.n, np.nan, complex)
     dev = torch.full((setup.n, 2), float("nan"), dtype=torch.float64, device="cuda")
@@ -66,6 +41,7 @@ def _run_ranks(hb, setup, q, engs):
     (3, ("sphere", 40_000, 2.0, 62, 4.0), 0),
     (4, ("cube", 20_000, 2.5, 63, 6.0), 0),
     (4, ("sphere", 40_000, 2.0, 62, 4.0), 1),  # near-pair-weighted partition (opt-in)
+    (8, ("cube", 60_000, 4.0, 64, 3.0), 0),
 ])
 def test_ranks_emulated_on_one_gpu(ranks, case, pw, native, refo):
     import paper_2006_15367_b200 as hb

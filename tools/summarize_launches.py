@@ -1,7 +1,7 @@
 """Per-kernel table (per evaluation) from an ncu launch list of bench.py, plus
 the per-phase DRAM traffic used by bench.py's roofline.traffic.
 
-usage: python tools/summarize_launches.py gpurun_out/bench_launches.csv profiles/<name>.txt
+usage: python tools/summarize_launches.py gpurun_out/bench_launches.csv profiles/<name>.txt [cfgN]
 """
 import collections
 import csv
@@ -9,6 +9,7 @@ import json
 import sys
 
 src, out = sys.argv[1], sys.argv[2]
+cfg = sys.argv[3] if len(sys.argv) > 3 else "cfg4"
 rows = list(csv.reader(open(src)))
 hdr, k = None, collections.OrderedDict()
 for r in rows:
@@ -29,7 +30,7 @@ for x in ks:
     a[2] += x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0)
 tot = sum(v[1] for v in agg.values()) / n_eval
 lines = ["# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none",
-         f"#   python bench.py --steps 2 --warmup 3 --no-cpu-baseline   (cfg2; {len(ks)} launches = {n_eval} evaluations)",
+         f"#   python bench.py --config {cfg} --steps 2 --warmup 3 --no-cpu-baseline   ({len(ks)} launches = {n_eval} evaluations)",
          "# per-evaluation averages; ncu serialises launches (cold caches), so compare shares, not absolutes",
          f"{'kernel':34s} {'grid':16s} {'ms/eval':>8s} {'share':>6s} {'GB/eval':>8s} {'GB/s':>7s}"]
 for (nm, gr), (c, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -41,5 +42,10 @@ print("\n".join(lines[:24]))
 traffic = {}
 for key, pre in (("M2L", "k_m2l"), ("M2M", "k_m2m"), ("L2L", "k_l2l")):
     traffic[key] = sum(b for (nm, gr), (c, t, b) in agg.items() if nm.split("::")[-1].startswith(pre)) / n_eval
-traffic["_note"] = f"DRAM bytes (read+write) per evaluation summed over the phase's launches, cfg2, from {out}"
-json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
+traffic["_note"] = f"DRAM bytes (read+write) per evaluation summed over the phase's launches, {cfg}, from {out}"
+try:
+    allt = json.load(open("profiles/ncu_traffic.json"))
+except (OSError, ValueError):
+    allt = {}
+allt[cfg] = traffic
+json.dump(allt, open("profiles/ncu_traffic.json", "w"), indent=1)
