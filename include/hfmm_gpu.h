@@ -97,6 +97,24 @@ void hfmm_setup_destroy(hfmm_setup* s);
 hfmm_status hfmm_setup_get(const hfmm_setup* s, const char* name, void* dst,
                            size_t cap, size_t* nbytes);
 
+/* Import of an EXISTING setup (the caller's GlobalSetup, traversal.hpp:93-118)
+ * without re-running build_setup: put every array under the names and
+ * layouts hfmm_setup_get() returns ("meta_i64", "meta_f64", "particles",
+ * "original_index", "leaf_codes", "leaf_start", "rank_ranges", "splitters",
+ * "near_off", "near", "m2l_plan", "near_plan" and per computed level l
+ * "L<l>.sampling|theta_weight|phi_weight|codes|centers|users|slices_off|
+ * slices|child_off|children|interp_off|interp|far_off|far"), then end.
+ * end validates sizes, offsets and indices (HFMM_ERR_INVALID_ARGUMENT /
+ * HFMM_ERR_OUT_OF_RANGE) and always consumes the import handle.  A setup
+ * imported from the reference's build_setup equals hfmm_setup_build's byte
+ * for byte (tests/test_setup_import.py, oracle/adapter). */
+typedef struct hfmm_setup_import hfmm_setup_import;
+hfmm_status hfmm_setup_import_begin(const hfmm_run_config* cfg, hfmm_setup_import** out);
+hfmm_status hfmm_setup_import_put(hfmm_setup_import* im, const char* name, const void* data,
+                                  size_t nbytes);
+hfmm_status hfmm_setup_import_end(hfmm_setup_import* im, hfmm_setup** out);
+void hfmm_setup_import_abort(hfmm_setup_import* im);
+
 /* ---------------- device engine (one logical rank per GPU) ---------------- */
 
 typedef struct hfmm_gpu hfmm_gpu;
@@ -222,6 +240,36 @@ hfmm_status hfmm_gpu_launch_count(hfmm_gpu* g, int64_t* launches);
  * far-field chain.  Off: strictly sequential phases, so hfmm_gpu_last_timing
  * reports each phase's own kernel time.  Results are identical either way. */
 hfmm_status hfmm_gpu_set_overlap(hfmm_gpu* g, int on);
+
+/* ---------------- world: every logical rank in one process ----------------
+ * The counterpart of the reference's run_world + evaluate_with_setup
+ * (runtime.cpp:274-290, traversal.cpp:790-817), which simulate all MPI ranks
+ * in one process: one engine per logical rank of the setup's partition, rank
+ * r on devices[r % ndev], the exchanges of the distributed schedule done by
+ * device (peer) copies inside the library.  Works for any num_ranks >= 1. */
+typedef struct hfmm_world hfmm_world;
+hfmm_status hfmm_world_create(const hfmm_setup* s, const int* devices, int ndev, hfmm_world** out);
+void hfmm_world_destroy(hfmm_world* w);
+/* Input-order charges (n*2) to every rank. */
+hfmm_status hfmm_world_set_charges(hfmm_world* w, const double* charges);
+/* One reference RankEngine phase on every rank (traversal.hpp:129-140), with
+ * the exchanges it owns: HFMM_PHASE_C2M, _M2M (+ plural reduce-scatter),
+ * _M2L (T build + sliced halo per level), _L2L (plural gather per level),
+ * _L2T (= l2o_near_phase: ghosts, L2T, near field). */
+hfmm_status hfmm_world_run_phase(hfmm_world* w, int phase);
+/* Full evaluation (charges may be NULL: keep); potentials in input order
+ * (n*2).  rank_ms (may be NULL) receives num_ranks * 7 device milliseconds in
+ * the reference ledger's phase order (ledger.hpp: Setup = T build, C2M, M2M,
+ * M2L, L2L, L2O, Near). */
+hfmm_status hfmm_world_evaluate(hfmm_world* w, const double* charges, double* pot_out,
+                                double* rank_ms);
+/* Potentials of all ranks in input order after hfmm_world_run_phase(L2T). */
+hfmm_status hfmm_world_potentials(hfmm_world* w, double* pot_out);
+/* Expansions of `level` as held by `rank` (n_nodes * S complex); the rows of
+ * the rank's own slice of every node it holds are valid (RankEngine::multipole /
+ * local_expansion, traversal.hpp:142-143). */
+hfmm_status hfmm_world_get_expansion(hfmm_world* w, int rank, int kind, int level, double* out,
+                                     size_t cap_doubles);
 
 /* One-shot: build_setup + evaluate on one device (evaluate_potential,
  * traversal.cpp:819-823).  Requires cfg->num_ranks == 1. */

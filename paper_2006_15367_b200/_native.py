@@ -87,6 +87,17 @@ _SIG = {
     "hfmm_setup_build": (ctypes.c_int, [_P, _P, ctypes.c_size_t, ctypes.POINTER(RunConfigC),
                                         ctypes.POINTER(_P)]),
     "hfmm_setup_destroy": (None, [_P]),
+    "hfmm_setup_import_begin": (ctypes.c_int, [ctypes.POINTER(RunConfigC), ctypes.POINTER(_P)]),
+    "hfmm_setup_import_put": (ctypes.c_int, [_P, ctypes.c_char_p, _P, ctypes.c_size_t]),
+    "hfmm_setup_import_end": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "hfmm_setup_import_abort": (None, [_P]),
+    "hfmm_world_create": (ctypes.c_int, [_P, _P, ctypes.c_int, ctypes.POINTER(_P)]),
+    "hfmm_world_destroy": (None, [_P]),
+    "hfmm_world_set_charges": (ctypes.c_int, [_P, _P]),
+    "hfmm_world_run_phase": (ctypes.c_int, [_P, ctypes.c_int]),
+    "hfmm_world_evaluate": (ctypes.c_int, [_P, _P, _P, _P]),
+    "hfmm_world_potentials": (ctypes.c_int, [_P, _P]),
+    "hfmm_world_get_expansion": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t]),
     "hfmm_setup_get": (ctypes.c_int, [_P, ctypes.c_char_p, _P, ctypes.c_size_t,
                                       ctypes.POINTER(ctypes.c_size_t)]),
     "hfmm_gpu_create": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),

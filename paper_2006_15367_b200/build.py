@@ -18,7 +18,7 @@ OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libhfmm_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["setup.cpp", "setup_gpu.cu", "engine.cu", "capi.cu"]
+SOURCES = ["setup.cpp", "setup_import.cpp", "setup_gpu.cu", "engine.cu", "world.cu", "capi.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h")))
 
 

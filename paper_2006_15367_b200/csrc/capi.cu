@@ -13,6 +13,7 @@
 #include "inputs.hpp"
 #include "interp.hpp"
 #include "setup.hpp"
+#include "world.hpp"
 
 struct hfmm_setup {
   // shared with every engine created from it (hfmm_gpu_create)
@@ -21,6 +22,9 @@ struct hfmm_setup {
 };
 struct hfmm_gpu {
   std::unique_ptr<hfmm_b200::Engine> eng;
+};
+struct hfmm_world {
+  std::unique_ptr<hfmm_b200::World> w;
 };
 
 namespace {
@@ -115,6 +119,42 @@ hfmm_status hfmm_setup_get(const hfmm_setup* s, const char* name, void* dst, siz
     if (nbytes) *nbytes = v.size();
     if (dst && cap) std::memcpy(dst, v.data(), std::min(cap, v.size()));
   });
+}
+
+hfmm_status hfmm_setup_import_begin(const hfmm_run_config* cfg, hfmm_setup_import** out) {
+  return guard([&] {
+    need(cfg, "hfmm_setup_import_begin(cfg)");
+    need(out, "hfmm_setup_import_begin(out)");
+    if (!(cfg->lambda > 0) || !(cfg->digits > 0) || !(cfg->leaf_lambda > 0) || cfg->num_ranks < 1 ||
+        cfg->buffer_limit == 0 || cfg->top_level < 1)
+      throw std::invalid_argument("RunConfig: invalid fields");
+    *out = reinterpret_cast<hfmm_setup_import*>(hfmm_b200::setup_import_begin(*cfg));
+  });
+}
+
+hfmm_status hfmm_setup_import_put(hfmm_setup_import* im, const char* name, const void* data, size_t nbytes) {
+  return guard([&] {
+    need(im, "hfmm_setup_import_put(import)");
+    need(name, "hfmm_setup_import_put(name)");
+    hfmm_b200::setup_import_put(reinterpret_cast<hfmm_b200::SetupImport*>(im), name, data, nbytes);
+  });
+}
+
+hfmm_status hfmm_setup_import_end(hfmm_setup_import* im, hfmm_setup** out) {
+  auto* p = reinterpret_cast<hfmm_b200::SetupImport*>(im);
+  hfmm_status st = guard([&] {
+    need(im, "hfmm_setup_import_end(import)");
+    need(out, "hfmm_setup_import_end(out)");
+    auto h = std::make_unique<hfmm_setup>();
+    h->s = hfmm_b200::setup_import_end(p);
+    *out = h.release();
+  });
+  if (p) hfmm_b200::setup_import_abort(p);
+  return st;
+}
+
+void hfmm_setup_import_abort(hfmm_setup_import* im) {
+  if (im) hfmm_b200::setup_import_abort(reinterpret_cast<hfmm_b200::SetupImport*>(im));
 }
 
 hfmm_status hfmm_gpu_create(const hfmm_setup* s, int device, int rank, hfmm_gpu** out) {
@@ -271,6 +311,70 @@ hfmm_status hfmm_gpu_launch_count(hfmm_gpu* g, int64_t* n) {
     need(g, "hfmm_gpu_launch_count(gpu)");
     need(n, "hfmm_gpu_launch_count(out)");
     *n = g->eng->launch_count();
+  });
+}
+
+hfmm_status hfmm_world_create(const hfmm_setup* s, const int* devices, int ndev, hfmm_world** out) {
+  return guard([&] {
+    need(s, "hfmm_world_create(setup)");
+    need(out, "hfmm_world_create(out)");
+    std::vector<int> devs;
+    if (devices && ndev > 0)
+      devs.assign(devices, devices + ndev);
+    else
+      devs.push_back(0);
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw std::runtime_error("no CUDA device available (the engine has no CPU fallback)");
+    for (int d : devs)
+      if (d < 0 || d >= count) throw std::invalid_argument("hfmm_world_create: bad device");
+    auto w = std::make_unique<hfmm_world>();
+    w->w = std::make_unique<hfmm_b200::World>(s->sp, devs);
+    *out = w.release();
+  });
+}
+
+void hfmm_world_destroy(hfmm_world* w) { delete w; }
+
+hfmm_status hfmm_world_set_charges(hfmm_world* w, const double* charges) {
+  return guard([&] {
+    need(w, "hfmm_world_set_charges(world)");
+    need(charges, "hfmm_world_set_charges(charges)");
+    w->w->set_charges(charges);
+  });
+}
+
+hfmm_status hfmm_world_run_phase(hfmm_world* w, int phase) {
+  return guard([&] {
+    need(w, "hfmm_world_run_phase(world)");
+    w->w->run_phase(phase);
+  });
+}
+
+hfmm_status hfmm_world_evaluate(hfmm_world* w, const double* charges, double* pot_out, double* rank_ms) {
+  return guard([&] {
+    need(w, "hfmm_world_evaluate(world)");
+    need(pot_out, "hfmm_world_evaluate(pot_out)");
+    w->w->evaluate(charges, pot_out);
+    if (rank_ms)
+      for (int r = 0; r < w->w->ranks(); ++r) w->w->rank_ms(r, rank_ms + size_t(r) * hfmm_b200::kLedgerPhases);
+  });
+}
+
+hfmm_status hfmm_world_potentials(hfmm_world* w, double* pot_out) {
+  return guard([&] {
+    need(w, "hfmm_world_potentials(world)");
+    need(pot_out, "hfmm_world_potentials(pot_out)");
+    w->w->potentials(pot_out);
+  });
+}
+
+hfmm_status hfmm_world_get_expansion(hfmm_world* w, int rank, int kind, int level, double* out, size_t cap) {
+  return guard([&] {
+    need(w, "hfmm_world_get_expansion(world)");
+    need(out, "hfmm_world_get_expansion(out)");
+    if (rank < 0 || rank >= w->w->ranks()) throw std::out_of_range("hfmm_world_get_expansion: bad rank");
+    w->w->engine(rank).get_expansion(kind, level, out, cap);
   });
 }
 

@@ -1041,6 +1041,15 @@ void Engine::get_potentials_sorted(double* out, size_t cap) {
 }
 
 
+void Engine::store_potentials_host(double* host_sorted) {
+  ck(cudaSetDevice(dev_), "cudaSetDevice");
+  ck(cudaStreamSynchronize(st_), "sync");
+  if (part_e_ > part_b_)
+    ck(cudaMemcpy(host_sorted + 2 * part_b_, d_pot + part_b_, size_t(part_e_ - part_b_) * sizeof(double2),
+                  cudaMemcpyDeviceToHost),
+       "D2H pot");
+}
+
 void Engine::upload_rank_plan() {
   const Setup& s = s_;
   const int L = s.L, P = s.P;

@@ -128,6 +128,11 @@ class Engine {
   int64_t particle_begin() const { return part_b_; }
   int64_t particle_end() const { return part_e_; }
   void get_potentials_sorted(double* out, size_t cap_doubles);
+  // This rank's particle range of the sorted potentials into a host array of
+  // n*2 doubles (same offsets; synchronous).
+  void store_potentials_host(double* host_sorted);
+  cudaStream_t stream() const { return st_; }
+  int device() const { return dev_; }
   int64_t launches() const { return launches_; }
   // Per-phase ms of the last evaluation (events on its stream), [0] T build .. [7] total.
   void last_timing(double* ms, int64_t* launches);

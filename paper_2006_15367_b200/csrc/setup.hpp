@@ -139,6 +139,14 @@ void device_keys_sort(const double* xyz, const double* q, size_t n, const double
                       std::vector<uint64_t>& order, std::vector<double>& xyz_s, std::vector<double>& q_s);
 void device_lists(Setup& s);
 
+// Import of an existing setup from the named flat arrays of setup_array()
+// (setup_import.cpp): begin, put every array, end (validates; consumes).
+struct SetupImport;
+SetupImport* setup_import_begin(const hfmm_run_config& cfg);
+void setup_import_put(SetupImport* im, const std::string& name, const void* data, size_t nbytes);
+Setup setup_import_end(SetupImport* im);
+void setup_import_abort(SetupImport* im);
+
 // Flat dump under the names used by oracle/ref_driver.cpp.
 std::vector<unsigned char> setup_array(const Setup& s, const std::string& name);
 

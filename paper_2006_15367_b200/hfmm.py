@@ -294,17 +294,94 @@ class RankEngine:
         self.close()
 
 
-def evaluate_with_setup(setup: GlobalSetup, device: int = 0) -> EvalResult:
-    """hfmm::evaluate_with_setup on one B200 (num_ranks must be 1; the
-    distributed runner in :mod:`paper_2006_15367_b200.distributed` drives N>1)."""
-    if setup.num_ranks != 1:
-        raise _native.InvalidArgument(
-            "evaluate_with_setup: num_ranks > 1 runs one process per GPU (see distributed.py)")
-    eng = RankEngine(setup, 0, device)
+LEDGER_PHASES = ("Setup", "C2M", "M2M", "M2L", "L2L", "L2O", "Near")  # ledger.hpp
+
+
+class World:
+    """Every logical rank of the setup's partition in this process (the
+    reference's run_world + evaluate_with_setup, runtime.cpp:274-290,
+    traversal.cpp:790-817): rank r on devices[r % len(devices)], exchanges by
+    device (peer) copies inside the native library."""
+
+    def __init__(self, setup: GlobalSetup, devices=(0,)):
+        self.setup = setup  # keeps the host setup alive
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        check(lib().hfmm_world_create(setup._h, devs, len(devices), ctypes.byref(h)))
+        self._h = h
+
+    def set_intensities(self, intensities) -> None:
+        _, q = _as_particles(np.zeros((self.setup.n, 3)), intensities)
+        check(lib().hfmm_world_set_charges(self._h, ptr(q)))
+
+    def run_phase(self, phase: int) -> None:
+        """One reference RankEngine phase on every rank (C2M, M2M, M2L, L2L,
+        L2T = l2o_near_phase), with the exchanges it owns."""
+        check(lib().hfmm_world_run_phase(self._h, int(phase)))
+
+    def evaluate(self, intensities=None) -> EvalResult:
+        q = None
+        if intensities is not None:
+            _, q = _as_particles(np.zeros((self.setup.n, 3)), intensities)
+        out = np.zeros((self.setup.n, 2))
+        ms = np.zeros((self.setup.num_ranks, len(LEDGER_PHASES)))
+        check(lib().hfmm_world_evaluate(self._h, ptr(q), ptr(out), ptr(ms)))
+        res = EvalResult(out[:, 0] + 1j * out[:, 1],
+                         {k: float(v) for k, v in zip(LEDGER_PHASES, ms.max(axis=0))})
+        res.rank_ms = ms
+        return res
+
+    def potentials(self) -> np.ndarray:
+        out = np.zeros((self.setup.n, 2))
+        check(lib().hfmm_world_potentials(self._h, ptr(out)))
+        return out[:, 0] + 1j * out[:, 1]
+
+    def expansion(self, rank: int, kind: int, level: int) -> np.ndarray:
+        """(n_nodes, S) expansions as held by `rank` (its slice rows valid)."""
+        _, nt, nphi = self.setup.sampling(level)
+        out = np.empty((self.setup.num_nodes(level), nt * nphi, 2))
+        check(lib().hfmm_world_get_expansion(self._h, rank, kind, level, ptr(out), out.size))
+        return out[..., 0] + 1j * out[..., 1]
+
+    def assembled(self, kind: int, level: int) -> np.ndarray:
+        """Every node's expansion assembled from its users' slices, as the
+        reference's RankEngine::multipole / local_expansion expose them."""
+        so = self.setup.array(f"L{level}.slices_off", np.uint64).astype(np.int64)
+        sl = self.setup.array(f"L{level}.slices", np.int64).reshape(-1, 3)
+        per = [self.expansion(r, kind, level) for r in range(self.setup.num_ranks)]
+        out = np.zeros_like(per[0])
+        for n in range(out.shape[0]):
+            for z in range(so[n], so[n + 1]):
+                r, b, e = (int(v) for v in sl[z])
+                out[n, b:e] = per[r][n, b:e]
+        return out
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _native._lib is not None:
+            _native._lib.hfmm_world_destroy(h)
+
+    def __del__(self):
+        self.close()
+
+
+def evaluate_with_setup(setup: GlobalSetup, device: int = 0, devices=None) -> EvalResult:
+    """hfmm::evaluate_with_setup (traversal.cpp:790-817).  One logical rank
+    runs as a single engine on `device`; num_ranks > 1 runs every rank in this
+    process (:class:`World`, ranks round-robin over `devices`, default
+    [device]) -- the reference's own in-process simulation of its ranks.  The
+    one-process-per-GPU NCCL runner is :mod:`paper_2006_15367_b200.distributed`."""
+    if setup.num_ranks == 1:
+        eng = RankEngine(setup, 0, device)
+        try:
+            return eng.evaluate()
+        finally:
+            eng.close()
+    w = World(setup, list(devices) if devices else [device])
     try:
-        return eng.evaluate()
+        return w.evaluate()
     finally:
-        eng.close()
+        w.close()
 
 
 def evaluate_potential(positions, intensities, config: RunConfig | None = None,

@@ -94,7 +94,7 @@ def run(name: str, eval_ranks: int) -> None:
     te = time.time()
     pot, sec, fl = rs.evaluate()
     out["eval_wall_s"] = time.time() - te
-    out["phase_sec_max_rank"] = dict(zip(["c2m", "m2m", "m2l", "l2l", "l2o", "near", "build"], sec.tolist()))
+    out["phase_sec_max_rank"] = dict(zip(["setup", "c2m", "m2m", "m2l", "l2l", "l2o", "near"], sec.tolist()))
     out["phase_flops"] = fl.tolist()
     out["targets_per_s"] = n / out["eval_wall_s"]
     print(f"[{name}] evaluate {out['eval_wall_s']:.1f}s", flush=True)
