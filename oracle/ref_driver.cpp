@@ -32,6 +32,7 @@
 #include "hfmm/traversal.hpp"
 #include "hfmm_gpu.h"
 #include "inputs.hpp"
+#include "adapter/setup_flat.hpp"
 
 using namespace hfmm;
 
@@ -110,121 +111,7 @@ struct RefSetup {
 };
 
 void make_dump(RefSetup& h) {
-  const GlobalSetup& s = h.s;
-  Dump& d = h.dump;
-  const int L = s.tree.levels;
-  const int P = s.partition.num_ranks;
-  d.put("meta_i64", std::vector<int64_t>{L, s.top_level, s.d_class,
-                                         int64_t(s.particles.size()),
-                                         int64_t(s.leaves.size()), P});
-  d.put("meta_f64", std::vector<double>{s.tree.root_side, s.tree.leaf_side,
-                                        s.tree.root_corner.x, s.tree.root_corner.y,
-                                        s.tree.root_corner.z, s.k.k});
-  std::vector<double> parts;
-  parts.reserve(s.particles.size() * 5);
-  for (const Particle& p : s.particles) {
-    parts.push_back(p.position.x);
-    parts.push_back(p.position.y);
-    parts.push_back(p.position.z);
-    parts.push_back(p.intensity.real());
-    parts.push_back(p.intensity.imag());
-  }
-  d.put("particles", parts);
-  std::vector<uint64_t> oi(s.original_index.begin(), s.original_index.end());
-  d.put("original_index", oi);
-  std::vector<uint64_t> lc, ls;
-  for (const MortonKey& k : s.leaves) lc.push_back(k.code);
-  for (auto& [b, e] : s.leaf_particles) ls.push_back(b);
-  ls.push_back(s.leaf_particles.empty() ? 0 : s.leaf_particles.back().second);
-  d.put("leaf_codes", lc);
-  d.put("leaf_start", ls);
-  std::vector<uint64_t> rr, sp;
-  for (auto& [b, e] : s.partition.rank_ranges) {
-    rr.push_back(b);
-    rr.push_back(e);
-  }
-  for (const MortonKey& k : s.partition.splitters) sp.push_back(k.packed());
-  d.put("rank_ranges", rr);
-  d.put("splitters", sp);
-
-  for (int l = s.top_level; l <= L; ++l) {
-    std::string p = "L" + std::to_string(l) + ".";
-    const LevelSampling& sm = s.samplings[l];
-    d.put(p + "sampling", std::vector<int64_t>{sm.trunc_order, int64_t(sm.n_theta),
-                                               int64_t(sm.n_phi)});
-    d.put(p + "theta_weight", s.quads[l].theta_weight);
-    d.put(p + "phi_weight", std::vector<double>{s.quads[l].phi_weight});
-    const LevelTable& t = s.levels[l];
-    std::vector<uint64_t> codes, soff{0}, coff{0}, ioff{0}, foff{0}, children, interp, far;
-    std::vector<double> centers;
-    std::vector<int64_t> users, slices;
-    for (const NodeInfo& n : t.nodes) {
-      codes.push_back(n.key.code);
-      centers.push_back(n.center.x);
-      centers.push_back(n.center.y);
-      centers.push_back(n.center.z);
-      users.push_back(n.first_user);
-      users.push_back(n.last_user);
-      users.push_back(n.plural ? 1 : 0);
-      for (const Slice& sl : n.slices) {
-        slices.push_back(sl.rank);
-        slices.push_back(int64_t(sl.begin));
-        slices.push_back(int64_t(sl.end));
-      }
-      soff.push_back(slices.size() / 3);
-      for (size_t c : n.children) children.push_back(c);
-      coff.push_back(children.size());
-      if (!n.interp_layout.splits.empty()) {
-        interp.push_back(n.interp_layout.n_theta);
-        interp.push_back(n.interp_layout.n_phi);
-        for (size_t v : n.interp_layout.splits) interp.push_back(v);
-      }
-      ioff.push_back(interp.size());
-      auto it = s.lists.far.find(n.key.packed());
-      if (it != s.lists.far.end())
-        for (const MortonKey& k : it->second) far.push_back(k.code);
-      foff.push_back(far.size());
-    }
-    d.put(p + "codes", codes);
-    d.put(p + "centers", centers);
-    d.put(p + "users", users);
-    d.put(p + "slices_off", soff);
-    d.put(p + "slices", slices);
-    d.put(p + "child_off", coff);
-    d.put(p + "children", children);
-    d.put(p + "interp_off", ioff);
-    d.put(p + "interp", interp);
-    d.put(p + "far_off", foff);
-    d.put(p + "far", far);
-  }
-  std::vector<uint64_t> noff{0}, near;
-  for (const MortonKey& k : s.leaves) {
-    for (const MortonKey& nk : s.lists.near.at(k.packed())) near.push_back(nk.code);
-    noff.push_back(near.size());
-  }
-  d.put("near_off", noff);
-  d.put("near", near);
-  std::vector<int64_t> plan;
-  for (const PairPlan& pp : s.m2l_plan.pairs) {
-    plan.push_back(pp.src);
-    plan.push_back(pp.dst);
-    plan.push_back(int64_t(pp.items.size()));
-    for (const PlanItem& it : pp.items) {
-      plan.push_back(it.node.level);
-      plan.push_back(int64_t(it.node.code));
-      plan.push_back(int64_t(it.begin));
-      plan.push_back(int64_t(it.end));
-    }
-  }
-  d.put("m2l_plan", plan);
-  std::vector<int64_t> np;
-  for (int q = 0; q < P; ++q)
-    for (int w = 0; w < P; ++w) {
-      const auto& lst = s.near_plan.send_leaves[q][w];
-      np.push_back(int64_t(lst.size()));
-      for (size_t li : lst) np.push_back(int64_t(li));
-    }
-  d.put("near_plan", np);
+  flatten_setup(h.s, [&](const std::string& name, const auto& v) { h.dump.put(name, v); });
 }
 
 }  // namespace

@@ -699,6 +699,7 @@ void Engine::phase_l2t() {
       // (n / 2 <= kQuadHalfMax keeps the table under 48 KB: no attribute needed)
       auto l2t_quads = [&](unsigned grid, int64_t lb, int64_t cnt, const int* list) {
         const int hn = int(d.nt / 2);
+        if (std::getenv("HFMM_L2T_V2")) {  // (temporary A/B: the previous small-leaf kernel)
 #define HFMM_L2TQ(HN)                                                                                          \
   do {                                                                                                          \
     if (d_ltab_)                                                                                                \
@@ -708,11 +709,43 @@ void Engine::phase_l2t() {
       k_l2t_quad2<HN, false><<<grid, 128, smem, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers,     \
                                                        d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);                  \
   } while (0)
-        if (hn == 9) HFMM_L2TQ(9);
-        else if (hn == 11) HFMM_L2TQ(11);
-        else if (hn == 13) HFMM_L2TQ(13);
-        else HFMM_L2TQ(0);
+          if (hn == 9) HFMM_L2TQ(9);
+          else if (hn == 11) HFMM_L2TQ(11);
+          else if (hn == 13) HFMM_L2TQ(13);
+          else HFMM_L2TQ(0);
 #undef HFMM_L2TQ
+          return;
+        }
+        // quads per lane: fewest lane slots (chunks x R), ties to fewer chunks; R <= 4
+        const int quads = hn * hn;
+        int r = 1, best = INT32_MAX;
+        for (int rr = 1; rr <= 4; ++rr) {
+          const int cost = (quads + 32 * rr - 1) / (32 * rr) * rr;
+          if (cost <= best) {
+            best = cost;
+            r = rr;
+          }
+        }
+#define HFMM_L2T3(RR, HN)                                                                                        \
+  do {                                                                                                            \
+    if (d_ltab_)                                                                                                  \
+      k_l2t_quad3<RR, HN, true><<<grid, 128, 0, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, \
+                                                       d.wq, d.nt, s_.k, d.loc, d_pot, d_ltab_, ltab_half_);        \
+    else                                                                                                          \
+      k_l2t_quad3<RR, HN, false><<<grid, 128, 0, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers,      \
+                                                        d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);                     \
+  } while (0)
+        if (r == 3 && hn == 9) HFMM_L2T3(3, 9);        // n = 18 (configs 1, 3, 4)
+        else if (r == 4 && hn == 11) HFMM_L2T3(4, 11);  // n = 22 (config 5)
+        else if (r == 3 && hn == 13) HFMM_L2T3(3, 13);  // n = 26 (config 2)
+        else
+          switch (r) {
+            case 1: HFMM_L2T3(1, 0); break;
+            case 2: HFMM_L2T3(2, 0); break;
+            case 3: HFMM_L2T3(3, 0); break;
+            default: HFMM_L2T3(4, 0); break;
+          }
+#undef HFMM_L2T3
       };
       if (n_dense_ > 0) {  // populous leaves: lane per observer, the rest: lanes over quads
         const int quads = int(d.nt / 2) * int(d.nt / 2);

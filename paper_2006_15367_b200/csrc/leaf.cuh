@@ -107,6 +107,7 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
                                                    int n, double k, double2* __restrict__ mp,
                                                    const double2* __restrict__ ltab = nullptr, int nh = 0) {
   __shared__ double4 sQ[4][kQuadP2][kQuadHalfMax];  // (Q+, Q-) per particle and theta row
+  __shared__ double2 sR[4][kQuadP2];                 // (x - cx, y - cy) per particle
   const double2* tb = TAB ? ltab + nh : nullptr;  // read through L1 (small CTAs: no staging)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t li = int64_t(blockIdx.x) * 4 + warp;
@@ -117,6 +118,7 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   double4 (*Qt)[kQuadHalfMax] = sQ[warp];
+  double2* Rt = sR[warp];
   for (int qc = 0; qc < quads; qc += 32 * R) {
     double ax[R], ay[R];
     int qi[R];
@@ -143,14 +145,15 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
         Qt[pp][i] = make_double4(fma(qq.x, cb, -qq.y * sb), fma(qq.x, sb, qq.y * cb),   // q e^{iB}
                                  fma(qq.x, cb, qq.y * sb), fma(qq.y, cb, -qq.x * sb));  // q e^{-iB}
       }
+      if (lane < np) Rt[lane] = make_double2(x[pc + lane] - cx, y[pc + lane] - cy);
       __syncwarp();
 #pragma unroll kC2MUnroll
       for (int pp = 0; pp < np; ++pp) {
-        const double rx = x[pc + pp] - cx, ry = y[pc + pp] - cy;
+        const double2 rr = Rt[pp];  // shared memory: no global load in the particle loop
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           double sa, ca;
-          sincos_l<TAB>(fma(ax[r], rx, ay[r] * ry), tb, nh, sa, ca);
+          sincos_l<TAB>(fma(ax[r], rr.x, ay[r] * rr.y), tb, nh, sa, ca);
           const double4 Q = Qt[pp][qi[r]];
           upx[r] = fma(Q.x, ca, upx[r]);
           upy[r] = fma(Q.x, sa, upy[r]);
@@ -261,6 +264,113 @@ __global__ void HFMM_LEAF_LB k_l2t_quad2(int64_t leaf_b, int64_t nl, const int* 
           ai[o] += __shfl_xor_sync(0xffffffffu, ai[o], off);
         }
         if (lane == 0 && pb + o < np) pot[pc + pb + o] = make_double2(-c * ai[o], c * ar[o]);
+      }
+    }
+  }
+}
+
+// L2T for small leaves, one warp per leaf, lanes over quads: each lane keeps
+// the weighted quad combinations (G, G', H, H') and k (dir_x, dir_y) of its R
+// quads in registers (built once per leaf and quad chunk), the particles are
+// staged per chunk in shared memory with their e^{iB} rows, so the
+// observer loop reads no global memory; kQuadOB observers per pass, one
+// shuffle reduction each.  Leaf grids with more than 32 R quads take several
+// quad chunks, whose sums lane 0 adds in chunk order (deterministic).
+template <int R, int HN = 0, bool TAB = false>
+__global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
+                                         const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
+                                         const double* __restrict__ y, const double* __restrict__ z,
+                                         const double* __restrict__ centers, const double* __restrict__ dir,
+                                         const double* __restrict__ wq, int n, double k,
+                                         const double2* __restrict__ loc, double2* __restrict__ pot,
+                                         const double2* __restrict__ ltab = nullptr, int nh = 0) {
+  __shared__ double2 sB[4][kQuadP2][kQuadHalfMax];  // e^{iB} per particle and theta row
+  __shared__ double2 sR[4][kQuadP2];                // k (x - cx), k (y - cy)
+  const double2* tb = TAB ? ltab + nh : nullptr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = HN > 0 ? HN : n / 2, quads = half * half, nphi = HN > 0 ? 2 * HN : n;
+  const int64_t S = int64_t(n) * n;
+  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
+  if (li >= nl) return;
+  const int64_t leaf = leaves ? int64_t(leaves[li]) : leaf_b + li;
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
+  const double2* lc = loc + leaf * S;
+  double2 (*Bt)[kQuadHalfMax] = sB[warp];
+  double2* Rt = sR[warp];
+  for (int qc = 0; qc < quads; qc += 32 * R) {
+    double2 G[R], Gp[R], H[R], Hp[R];
+    double dx[R], dy[R];
+    int qi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int qd = qc + lane + 32 * r;
+      const bool live = qd < quads;
+      const int i = live ? qd / half : 0, j = live ? qd - i * half : 0;
+      qi[r] = i;
+      const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
+      auto lw = [&](int64_t s) {
+        const double2 v = __ldg(lc + s);
+        const double w = live ? __ldg(wq + s) : 0.0;
+        return make_double2(w * v.x, w * v.y);
+      };
+      const double2 l1 = lw(s1), l2 = lw(s2), l3 = lw(s1 + half), l4 = lw(s2 + half);
+      const double2 s12 = make_double2(l1.x + l2.x, l1.y + l2.y), s34 = make_double2(l3.x + l4.x, l3.y + l4.y);
+      const double2 d12 = make_double2(l2.x - l1.x, l2.y - l1.y), d34 = make_double2(l4.x - l3.x, l4.y - l3.y);
+      G[r] = make_double2(s12.x + s34.x, s12.y + s34.y);
+      Gp[r] = make_double2(s34.x - s12.x, s34.y - s12.y);
+      H[r] = make_double2(d12.x + d34.x, d12.y + d34.y);
+      Hp[r] = make_double2(d34.x - d12.x, d34.y - d12.y);
+      dx[r] = dir[3 * s1];
+      dy[r] = dir[3 * s1 + 1];
+    }
+    for (int64_t pc = p0; pc < p1; pc += kQuadP2) {
+      const int np = int(p1 - pc < kQuadP2 ? p1 - pc : kQuadP2);
+      __syncwarp();
+      for (int t = lane; t < np * half; t += 32) {
+        const int pp = t / half, i = t - pp * half;
+        double sn, cs;
+        sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sn, cs);
+        Bt[pp][i] = make_double2(cs, sn);
+      }
+      if (lane < np) Rt[lane] = make_double2(k * (x[pc + lane] - cx), k * (y[pc + lane] - cy));
+      __syncwarp();
+      for (int pb = 0; pb < np; pb += kQuadOB) {
+        double ar[kQuadOB], ai[kQuadOB];
+#pragma unroll
+        for (int o = 0; o < kQuadOB; ++o) {
+          const int pp = pb + o < np ? pb + o : pb;  // idle slots repeat a live observer
+          const double2 rr = Rt[pp];
+          ar[o] = 0.0;
+          ai[o] = 0.0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            double sa, ca;
+            sincos_l<TAB>(fma(dx[r], rr.x, dy[r] * rr.y), tb, nh, sa, ca);
+            const double2 eb = Bt[pp][qi[r]];
+            const double u = eb.x * ca, v = eb.x * sa, w = eb.y * ca, zz = eb.y * sa;
+            ar[o] = fma(u, G[r].x, fma(-v, Gp[r].y, fma(-w, H[r].y, fma(-zz, Hp[r].x, ar[o]))));
+            ai[o] = fma(u, G[r].y, fma(v, Gp[r].x, fma(w, H[r].x, fma(-zz, Hp[r].y, ai[o]))));
+          }
+        }
+#pragma unroll
+        for (int o = 0; o < kQuadOB; ++o) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            ar[o] += __shfl_xor_sync(0xffffffffu, ar[o], off);
+            ai[o] += __shfl_xor_sync(0xffffffffu, ai[o], off);
+          }
+          if (lane == 0 && pb + o < np) {
+            const double2 v = make_double2(-c * ai[o], c * ar[o]);
+            if (qc == 0) {
+              pot[pc + pb + o] = v;
+            } else {
+              const double2 cur = pot[pc + pb + o];
+              pot[pc + pb + o] = make_double2(cur.x + v.x, cur.y + v.y);
+            }
+          }
+        }
       }
     }
   }
