@@ -699,23 +699,6 @@ void Engine::phase_l2t() {
       // (n / 2 <= kQuadHalfMax keeps the table under 48 KB: no attribute needed)
       auto l2t_quads = [&](unsigned grid, int64_t lb, int64_t cnt, const int* list) {
         const int hn = int(d.nt / 2);
-        if (std::getenv("HFMM_L2T_V2")) {  // (temporary A/B: the previous small-leaf kernel)
-#define HFMM_L2TQ(HN)                                                                                          \
-  do {                                                                                                          \
-    if (d_ltab_)                                                                                                \
-      k_l2t_quad2<HN, true><<<grid, 128, smem, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers,      \
-                                                      d.dir, d.wq, d.nt, s_.k, d.loc, d_pot, d_ltab_, ltab_half_);\
-    else                                                                                                        \
-      k_l2t_quad2<HN, false><<<grid, 128, smem, st_>>>(lb, cnt, list, d_leaf_start, d_x, d_y, d_z, d.centers,     \
-                                                       d.dir, d.wq, d.nt, s_.k, d.loc, d_pot);                  \
-  } while (0)
-          if (hn == 9) HFMM_L2TQ(9);
-          else if (hn == 11) HFMM_L2TQ(11);
-          else if (hn == 13) HFMM_L2TQ(13);
-          else HFMM_L2TQ(0);
-#undef HFMM_L2TQ
-          return;
-        }
         // quads per lane: fewest lane slots (chunks x R), ties to fewer chunks; R <= 4
         const int quads = hn * hn;
         int r = 1, best = INT32_MAX;

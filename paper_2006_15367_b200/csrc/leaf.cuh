@@ -119,6 +119,26 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   double4 (*Qt)[kQuadHalfMax] = sQ[warp];
   double2* Rt = sR[warp];
+  // Grids needing several quad passes (n = 26: 169 quads over 96 lane slots):
+  // a leaf with <= kQuadP2 particles builds its tables once for all passes.
+  // (Single-pass grids keep the build inside the particle loop: fewer live
+  // registers, measured faster at n = 18.)
+  constexpr bool kMultiPass = HN == 0 || HN * HN > 32 * R;
+  const bool one_chunk = kMultiPass && p1 - p0 <= kQuadP2;
+  auto build = [&](int64_t pc, int np) {
+    __syncwarp();
+    for (int t = lane; t < np * half; t += 32) {
+      const int pp = t / half, i = t - pp * half;
+      double sb, cb;
+      sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sb, cb);
+      const double2 qq = q[pc + pp];
+      Qt[pp][i] = make_double4(fma(qq.x, cb, -qq.y * sb), fma(qq.x, sb, qq.y * cb),   // q e^{iB}
+                               fma(qq.x, cb, qq.y * sb), fma(qq.y, cb, -qq.x * sb));  // q e^{-iB}
+    }
+    if (lane < np) Rt[lane] = make_double2(x[pc + lane] - cx, y[pc + lane] - cy);
+    __syncwarp();
+  };
+  if (one_chunk) build(p0, int(p1 - p0));
   for (int qc = 0; qc < quads; qc += 32 * R) {
     double ax[R], ay[R];
     int qi[R];
@@ -136,17 +156,7 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
     }
     for (int64_t pc = p0; pc < p1; pc += kQuadP2) {
       const int np = int(p1 - pc < kQuadP2 ? p1 - pc : kQuadP2);
-      __syncwarp();
-      for (int t = lane; t < np * half; t += 32) {
-        const int pp = t / half, i = t - pp * half;
-        double sb, cb;
-        sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sb, cb);
-        const double2 qq = q[pc + pp];
-        Qt[pp][i] = make_double4(fma(qq.x, cb, -qq.y * sb), fma(qq.x, sb, qq.y * cb),   // q e^{iB}
-                                 fma(qq.x, cb, qq.y * sb), fma(qq.y, cb, -qq.x * sb));  // q e^{-iB}
-      }
-      if (lane < np) Rt[lane] = make_double2(x[pc + lane] - cx, y[pc + lane] - cy);
-      __syncwarp();
+      if (!one_chunk) build(pc, np);
 #pragma unroll kC2MUnroll
       for (int pp = 0; pp < np; ++pp) {
         const double2 rr = Rt[pp];  // shared memory: no global load in the particle loop
@@ -183,99 +193,22 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
 }
 
 constexpr int kQuadOB = 4;  // observers per L2T pass
-// L2T, one warp per leaf: lanes over quads, kQuadOB observers per pass
-// (warp-shuffle reduction per observer), e^{iB} table per particle and row.
-// leaves != nullptr: warp w takes leaves[w] (a population class), else leaf_b + w.
-// HN as in k_c2m_quad2.
-template <int HN = 0, bool TAB = false>
-__global__ void HFMM_LEAF_LB k_l2t_quad2(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
-                                                   const int64_t* __restrict__ leaf_start,
-                                                   const double* __restrict__ x, const double* __restrict__ y,
-                                                   const double* __restrict__ z, const double* __restrict__ centers,
-                                                   const double* __restrict__ dir, const double* __restrict__ wq,
-                                                   int n, double k, const double2* __restrict__ loc,
-                                                   double2* __restrict__ pot, const double2* __restrict__ ltab = nullptr,
-                                                   int nh = 0) {
-  extern __shared__ double2 qsm[];
-  const double2* tb = TAB ? ltab + nh : nullptr;  // read through L1 (small CTAs: no staging)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = HN > 0 ? HN : n / 2, quads = half * half, nphi = HN > 0 ? 2 * HN : n;
-  const int64_t S = int64_t(n) * n;
-  double2* Bt = qsm + warp * (kQuadP * half);  // e^{iB} table of this warp
-  const int64_t li = int64_t(blockIdx.x) * 4 + warp;
-  if (li >= nl) return;
-  const int64_t leaf = leaves ? int64_t(leaves[li]) : leaf_b + li;
-  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
-  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
-  const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
-  const double2* lc = loc + leaf * S;
-  for (int64_t pc = p0; pc < p1; pc += kQuadP) {
-    const int np = int(p1 - pc < kQuadP ? p1 - pc : kQuadP);
-    __syncwarp();
-    for (int t = lane; t < np * half; t += 32) {
-      const int pp = t / half, i = t - pp * half;
-      double sn, cs;
-      sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sn, cs);
-      Bt[pp * half + i] = make_double2(cs, sn);
-    }
-    __syncwarp();
-    for (int pb = 0; pb < np; pb += kQuadOB) {
-      double rx[kQuadOB], ry[kQuadOB], ar[kQuadOB], ai[kQuadOB];
-#pragma unroll
-      for (int o = 0; o < kQuadOB; ++o) {
-        const int pp = pb + o < np ? pb + o : pb;  // idle slots repeat a live observer
-        rx[o] = k * (x[pc + pp] - cx);
-        ry[o] = k * (y[pc + pp] - cy);
-        ar[o] = 0.0;
-        ai[o] = 0.0;
-      }
-      for (int qd = lane; qd < quads; qd += 32) {
-        const int i = qd / half, j = qd - i * half;
-        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
-        const double dxs = dir[3 * s1], dys = dir[3 * s1 + 1];
-        auto lw = [&](int64_t s) {
-          const double2 v = __ldg(lc + s);
-          const double w = __ldg(wq + s);
-          return make_double2(w * v.x, w * v.y);
-        };
-        const double2 l1 = lw(s1), l2 = lw(s2), l3 = lw(s1 + half), l4 = lw(s2 + half);
-        const double2 s12 = make_double2(l1.x + l2.x, l1.y + l2.y), s34 = make_double2(l3.x + l4.x, l3.y + l4.y);
-        const double2 d12 = make_double2(l2.x - l1.x, l2.y - l1.y), d34 = make_double2(l4.x - l3.x, l4.y - l3.y);
-        const double2 G = make_double2(s12.x + s34.x, s12.y + s34.y);
-        const double2 Gp = make_double2(s34.x - s12.x, s34.y - s12.y);
-        const double2 H = make_double2(d12.x + d34.x, d12.y + d34.y);
-        const double2 Hp = make_double2(d34.x - d12.x, d34.y - d12.y);
-#pragma unroll
-        for (int o = 0; o < kQuadOB; ++o) {
-          const int pp = pb + o < np ? pb + o : pb;
-          double sa, ca;
-          sincos_l<TAB>(fma(dxs, rx[o], dys * ry[o]), tb, nh, sa, ca);
-          const double2 eb = Bt[pp * half + i];
-          const double u = eb.x * ca, v = eb.x * sa, w = eb.y * ca, zz = eb.y * sa;
-          ar[o] = fma(u, G.x, fma(-v, Gp.y, fma(-w, H.y, fma(-zz, Hp.x, ar[o]))));
-          ai[o] = fma(u, G.y, fma(v, Gp.x, fma(w, H.x, fma(-zz, Hp.y, ai[o]))));
-        }
-      }
-#pragma unroll
-      for (int o = 0; o < kQuadOB; ++o) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          ar[o] += __shfl_xor_sync(0xffffffffu, ar[o], off);
-          ai[o] += __shfl_xor_sync(0xffffffffu, ai[o], off);
-        }
-        if (lane == 0 && pb + o < np) pot[pc + pb + o] = make_double2(-c * ai[o], c * ar[o]);
-      }
-    }
-  }
-}
-
 // L2T for small leaves, one warp per leaf, lanes over quads: each lane keeps
 // the weighted quad combinations (G, G', H, H') and k (dir_x, dir_y) of its R
 // quads in registers (built once per leaf and quad chunk), the particles are
 // staged per chunk in shared memory with their e^{iB} rows, so the
 // observer loop reads no global memory; kQuadOB observers per pass, one
 // shuffle reduction each.  Leaf grids with more than 32 R quads take several
-// quad chunks, whose sums lane 0 adds in chunk order (deterministic).
+// quad chunks per particle chunk (the tables are built once), whose sums lane
+// 0 adds in chunk order (deterministic).
+// L2T for small leaves, one warp per leaf, lanes over quads: each lane keeps
+// the weighted quad combinations (G, G', H, H') and k (dir_x, dir_y) of its R
+// quads in registers (built once per leaf and quad chunk), the particles are
+// staged in shared memory with their e^{iB} rows, so the observer loop reads
+// no global memory; kQuadOB observers per pass, one shuffle reduction each.
+// Leaf grids with more than 32 R quads take several quad chunks, whose sums
+// lane 0 adds in chunk order (deterministic); a leaf of <= kQuadP2 particles
+// then builds its tables once for all chunks.
 template <int R, int HN = 0, bool TAB = false>
 __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
                                          const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
@@ -299,6 +232,20 @@ __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* 
   const double2* lc = loc + leaf * S;
   double2 (*Bt)[kQuadHalfMax] = sB[warp];
   double2* Rt = sR[warp];
+  auto build = [&](int64_t pc, int np) {
+    __syncwarp();
+    for (int t = lane; t < np * half; t += 32) {
+      const int pp = t / half, i = t - pp * half;
+      double sn, cs;
+      sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sn, cs);
+      Bt[pp][i] = make_double2(cs, sn);
+    }
+    if (lane < np) Rt[lane] = make_double2(k * (x[pc + lane] - cx), k * (y[pc + lane] - cy));
+    __syncwarp();
+  };
+  constexpr bool kMultiPass = HN == 0 || HN * HN > 32 * R;
+  const bool one_chunk = kMultiPass && p1 - p0 <= kQuadP2;
+  if (one_chunk) build(p0, int(p1 - p0));
   for (int qc = 0; qc < quads; qc += 32 * R) {
     double2 G[R], Gp[R], H[R], Hp[R];
     double dx[R], dy[R];
@@ -327,15 +274,7 @@ __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* 
     }
     for (int64_t pc = p0; pc < p1; pc += kQuadP2) {
       const int np = int(p1 - pc < kQuadP2 ? p1 - pc : kQuadP2);
-      __syncwarp();
-      for (int t = lane; t < np * half; t += 32) {
-        const int pp = t / half, i = t - pp * half;
-        double sn, cs;
-        sincos_l<TAB>(k * dir[3 * int64_t(i) * nphi + 2] * (z[pc + pp] - cz), tb, nh, sn, cs);
-        Bt[pp][i] = make_double2(cs, sn);
-      }
-      if (lane < np) Rt[lane] = make_double2(k * (x[pc + lane] - cx), k * (y[pc + lane] - cy));
-      __syncwarp();
+      if (!one_chunk) build(pc, np);
       for (int pb = 0; pb < np; pb += kQuadOB) {
         double ar[kQuadOB], ai[kQuadOB];
 #pragma unroll

@@ -10,5 +10,5 @@ O=paper_2006_15367_b200/_lib/obj
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC "$@" \
   -I include -I paper_2006_15367_b200/csrc -c paper_2006_15367_b200/csrc/engine.cu -o tools/variants/$name.engine.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o tools/variants/$name.so tools/variants/$name.engine.o \
-  $O/setup.cpp.o $O/setup_gpu.cu.o $O/capi.cu.o -Xcompiler -pthread
+  $O/setup.cpp.o $O/setup_import.cpp.o $O/setup_gpu.cu.o $O/world.cu.o $O/capi.cu.o -Xcompiler -pthread
 echo tools/variants/$name.so
