@@ -15,6 +15,7 @@
 #include "leaf.cuh"
 #include "m2l_tc.cuh"
 #include "interp_rb.cuh"
+#include "interp_fused.cuh"
 #include "interp_big.cuh"
 
 namespace hfmm_b200 {
@@ -568,6 +569,15 @@ void Engine::phase_m2m() {
                       R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
                       oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
     if (rl.n_par == 0) continue;
+    // 0. fused single-kernel pair (folded circles stay in shared memory)
+#if !defined(HFMM_NO_FZ) && !defined(HFMM_NO_FZ_M2M)
+    if (!hook_no_rb_ && fz_pair(nc, np)) {
+      launch_m2m_fz(rl, sms_, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up);
+      ++launches_;
+      ck(cudaGetLastError(), "k_m2m_fz");
+      continue;
+    }
+#endif
     // 1. compile-time-shaped streaming pairs (the BASELINE leaf-side pairs)
     if (!hook_no_rb_ && rb_pair(nc, np) &&
         launch_m2m_rb(nc, np, rl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up, d_tmp)) {
@@ -651,6 +661,15 @@ void Engine::phase_l2l(int lo, int hi) {
                       R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
                       oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
     if (rl.n_par == 0) continue;
+    // 0. fused single-kernel pair (narrow rows stay in shared memory)
+#if !defined(HFMM_NO_FZ) && !defined(HFMM_NO_FZ_L2L)
+    if (!hook_no_rb_ && fz_pair(nc, np)) {
+      launch_l2l_fz(rl, sms_, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn);
+      ++launches_;
+      ck(cudaGetLastError(), "k_l2l_fz");
+      continue;
+    }
+#endif
     // 1. compile-time-shaped streaming pairs
     if (!hook_no_rb_ && rb_pair(nc, np) &&
         launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn, d_tmp)) {

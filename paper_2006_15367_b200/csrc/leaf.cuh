@@ -193,6 +193,77 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
 }
 
 constexpr int kQuadOB = 4;  // observers per L2T pass
+// Multi-chunk grids (n = 26: 169 quads over 96 lane slots) for k_l2t_quad3:
+// particle chunks outside (tables built once per chunk), quad chunks inside,
+// one observer per pass (fewest live registers; measured fastest there).
+template <int R, int HN, bool TAB, class Build>
+__device__ __forceinline__ void l2t_quad3_multi(int64_t p0, int64_t p1, int half, int quads, int nphi, int n, double k,
+                                                double c, const double2* __restrict__ lc,
+                                                const double* __restrict__ wq, const double* __restrict__ dir,
+                                                const double2* __restrict__ tb, int nh,
+                                                double2 (*Bt)[kQuadHalfMax], double2* Rt, Build& build,
+                                                double2* __restrict__ pot) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t pc = p0; pc < p1; pc += kQuadP2) {
+    const int np = int(p1 - pc < kQuadP2 ? p1 - pc : kQuadP2);
+    build(pc, np);
+    for (int qc = 0; qc < quads; qc += 32 * R) {
+      double2 G[R], Gp[R], H[R], Hp[R];
+      double dx[R], dy[R];
+      int qi[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int qd = qc + lane + 32 * r;
+        const bool live = qd < quads;
+        const int i = live ? qd / half : 0, j = live ? qd - i * half : 0;
+        qi[r] = i;
+        const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
+        auto lw = [&](int64_t s) {
+          const double2 v = __ldg(lc + s);
+          const double w = live ? __ldg(wq + s) : 0.0;
+          return make_double2(w * v.x, w * v.y);
+        };
+        const double2 l1 = lw(s1), l2 = lw(s2), l3 = lw(s1 + half), l4 = lw(s2 + half);
+        const double2 s12 = make_double2(l1.x + l2.x, l1.y + l2.y), s34 = make_double2(l3.x + l4.x, l3.y + l4.y);
+        const double2 d12 = make_double2(l2.x - l1.x, l2.y - l1.y), d34 = make_double2(l4.x - l3.x, l4.y - l3.y);
+        G[r] = make_double2(s12.x + s34.x, s12.y + s34.y);
+        Gp[r] = make_double2(s34.x - s12.x, s34.y - s12.y);
+        H[r] = make_double2(d12.x + d34.x, d12.y + d34.y);
+        Hp[r] = make_double2(d34.x - d12.x, d34.y - d12.y);
+        dx[r] = dir[3 * s1];
+        dy[r] = dir[3 * s1 + 1];
+      }
+      for (int pp = 0; pp < np; ++pp) {
+        const double2 rr = Rt[pp];
+        double ar = 0.0, ai = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          double sa, ca;
+          sincos_l<TAB>(fma(dx[r], rr.x, dy[r] * rr.y), tb, nh, sa, ca);
+          const double2 eb = Bt[pp][qi[r]];
+          const double u = eb.x * ca, v = eb.x * sa, w = eb.y * ca, zz = eb.y * sa;
+          ar = fma(u, G[r].x, fma(-v, Gp[r].y, fma(-w, H[r].y, fma(-zz, Hp[r].x, ar))));
+          ai = fma(u, G[r].y, fma(v, Gp[r].x, fma(w, H[r].x, fma(-zz, Hp[r].y, ai))));
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          ar += __shfl_xor_sync(0xffffffffu, ar, off);
+          ai += __shfl_xor_sync(0xffffffffu, ai, off);
+        }
+        if (lane == 0) {
+          const double2 v = make_double2(-c * ai, c * ar);
+          if (qc == 0) {
+            pot[pc + pp] = v;
+          } else {
+            const double2 cur = pot[pc + pp];
+            pot[pc + pp] = make_double2(cur.x + v.x, cur.y + v.y);
+          }
+        }
+      }
+    }
+  }
+}
+
 // L2T for small leaves, one warp per leaf, lanes over quads: each lane keeps
 // the weighted quad combinations (G, G', H, H') and k (dir_x, dir_y) of its R
 // quads in registers (built once per leaf and quad chunk), the particles are
@@ -206,9 +277,8 @@ constexpr int kQuadOB = 4;  // observers per L2T pass
 // quads in registers (built once per leaf and quad chunk), the particles are
 // staged in shared memory with their e^{iB} rows, so the observer loop reads
 // no global memory; kQuadOB observers per pass, one shuffle reduction each.
-// Leaf grids with more than 32 R quads take several quad chunks, whose sums
-// lane 0 adds in chunk order (deterministic); a leaf of <= kQuadP2 particles
-// then builds its tables once for all chunks.
+// Leaf grids with more than 32 R quads take several quad chunks
+// (l2t_quad3_multi), whose sums lane 0 adds in chunk order (deterministic).
 template <int R, int HN = 0, bool TAB = false>
 __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* __restrict__ leaves,
                                          const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
@@ -244,8 +314,10 @@ __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* 
     __syncwarp();
   };
   constexpr bool kMultiPass = HN == 0 || HN * HN > 32 * R;
-  const bool one_chunk = kMultiPass && p1 - p0 <= kQuadP2;
-  if (one_chunk) build(p0, int(p1 - p0));
+  if constexpr (kMultiPass) {  // several quad chunks: particle chunks outside, one observer per pass
+    l2t_quad3_multi<R, HN, TAB>(p0, p1, half, quads, nphi, n, k, c, lc, wq, dir, tb, nh, Bt, Rt, build, pot);
+    return;
+  }
   for (int qc = 0; qc < quads; qc += 32 * R) {
     double2 G[R], Gp[R], H[R], Hp[R];
     double dx[R], dy[R];
@@ -274,7 +346,7 @@ __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* 
     }
     for (int64_t pc = p0; pc < p1; pc += kQuadP2) {
       const int np = int(p1 - pc < kQuadP2 ? p1 - pc : kQuadP2);
-      if (!one_chunk) build(pc, np);
+      build(pc, np);
       for (int pb = 0; pb < np; pb += kQuadOB) {
         double ar[kQuadOB], ai[kQuadOB];
 #pragma unroll
