@@ -94,6 +94,17 @@ Engine::Engine(std::shared_ptr<const Setup> sp, int device, int rank)
   ck(cudaStreamCreateWithFlags(&st_cp_, cudaStreamNonBlocking), "copy stream");
   ck(cudaEventCreateWithFlags(&ev_q_, cudaEventDisableTiming), "event");
   ck(cudaEventCreateWithFlags(&ev_cp_order_, cudaEventDisableTiming), "event");
+  if (dist_) {  // rank plan first: it sizes the compact per-rank storage
+    rp_ = std::make_unique<RankPlan>(build_rank_plan(s, rank));
+    rows_.assign(size_t(s.L + 1), {});
+    for (int l = s.top; l <= s.L; ++l) {
+      auto& ro = rows_[size_t(l)];
+      ro.assign(s.levels[size_t(l)].num_nodes(), -1);
+      int r = 0;
+      for (int n : rp_->held[size_t(l)]) ro[size_t(n)] = r++;
+      for (int n : rp_->halo[size_t(l)]) ro[size_t(n)] = r++;
+    }
+  }
   upload();
   if (dist_) upload_rank_plan();
   ck(cudaStreamSynchronize(st_), "upload sync");
@@ -170,7 +181,7 @@ void Engine::setup_interp(DevLevel& P, const DevLevel& C, const LevelData& tp, c
     P.big_rc[1] = int(std::max<size_t>(1, std::min<size_t>(size_t(nc), row_budget / (size_t(P.dn_phi[2]) * sizeof(double2)))));
     P.big_smem[3] = size_t(P.big_rc[1]) * P.dn_phi[2] * sizeof(double2);
     P.big_ldn = P.dn_phi[2];
-    tmp_need_ = std::max(tmp_need_, std::max(size_t(C.n_nodes) * half * ldf, size_t(C.n_nodes) * nc * P.big_ldn));
+    tmp_need_ = std::max(tmp_need_, std::max(size_t(C.n_rows) * half * ldf, size_t(C.n_rows) * nc * P.big_ldn));
   }
 }
 
@@ -340,6 +351,8 @@ void Engine::upload() {
     d.trunc = t.trunc;
     d.S = t.samples();
     d.n_nodes = int(t.num_nodes());
+    // rows: every node (one rank), or held + halo + one zero row (distributed mode)
+    d.n_rows = dist_ ? int(rp_->held[size_t(l)].size() + rp_->halo[size_t(l)].size()) + 1 : d.n_nodes;
     d.side = t.side;
     // Directions exactly as LevelSampling::direction (sphere_grid.cpp:25-37).
     std::vector<double> dir(size_t(3 * d.S)), wq(size_t(d.S));
@@ -357,10 +370,10 @@ void Engine::upload() {
     hdir[size_t(l)] = dir;
     d.wq = upload_vec(wq);
     d.centers = upload_vec(t.centers);
-    d.mp = alloc<double2>(size_t(d.n_nodes) * size_t(d.S));
-    d.loc = alloc<double2>(size_t(d.n_nodes) * size_t(d.S));
-    ck(cudaMemsetAsync(d.mp, 0, size_t(d.n_nodes) * size_t(d.S) * sizeof(double2), st_), "memset mp");
-    ck(cudaMemsetAsync(d.loc, 0, size_t(d.n_nodes) * size_t(d.S) * sizeof(double2), st_), "memset loc");
+    d.mp = alloc<double2>(size_t(d.n_rows) * size_t(d.S));
+    d.loc = alloc<double2>(size_t(d.n_rows) * size_t(d.S));
+    ck(cudaMemsetAsync(d.mp, 0, size_t(d.n_rows) * size_t(d.S) * sizeof(double2), st_), "memset mp");
+    ck(cudaMemsetAsync(d.loc, 0, size_t(d.n_rows) * size_t(d.S) * sizeof(double2), st_), "memset loc");
     // Far lists as (source, offset slot) and the used slots.
     std::vector<int64_t> foff(t.far_off.begin(), t.far_off.end());
     std::vector<int2> far(t.far.size());
@@ -376,6 +389,20 @@ void Engine::upload() {
         used[size_t(sl)] = 1;
       }
     d.n_far = int64_t(far.size());
+    if (dist_) {  // far-list CSR over the held observers (rows 0..H-1), sources as rows
+      const int zero_row = d.n_rows - 1;  // absent sources (outside every needed slice) read zeros
+      std::vector<int64_t> fo{0};
+      std::vector<int2> fr;
+      for (int o : rp_->held[size_t(l)]) {
+        for (uint64_t f = t.far_off[size_t(o)]; f < t.far_off[size_t(o) + 1]; ++f) {
+          const int r = row(l, int(far[f].x));
+          fr.push_back(make_int2(r >= 0 ? r : zero_row, far[f].y));
+        }
+        fo.push_back(int64_t(fr.size()));
+      }
+      foff.swap(fo);
+      far.swap(fr);
+    }
     d.far_off = upload_vec(foff);
     d.far = upload_vec(far);
     d.slot_used = upload_vec(used);
@@ -412,7 +439,7 @@ void Engine::upload() {
       for (size_t i = 0; i < t.num_nodes(); ++i) {
         const uint64_t c = t.codes[i];
         const size_t gx = cell_axis(c, l, 0) + 3, gy = cell_axis(c, l, 1) + 3, gz = cell_axis(c, l, 2) + 3;
-        lk[(gz * GP + gy) * GP + gx] = int(i);
+        lk[(gz * GP + gy) * GP + gx] = row(l, int(i));  // -1: not stored on this rank (zero-filled)
       }
       d.lookup = upload_vec(lk);
       d.dense = true;
@@ -425,11 +452,14 @@ void Engine::upload() {
       d.child_off = upload_vec(coff);
       d.children = upload_vec(ch);
     }
-    if (l > s.top) {
+    if (l > s.top) {  // parent row of every row
       const LevelData& pt = s.levels[size_t(l - 1)];
-      std::vector<int> par(t.num_nodes(), -1);
+      std::vector<int> par(size_t(d.n_rows), -1);
       for (size_t p = 0; p < pt.num_nodes(); ++p)
-        for (uint64_t z2 = pt.child_off[p]; z2 < pt.child_off[p + 1]; ++z2) par[pt.children[z2]] = int(p);
+        for (uint64_t z2 = pt.child_off[p]; z2 < pt.child_off[p + 1]; ++z2) {
+          const int rc = row(l, int(pt.children[z2]));
+          if (rc >= 0) par[size_t(rc)] = row(l - 1, int(p));
+        }
       d.parent = upload_vec(par);
     }
   }
@@ -437,8 +467,11 @@ void Engine::upload() {
   std::vector<uint8_t*> octs(size_t(L + 1), nullptr);
   for (int l = s.top; l <= L; ++l) {
     const LevelData& t = s.levels[size_t(l)];
-    std::vector<uint8_t> oc(t.num_nodes());
-    for (size_t i = 0; i < t.num_nodes(); ++i) oc[i] = uint8_t(t.codes[i] & 7);
+    std::vector<uint8_t> oc(size_t(lv_[size_t(l)].n_rows), 0);  // per row
+    for (size_t i = 0; i < t.num_nodes(); ++i) {
+      const int r = row(l, int(i));
+      if (r >= 0) oc[size_t(r)] = uint8_t(t.codes[i] & 7);
+    }
     octs[size_t(l)] = upload_vec(oc);
   }
   oct_ = octs;
@@ -468,9 +501,9 @@ void Engine::upload() {
     P.shift_up = upload_vec(up);
     P.shift_dn = upload_vec(dn);
     setup_interp(P, C, tp, tc);
-    tmp = std::max(tmp, size_t(C.n_nodes) * size_t(nc) * size_t(np));
-    tmp = std::max(tmp, rb_m2m_scratch(C.n_nodes, nc, np));
-    tmp = std::max(tmp, rb_l2l_scratch(C.n_nodes, nc, np));
+    tmp = std::max(tmp, size_t(C.n_rows) * size_t(nc) * size_t(np));
+    tmp = std::max(tmp, rb_m2m_scratch(C.n_rows, nc, np));
+    tmp = std::max(tmp, rb_l2l_scratch(C.n_rows, nc, np));
   }
   tmp_elems_ = std::max(tmp, tmp_need_);
   d_tmp = alloc<double2>(tmp_elems_);
@@ -603,7 +636,7 @@ void Engine::phase_m2m() {
       continue;
     }
     // 3. two-stage large-grid kernels (any grid; B streams from L2)
-    const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
+    const int* clist = nullptr;  // children rows 0..ncl-1 (held rows come first)
     const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
     ck(cudaFuncSetAttribute(k_m2m_big_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[0])), "attr");
     ck(cudaFuncSetAttribute(k_m2m_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[1])), "attr");
@@ -642,7 +675,7 @@ void Engine::phase_m2l(int lo, int hi) {
       const int nobs = dist_ ? held_cnt_[size_t(l)] : int(d.n_nodes);
       if (nobs == 0) continue;
       dim3 grid(unsigned(nobs), unsigned((d.S + 127) / 128));
-      k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, dist_ ? held_[size_t(l)] : nullptr, d.far_off, d.far, d.T, d.mp, d.loc);
+      k_m2l<<<grid, 128, 0, st_>>>(d.S, 0, nullptr, d.far_off, d.far, d.T, d.mp, d.loc);  // rows 0..nobs-1
     }
     ++launches_;
   }
@@ -691,7 +724,7 @@ void Engine::phase_l2l(int lo, int hi) {
       continue;
     }
     // 3. two-stage large-grid kernels
-    const int* clist = dist_ ? held_[size_t(l + 1)] : nullptr;
+    const int* clist = nullptr;  // children rows 0..ncl-1 (held rows come first)
     const int ncl = dist_ ? held_cnt_[size_t(l + 1)] : C.n_nodes;
     if (ncl == 0) continue;
     ck(cudaFuncSetAttribute(k_l2l_big_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.big_smem[2])), "attr");
@@ -761,11 +794,11 @@ void Engine::phase_l2t() {
     }                                                                                                          \
     if (d_ltab_)                                                                                               \
       k_l2t_obs<HN, true><<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(                                      \
-          n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot, \
+          leaf_b_, n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot, \
           d_ltab_, ltab_half_);                                                                                \
     else                                                                                                       \
       k_l2t_obs<HN, false><<<unsigned((n_dense_ + 3) / 4), 128, so, st_>>>(                                     \
-          n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot); \
+          leaf_b_, n_dense_, d_dense_leaves_, d_leaf_start, d_x, d_y, d_z, d.centers, d.dir, d.wq, d.nt, s_.k, d.loc, d_pot); \
   } while (0)
         if (hn == 9) HFMM_L2TO(9);
         else if (hn == 11) HFMM_L2TO(11);
@@ -796,6 +829,7 @@ void Engine::near_start() {
   const int64_t cnt = part_e_ - part_b_;
   if (cnt > 0)
     ck(cudaMemsetAsync(d_pot_near + part_b_, 0, size_t(cnt) * sizeof(double2), st2_), "memset near");
+#ifdef HFMM_P2P_OLD
   if (n_tiny_ > 0) {
     if (d_ptab_)
       k_p2p_small_w<true><<<unsigned((n_tiny_ + 3) / 4), 128, 0, st2_>>>(
@@ -816,6 +850,20 @@ void Engine::near_start() {
                                                          d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near);
     ++launches_;
   }
+#else
+  if (n_tiny_ + n_small_ > 0) {  // leaves with <= 32 particles: one warp per leaf
+    const int nl = n_tiny_ + n_small_;
+    if (d_ptab_)
+      k_p2p_leaf2<true><<<unsigned((nl + 3) / 4), 128, 0, st2_>>>(nl, d_sparse_leaves_, d_leaf_start, d_near_off,
+                                                                  d_near, d.centers, d_x, d_y, d_z, d_q, s_.k,
+                                                                  d_pot_near, d_ptab_, ptab_max_);
+    else
+      k_p2p_leaf2<false><<<unsigned((nl + 3) / 4), 128, 0, st2_>>>(nl, d_sparse_leaves_, d_leaf_start, d_near_off,
+                                                                   d_near, d.centers, d_x, d_y, d_z, d_q, s_.k,
+                                                                   d_pot_near);
+    ++launches_;
+  }
+#endif
   if (n_dense_ > 0) {
     for (int c = 3; c >= 0; --c) {
         if (p2p_items_n_[c] == 0) continue;
@@ -1066,7 +1114,19 @@ void Engine::get_expansion(int kind, int level, double* out, size_t cap) {
   const size_t cnt = size_t(d.n_nodes) * size_t(d.S) * 2;
   if (cap < cnt) throw std::invalid_argument("get_expansion: buffer too small");
   ck(cudaStreamSynchronize(st_), "sync");
-  ck(cudaMemcpy(out, kind == 0 ? d.mp : d.loc, cnt * sizeof(double), cudaMemcpyDeviceToHost), "D2H exp");
+  const double2* src = kind == 0 ? d.mp : d.loc;
+  if (rows_.empty()) {
+    ck(cudaMemcpy(out, src, cnt * sizeof(double), cudaMemcpyDeviceToHost), "D2H exp");
+    return;
+  }
+  // distributed mode: rows -> node order; nodes not stored here read as zero
+  std::vector<double2> tmp(size_t(d.n_rows) * size_t(d.S));
+  ck(cudaMemcpy(tmp.data(), src, tmp.size() * sizeof(double2), cudaMemcpyDeviceToHost), "D2H exp");
+  std::memset(out, 0, cnt * sizeof(double));
+  for (int n = 0; n < d.n_nodes; ++n) {
+    const int r = row(level, n);
+    if (r >= 0) std::memcpy(out + size_t(n) * size_t(d.S) * 2, tmp.data() + size_t(r) * size_t(d.S), size_t(d.S) * 16);
+  }
 }
 
 void Engine::get_potentials_sorted(double* out, size_t cap) {
@@ -1088,21 +1148,27 @@ void Engine::store_potentials_host(double* host_sorted) {
 void Engine::upload_rank_plan() {
   const Setup& s = s_;
   const int L = s.L, P = s.P;
-  RankPlan rp = build_rank_plan(s, rank_);
+  const RankPlan& rp = *rp_;
+  // Every index the kernels see is a ROW of the compact per-rank storage.
+  auto rows_of = [&](int l, const std::vector<int>& nodes) {
+    std::vector<int> v(nodes.size());
+    for (size_t i = 0; i < nodes.size(); ++i) v[i] = row(l, nodes[i]);
+    return v;
+  };
   rl_.assign(size_t(L + 1), RankLevel{});
   for (int l = s.top; l < L; ++l) {
     RankLevel& R = rl_[size_t(l)];
     R.n_par = int(rp.held[size_t(l)].size());
-    R.plist = upload_vec(rp.held[size_t(l)]);
+    R.plist = upload_vec(rows_of(l, rp.held[size_t(l)]));  // 0..H-1
     R.child_off = upload_vec(rp.child_off[size_t(l)]);
-    R.children = upload_vec(rp.children[size_t(l)]);
+    R.children = upload_vec(rows_of(l + 1, rp.children[size_t(l)]));
     R.n_children = int64_t(rp.children[size_t(l)].size());
   }
   held_.assign(size_t(L + 1), nullptr);
   held_cnt_.assign(size_t(L + 1), 0);
   for (int l = s.top; l <= L; ++l) {
     held_cnt_[size_t(l)] = int(rp.held[size_t(l)].size());
-    held_[size_t(l)] = upload_vec(rp.held[size_t(l)]);
+    held_[size_t(l)] = upload_vec(rows_of(l, rp.held[size_t(l)]));
     DevLevel& d = lv_[size_t(l)];
     if (d.dense) {  // the 8^3 observer blocks (Morton subtrees) holding held nodes
       const int nb = (d.G + m2l::MB - 1) / m2l::MB;
@@ -1134,7 +1200,9 @@ void Engine::upload_rank_plan() {
         for (const RowItem& it : items) {  // (level, node, begin) order
           auto& v = per[size_t(it.level)];
           const int64_t len = it.end - it.begin;
-          v.insert(v.end(), {int64_t(it.node), it.begin, len, x.len[size_t(it.level)]});
+          const int r = row(it.level, it.node);
+          if (r < 0) throw std::logic_error("exchange plan: node not stored on this rank");
+          v.insert(v.end(), {int64_t(r), it.begin, len, x.len[size_t(it.level)]});
           x.len[size_t(it.level)] += len;
           x.maxlen[size_t(it.level)] = std::max(x.maxlen[size_t(it.level)], len);
         }

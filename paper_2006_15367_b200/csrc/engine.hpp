@@ -20,6 +20,7 @@ struct DevLevel {
   int level = 0, nt = 0, np = 0, trunc = 0;
   int64_t S = 0;
   int n_nodes = 0;
+  int n_rows = 0;             // expansion rows allocated (one logical rank: n_nodes; see Engine::rows_)
   double side = 0.0;
   double* dir = nullptr;      // S*3 sample directions (sphere_grid.cpp:31-37)
   double* wq = nullptr;       // S quadrature weights theta_w[i]*phi_w
@@ -231,6 +232,13 @@ class Engine {
   std::vector<int> held_cnt_;
   std::vector<PeerPlan> peers_;             // [peer]
   void upload_rank_plan();
+  // Compact per-rank storage (distributed mode): the expansions of level l
+  // are rows [held nodes (sorted) | halo nodes received through the M2L plan
+  // | one zero row]; rows_[l][node] = row or -1.  One logical rank: rows =
+  // nodes (rows_ empty).
+  std::unique_ptr<RankPlan> rp_;
+  std::vector<std::vector<int>> rows_;
+  int row(int l, int node) const { return rows_.empty() ? node : rows_[size_t(l)][size_t(node)]; }
   int64_t last_launches_ = 0;
   bool timed_ = false;
 };

@@ -8,9 +8,14 @@
 // Same algebra and the same device helpers as interp_rb.cuh (real + rank-1
 // matrices on DMMA, complex-row warp tiles, child sum as a reduce-scatter);
 // traversal.cpp:322-429 (M2M) and :583-707 (L2L), sphere_grid.cpp:183-214.
+// Data movement uses the Blackwell bulk-copy engine (bulk.cuh): the L2L
+// parent local is staged into shared memory by one cp.async.bulk with an
+// mbarrier, and each M2M CTA prefetches its NEXT parent's children into L2
+// with cp.async.bulk.prefetch while the current parent computes.
 #ifndef HFMM_B200_INTERP_FUSED_CUH
 #define HFMM_B200_INTERP_FUSED_CUH
 
+#include "bulk.cuh"
 #include "interp_rb.cuh"
 
 namespace hfmm_b200 {
@@ -31,6 +36,18 @@ struct Lay {
   static constexpr int BDTH = D::DTH_K * D::DTH_LDB, BDPHI = D::DPHI_K * D::DPHI_LDB;
   static constexpr int L2L_SMEM = (BDTH + BDPHI) * 8 + 8 * CSN * 16 + D::SP * 16;  // + the parent local
 };
+
+// L2 prefetch of a parent's children block (children of a parent are
+// consecutive nodes, so their expansions are one contiguous block).
+__device__ __forceinline__ void prefetch_children(int par, int n_par, const int* __restrict__ child_off,
+                                                  const int* __restrict__ children, const double2* base, int S) {
+  if (par >= n_par) return;
+  const int cb = child_off[par], n = child_off[par + 1] - cb;
+  if (n <= 0) return;
+  const int c0 = children[cb];
+  if (children[cb + n - 1] - c0 != n - 1) return;  // not contiguous: no hint
+  bulk::prefetch_l2(base + int64_t(c0) * S, uint32_t(n) * uint32_t(S) * 16u);
+}
 
 }  // namespace fz
 
@@ -60,6 +77,7 @@ __global__ void __launch_bounds__(fz::kThreads, 2) k_m2m_fz(int n_par, const int
   constexpr int NW = fz::kThreads / 32;
   for (int par = blockIdx.x; par < n_par; par += gridDim.x) {
     const int cb = child_off[par], nch = child_off[par + 1] - cb;
+    if (threadIdx.x == 0) fz::prefetch_children(par + gridDim.x, n_par, child_off, children, mp_c, SC);
     // phi pass: rows (child c, theta row i) -> folded circles in shared memory
     const int rows = nch * NC, tiles = (rows + 7) / 8;
     for (int t = warp; t < tiles; t += NW) {
@@ -174,19 +192,23 @@ __global__ void __launch_bounds__(fz::kThreads, 2) k_l2l_fz(int n_par, const int
   double* Bp = Bt + Y::BDTH;
   double2* Ns = reinterpret_cast<double2*>(Bp + Y::BDPHI);
   double2* Ls = Ns + 8 * Y::CSN;  // the parent's local expansion, staged per parent
+  __shared__ __align__(8) uint64_t lbar;  // completion of the parent-local bulk copy
+  if (threadIdx.x == 0) {
+    bulk::mbar_init(&lbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   rb::stage_b<D::DTH_K, D::DTH_N, D::DTH_LDB>(Bt, Bth);
   rb::stage_b<D::DPHI_K, D::DPHI_N, D::DPHI_LDB>(Bp, Bphi);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   constexpr int NW = fz::kThreads / 32;
-  for (int par = blockIdx.x; par < n_par; par += gridDim.x) {
+  uint32_t phase = 0;
+  for (int par = blockIdx.x; par < n_par; par += gridDim.x, phase ^= 1u) {
     const int cb = child_off[par], nch = child_off[par + 1] - cb;
-    {  // stage the parent local (cp.async, 16 B per sample): one wait per parent
-      const double2* Lg = loc_p + int64_t(plist ? plist[par] : par) * SP;
-      for (int t = threadIdx.x; t < SP; t += blockDim.x) cp_async16(Ls + t, Lg + t, true);
-      cp_async_commit();
-      cp_async_wait_all();
-      __syncthreads();
+    if (threadIdx.x == 0) {  // the parent local: one bulk copy
+      bulk::mbar_expect_tx(&lbar, uint32_t(SP) * 16u);
+      bulk::copy_g2s(Ls, loc_p + int64_t(plist ? plist[par] : par) * SP, uint32_t(SP) * 16u, &lbar);
     }
+    bulk::mbar_wait(&lbar, phase);
     const double2* L = Ls;
     // theta pass: rows (child c, circle p) built on the fly from the shifted
     // parent local -> narrow rows in shared memory

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(128) k_c2m(int64_t leaf_b, const int64_t* __re
 #pragma unroll
     for (int r = 0; r < kC2MR; ++r) {
       const int64_t s = sb + threadIdx.x + int64_t(r) * blockDim.x;
-      if (s < S) mp[leaf * S + s] = acc[r];
+      if (s < S) mp[int64_t(blockIdx.x) * S + s] = acc[r];  // row: leaf - leaf_b
     }
   }
 }
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(128) k_l2t(int64_t leaf_b, const int64_t* __re
     const int ns = int(S - sb < kL2TChunk ? S - sb : kL2TChunk);
     __syncthreads();
     for (int t = threadIdx.x; t < ns; t += blockDim.x) {
-      const double2 v = loc[leaf * S + sb + t];
+      const double2 v = loc[int64_t(blockIdx.x) * S + sb + t];  // row: leaf - leaf_b
       const double w = wq[sb + t];
       sL[t] = make_double2(w * v.x, w * v.y);
       sd[3 * t] = dir[3 * (sb + t)];
@@ -341,6 +341,28 @@ __device__ __forceinline__ void green_tab(double r2, const double2* __restrict__
   const double cs = fma(d2, fma(d2, 4.1666666666666667e-2, -0.5), 1.0);
   const double2 c0 = tab[n];  // (cos x0, -sin x0); shared (symmetric kernel) or global (small leaves)
   // exp(-i (x0 + d)) = (cos x0 - i sin x0)(cos d - i sin d)
+  gr = fma(c0.x, cs, c0.y * sn) * ri;
+  gi = fma(c0.y, cs, -(c0.x * sn)) * ri;
+}
+
+// green_tab without the index clamp, for callers whose r' is always inside
+// the table (real observer and source particles of adjacent leaves).
+__device__ __forceinline__ void green_tab_nc(double r2, const double2* __restrict__ tab, double& gr, double& gi) {
+  double y0;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(r2));
+  const double t = r2 * y0;
+  const double e = fma(-t, y0, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  const double ri = fma(y0 * e, p, y0);
+  const double x = r2 * ri;
+  const double kMagic = 6755399441055744.0;
+  const double tq = fma(t, 128.0, kMagic);
+  const int n = __double2loint(tq);
+  const double d = fma(tq - kMagic, -0.0078125, x);
+  const double d2 = d * d;
+  const double sn = fma(d * d2, fma(d2, 8.3333333333333333e-3, -1.6666666666666667e-1), d);
+  const double cs = fma(d2, fma(d2, 4.1666666666666667e-2, -0.5), 1.0);
+  const double2 c0 = tab[n];
   gr = fma(c0.x, cs, c0.y * sn) * ri;
   gi = fma(c0.y, cs, -(c0.x * sn)) * ri;
 }

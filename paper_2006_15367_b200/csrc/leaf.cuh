@@ -181,7 +181,7 @@ __global__ void HFMM_LEAF_LB k_c2m_quad2(int64_t leaf_b, int64_t nl, const int64
       const int qd = qc + lane + 32 * r;
       if (qd < quads) {
         const int i = qd / half, j = qd - i * half;
-        double2* m = mp + leaf * S;
+        double2* m = mp + li * S;  // row of the leaf: leaf - leaf_b (engine rows, world.hpp)
         const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;
         m[s1] = make_double2(upx[r] - vpy[r], upy[r] + vpx[r]);         // A + B
         m[s2] = make_double2(umx[r] - vmy[r], umy[r] + vmx[r]);         // A - B   (pi - theta)
@@ -299,7 +299,7 @@ __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* 
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
-  const double2* lc = loc + leaf * S;
+  const double2* lc = loc + (leaf - leaf_b) * S;  // leaf rows start at leaf_b
   double2 (*Bt)[kQuadHalfMax] = sB[warp];
   double2* Rt = sR[warp];
   auto build = [&](int64_t pc, int np) {
@@ -395,7 +395,7 @@ __global__ void HFMM_LEAF_LB k_l2t_quad3(int64_t leaf_b, int64_t nl, const int* 
 // acc += cos B_i X + sin B_i Y.  No cross-lane reduction.
 // Shared memory per warp: quads x (4 + 1) double2.
 template <int HN = 0, bool TAB = false>
-__global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restrict__ leaves,
+__global__ void __launch_bounds__(128) k_l2t_obs(int64_t row0, int64_t nl, const int* __restrict__ leaves,
                                                  const int64_t* __restrict__ leaf_start, const double* __restrict__ x,
                                                  const double* __restrict__ y, const double* __restrict__ z,
                                                  const double* __restrict__ centers, const double* __restrict__ dir,
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(128) k_l2t_obs(int64_t nl, const int* __restri
   const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
   const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
   const double c = -k / (16.0 * M_PI * M_PI);  // norm = (0, c)
-  const double2* lc = loc + leaf * S;
+  const double2* lc = loc + (leaf - row0) * S;  // leaf rows start at the rank's first leaf
   for (int qd = lane; qd < quads; qd += 32) {
     const int i = qd / half, j = qd - i * half;
     const int64_t s1 = int64_t(i) * nphi + j, s2 = int64_t(n - 1 - i) * nphi + j;

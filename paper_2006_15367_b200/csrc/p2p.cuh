@@ -276,6 +276,136 @@ __global__ void __launch_bounds__(128, HFMM_P2P_MINB) k_p2p_sym2(const int2* __r
                                sym_scr, int64_t(pass) * sym_rows[i], leaf_start, x, y, z, q, pot, scratch, red);
 }
 
+// ---------------------------------------------------------------------------
+// Near field of leaves with <= 32 observers (configs 2 and 4: 4-8 particles
+// per leaf), one WARP per leaf.  ncu (config 4) showed the previous kernels
+// issue-bound -- ~60% of their instructions were not FP64: per-pair
+// self-pair masking, table-index clamping, four shared loads, and lanes
+// idled by power-of-two observer groups.  Here:
+//  * G = floor(32 / n_o) lanes per observer (any G, not only powers of two),
+//    reduced with a guarded shuffle tree;
+//  * sources are staged as (x, y, z, q_re) + q_im: two shared loads per pair;
+//  * the exact-zero self pair can only occur in the leaf itself, whose
+//    sources are a contiguous range of the staged list: only that range takes
+//    the masked pair; every other pair skips the mask and the index clamp
+//    (all lanes that compute hold a real observer, r' stays in the table);
+//  * two independent accumulators per lane (even / odd sources).
+template <bool TAB>
+__device__ __forceinline__ void p2p_pair_fast(double xo, double yo, double zo, const double4 s, double qim,
+                                              double& ar, double& ai, const double2* __restrict__ tab, int tmax) {
+  const double dx = xo - s.x, dy = yo - s.y, dz = zo - s.z;
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  double gr, gi;
+  if constexpr (TAB) green_tab_nc(r2, tab, gr, gi); else green_scaled(r2, gr, gi);
+  ar = fma(gr, s.w, fma(-gi, qim, ar));
+  ai = fma(gr, qim, fma(gi, s.w, ai));
+}
+
+constexpr int kTW = 64;  // sources staged per round (per warp)
+template <bool TAB>
+__global__ void __launch_bounds__(128) k_p2p_leaf2(int n_leaves, const int* __restrict__ leaves,
+                                                   const int64_t* __restrict__ leaf_start,
+                                                   const int64_t* __restrict__ near_off, const int* __restrict__ near,
+                                                   const double* __restrict__ centers, const double* __restrict__ x,
+                                                   const double* __restrict__ y, const double* __restrict__ z,
+                                                   const double2* __restrict__ q, double k, double2* __restrict__ pot,
+                                                   const double2* __restrict__ ptab = nullptr, int tmax = 0) {
+  __shared__ double4 sA[4][kTW];
+  __shared__ double sQ[4][kTW];
+  __shared__ int64_t spref[4][32], sbeg[4][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 4 + warp;
+  if (i >= n_leaves) return;  // whole warp
+  const int64_t leaf = leaves[i];
+  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
+  const int n_o = int(p1 - p0);
+  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
+  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
+  const int64_t nb = near_off[leaf];
+  const int nn = int(near_off[leaf + 1] - nb);
+  int64_t cnt = 0, beg = 0;
+  int self = 0;
+  if (lane < nn) {
+    const int lf = near[nb + lane];
+    beg = leaf_start[lf];
+    cnt = leaf_start[lf + 1] - beg;
+    self = lf == leaf;
+  }
+  int64_t incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t u = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += u;
+  }
+  const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+  const unsigned selfmask = __ballot_sync(0xffffffffu, self);
+  const int sl = selfmask ? __ffs(selfmask) - 1 : 0;
+  const int64_t self_b = selfmask ? __shfl_sync(0xffffffffu, incl - cnt, sl) : total;  // self range in the list
+  const int64_t self_e = selfmask ? self_b + n_o : total;
+  spref[warp][lane] = incl - cnt;  // lanes >= nn: total
+  sbeg[warp][lane] = beg;
+  const int G = n_o > 0 ? 32 / n_o : 32;
+  const int o = lane / G, sub = lane - o * G;
+  const bool valid = o < n_o;
+  const double xo = valid ? k * (x[p0 + o] - cx) : 0.0;
+  const double yo = valid ? k * (y[p0 + o] - cy) : 0.0;
+  const double zo = valid ? k * (z[p0 + o] - cz) : 0.0;
+  double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+  for (int64_t cb = 0; cb < total; cb += kTW) {
+    const int n = int(total - cb < kTW ? total - cb : kTW);
+    __syncwarp();
+    for (int t = lane; t < n; t += 32) {
+      const int64_t v = cb + t;
+      int lo = 0, hi = nn;  // largest j with spref[j] <= v
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (spref[warp][mid] <= v) lo = mid; else hi = mid;
+      }
+      const int64_t src = sbeg[warp][lo] + (v - spref[warp][lo]);
+      const double2 qq = q[src];
+      sA[warp][t] = make_double4(k * (x[src] - cx), k * (y[src] - cy), k * (z[src] - cz), qs * qq.x);
+      sQ[warp][t] = qs * qq.y;
+    }
+    __syncwarp();
+    if (valid) {
+      // [0, n) minus the self range [sb, se) of this chunk: two plain segments
+      const int sb = int(min(max(self_b - cb, int64_t(0)), int64_t(n)));
+      const int se = int(min(max(self_e - cb, int64_t(0)), int64_t(n)));
+#pragma unroll
+      for (int seg = 0; seg < 2; ++seg) {
+        const int lo = seg == 0 ? 0 : se, hi = seg == 0 ? sb : n;
+        int t = lo + sub;
+        for (; t + G < hi; t += 2 * G) {
+          p2p_pair_fast<TAB>(xo, yo, zo, sA[warp][t], sQ[warp][t], ar0, ai0, ptab, tmax);
+          p2p_pair_fast<TAB>(xo, yo, zo, sA[warp][t + G], sQ[warp][t + G], ar1, ai1, ptab, tmax);
+        }
+        if (t < hi) p2p_pair_fast<TAB>(xo, yo, zo, sA[warp][t], sQ[warp][t], ar0, ai0, ptab, tmax);
+      }
+      // the leaf's own particles: the exact-zero self pair is masked (operators.cpp:118)
+      for (int t = sb + sub; t < se; t += G) {
+        const double4 sa = sA[warp][t];
+        p2p_pair<TAB>(xo, yo, zo, sa.x, sa.y, sa.z, make_double2(sa.w, sQ[warp][t]), ar1, ai1, ptab, tmax);
+      }
+    }
+  }
+  double ar = ar0 + ar1, ai = ai0 + ai1;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {  // guarded tree over the G lanes of an observer
+    const double ur = __shfl_down_sync(0xffffffffu, ar, off);
+    const double ui = __shfl_down_sync(0xffffffffu, ai, off);
+    if (sub + off < G) {
+      ar += ur;
+      ai += ui;
+    }
+  }
+  if (valid && sub == 0) {
+    double2 cur = pot[p0 + o];
+    cur.x += ar;
+    cur.y += ai;
+    pot[p0 + o] = cur;
+  }
+}
+
 }  // namespace hfmm_b200
 
 #endif  // HFMM_B200_P2P_CUH
