@@ -217,7 +217,7 @@ void Engine::upload() {
   d_near_off = upload_vec(no);
   std::vector<int> nr(s.near.begin(), s.near.end());
   d_near = upload_vec(nr);
-  // P2P launch lists: own leaves by population (k_p2p<false> / <true>)
+  // P2P launch lists: own leaves by population (k_p2p_leaf2 for <= 32, k_p2p_sym2 above)
   {
     // tiny (<= 8: warp per leaf), small (<= 32: CTA per leaf), dense (symmetric)
     std::vector<int> tiny, small, dense;
@@ -603,7 +603,7 @@ void Engine::phase_m2m() {
                       oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
     if (rl.n_par == 0) continue;
     // 0. fused single-kernel pair (folded circles stay in shared memory)
-#if !defined(HFMM_NO_FZ) && !defined(HFMM_NO_FZ_M2M)
+#ifndef HFMM_NO_FZ
     if (!hook_no_rb_ && fz_pair(nc, np)) {
       launch_m2m_fz(rl, sms_, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up);
       ++launches_;
@@ -694,15 +694,6 @@ void Engine::phase_l2l(int lo, int hi) {
                       R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
                       oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
     if (rl.n_par == 0) continue;
-    // 0. fused single-kernel pair (narrow rows stay in shared memory)
-#if !defined(HFMM_NO_FZ) && !defined(HFMM_NO_FZ_L2L)
-    if (!hook_no_rb_ && fz_pair(nc, np)) {
-      launch_l2l_fz(rl, sms_, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn);
-      ++launches_;
-      ck(cudaGetLastError(), "k_l2l_fz");
-      continue;
-    }
-#endif
     // 1. compile-time-shaped streaming pairs
     if (!hook_no_rb_ && rb_pair(nc, np) &&
         launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn, d_tmp)) {
@@ -806,7 +797,7 @@ void Engine::phase_l2t() {
         else HFMM_L2TO(0);
 #undef HFMM_L2TO
         ++launches_;
-        if (n_sparse_ > 0) l2t_quads(unsigned((n_sparse_ + 3) / 4), 0, n_sparse_, d_sparse_leaves_);
+        if (n_sparse_ > 0) l2t_quads(unsigned((n_sparse_ + 3) / 4), leaf_b_, n_sparse_, d_sparse_leaves_);  // rows start at leaf_b_
       } else {
         l2t_quads(unsigned((nl + 3) / 4), leaf_b_, nl, nullptr);
       }
@@ -829,28 +820,6 @@ void Engine::near_start() {
   const int64_t cnt = part_e_ - part_b_;
   if (cnt > 0)
     ck(cudaMemsetAsync(d_pot_near + part_b_, 0, size_t(cnt) * sizeof(double2), st2_), "memset near");
-#ifdef HFMM_P2P_OLD
-  if (n_tiny_ > 0) {
-    if (d_ptab_)
-      k_p2p_small_w<true><<<unsigned((n_tiny_ + 3) / 4), 128, 0, st2_>>>(
-          n_tiny_, d_tiny_leaves_, d_leaf_start, d_near_off, d_near, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near,
-          d_ptab_, ptab_max_);
-    else
-      k_p2p_small_w<false><<<unsigned((n_tiny_ + 3) / 4), 128, 0, st2_>>>(
-          n_tiny_, d_tiny_leaves_, d_leaf_start, d_near_off, d_near, d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near);
-    ++launches_;
-  }
-  if (n_small_ > 0) {
-    if (d_ptab_)
-      k_p2p<false, true><<<unsigned(n_small_), 128, 0, st2_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near,
-                                                               d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near,
-                                                               d_ptab_, ptab_max_);
-    else
-      k_p2p<false><<<unsigned(n_small_), 128, 0, st2_>>>(d_small_leaves_, d_leaf_start, d_near_off, d_near,
-                                                         d.centers, d_x, d_y, d_z, d_q, s_.k, d_pot_near);
-    ++launches_;
-  }
-#else
   if (n_tiny_ + n_small_ > 0) {  // leaves with <= 32 particles: one warp per leaf
     const int nl = n_tiny_ + n_small_;
     if (d_ptab_)
@@ -863,7 +832,6 @@ void Engine::near_start() {
                                                                    d_pot_near);
     ++launches_;
   }
-#endif
   if (n_dense_ > 0) {
     for (int c = 3; c >= 0; --c) {
         if (p2p_items_n_[c] == 0) continue;

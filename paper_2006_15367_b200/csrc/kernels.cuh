@@ -431,182 +431,6 @@ __device__ __forceinline__ void p2p_stage(P2PShared& sh, int64_t cb, int n, cons
   }
 }
 
-template <bool DENSE, bool TAB = false>
-__global__ void __launch_bounds__(128) k_p2p(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
-                                             const int64_t* __restrict__ near_off, const int* __restrict__ near,
-                                             const double* __restrict__ centers, const double* __restrict__ x,
-                                             const double* __restrict__ y, const double* __restrict__ z,
-                                             const double2* __restrict__ q, double k, double2* __restrict__ pot,
-                                             const double2* __restrict__ ptab = nullptr, int tmax = 0) {
-  __shared__ P2PShared sh;
-  const double2* stab = ptab;  // small CTAs: the table is read through L1 (no staging)
-  const int64_t leaf = leaves[blockIdx.x];
-  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
-  const int n_o = int(p1 - p0);
-  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
-  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
-  const int64_t total = p2p_prepare(sh, leaf, leaf_start, near_off, near);
-  if (!DENSE) {
-    int G = 32;
-    while (G > 1 && G * n_o > int(blockDim.x)) G >>= 1;
-    const int o = threadIdx.x / G, j = threadIdx.x % G;
-    const bool valid = o < n_o;
-    const double xo = valid ? k * (x[p0 + o] - cx) : 1e300;
-    const double yo = valid ? k * (y[p0 + o] - cy) : 0.0;
-    const double zo = valid ? k * (z[p0 + o] - cz) : 0.0;
-    double ar = 0.0, ai = 0.0;
-    for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
-      const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
-      __syncthreads();
-      p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
-      __syncthreads();
-      if (valid)
-        for (int t = j; t < n; t += G)
-          p2p_pair<TAB>(xo, yo, zo, sh.sx[t], sh.sy[t], sh.sz[t], sh.sq[t], ar, ai, stab, tmax);
-    }
-    for (int off = G >> 1; off > 0; off >>= 1) {
-      ar += __shfl_down_sync(0xffffffffu, ar, off, G);
-      ai += __shfl_down_sync(0xffffffffu, ai, off, G);
-    }
-    if (valid && j == 0) {
-      double2 cur = pot[p0 + o];
-      cur.x += ar;
-      cur.y += ai;
-      pot[p0 + o] = cur;
-    }
-    return;
-  }
-  __shared__ double2 red[4][32 * kP2PObsPerLane];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-  for (int ob = 0; ob < n_o; ob += 32 * kP2PObsPerLane) {
-    const int no = min(n_o - ob, 32 * kP2PObsPerLane);
-    const int nc = (no + 31) >> 5;  // observer slots of this pass
-    double xo[kP2PObsPerLane], yo[kP2PObsPerLane], zo[kP2PObsPerLane];
-    double ar[kP2PObsPerLane], ai[kP2PObsPerLane];
-#pragma unroll
-    for (int c = 0; c < kP2PObsPerLane; ++c) {
-      const int o = lane + 32 * c;
-      const bool v = c < nc && o < no;
-      xo[c] = v ? k * (x[p0 + ob + o] - cx) : 1e300;
-      yo[c] = v ? k * (y[p0 + ob + o] - cy) : 0.0;
-      zo[c] = v ? k * (z[p0 + ob + o] - cz) : 0.0;
-      ar[c] = 0.0;
-      ai[c] = 0.0;
-    }
-    for (int64_t cb = 0; cb < total; cb += kP2PChunk) {
-      const int n = int(total - cb < kP2PChunk ? total - cb : kP2PChunk);
-      __syncthreads();
-      p2p_stage(sh, cb, n, x, y, z, q, cx, cy, cz, k, qs);
-      __syncthreads();
-      for (int t = warp; t < n; t += nwarp) {
-        const double px = sh.sx[t], py = sh.sy[t], pz = sh.sz[t];
-        const double2 qq = sh.sq[t];
-#pragma unroll
-        for (int c = 0; c < kP2PObsPerLane; ++c)
-          if (c < nc) p2p_pair<TAB>(xo[c], yo[c], zo[c], px, py, pz, qq, ar[c], ai[c], stab, tmax);
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < kP2PObsPerLane; ++c) red[warp][lane + 32 * c] = make_double2(ar[c], ai[c]);
-    __syncthreads();
-    for (int o = threadIdx.x; o < no; o += blockDim.x) {
-      double2 sum = red[0][o];
-      for (int w = 1; w < nwarp; ++w) {
-        sum.x += red[w][o].x;
-        sum.y += red[w][o].y;
-      }
-      double2 cur = pot[p0 + ob + o];
-      cur.x += sum.x;
-      cur.y += sum.y;
-      pot[p0 + ob + o] = cur;
-    }
-    __syncthreads();
-  }
-}
-
-// Small leaves (<= 32 observers), one WARP per leaf: the near leaves' prefix
-// sums come from a warp scan, sources are staged kSW at a time in warp-private
-// shared memory (__syncwarp only), G = 32 / n_o lanes share an observer.
-constexpr int kSW = 64;
-template <bool TAB = false>
-__global__ void __launch_bounds__(128) k_p2p_small_w(int n_small, const int* __restrict__ leaves,
-                                                     const int64_t* __restrict__ leaf_start,
-                                                     const int64_t* __restrict__ near_off, const int* __restrict__ near,
-                                                     const double* __restrict__ centers, const double* __restrict__ x,
-                                                     const double* __restrict__ y, const double* __restrict__ z,
-                                                     const double2* __restrict__ q, double k, double2* __restrict__ pot,
-                                                     const double2* __restrict__ ptab = nullptr, int tmax = 0) {
-  __shared__ double sx[4][kSW], sy[4][kSW], sz[4][kSW];
-  __shared__ double2 sq[4][kSW];
-  __shared__ int64_t spref[4][32], sbeg[4][32];
-  const double2* stab = ptab;  // small CTAs: the table is read through L1 (no staging)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * 4 + warp;
-  if (i >= n_small) return;  // whole warp
-  const int64_t leaf = leaves[i];
-  const int64_t p0 = leaf_start[leaf], p1 = leaf_start[leaf + 1];
-  const int n_o = int(p1 - p0);
-  const double cx = centers[3 * leaf], cy = centers[3 * leaf + 1], cz = centers[3 * leaf + 2];
-  const double qs = k * 0.079577471545947667884;  // k / (4 pi)
-  const int64_t nb = near_off[leaf];
-  const int nn = int(near_off[leaf + 1] - nb);
-  int64_t cnt = 0, beg = 0;
-  if (lane < nn) {
-    const int lf = near[nb + lane];
-    beg = leaf_start[lf];
-    cnt = leaf_start[lf + 1] - beg;
-  }
-  int64_t incl = cnt;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int64_t u = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += u;
-  }
-  const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
-  spref[warp][lane] = incl - cnt;  // lanes >= nn: total
-  sbeg[warp][lane] = beg;
-  int G = 32;
-  while (G > 1 && G * n_o > 32) G >>= 1;
-  const int o = lane / G, sub = lane - o * G;
-  const bool valid = o < n_o;
-  const double xo = valid ? k * (x[p0 + o] - cx) : 1e300;
-  const double yo = valid ? k * (y[p0 + o] - cy) : 0.0;
-  const double zo = valid ? k * (z[p0 + o] - cz) : 0.0;
-  double ar = 0.0, ai = 0.0;
-  for (int64_t cb = 0; cb < total; cb += kSW) {
-    const int n = int(total - cb < kSW ? total - cb : kSW);
-    __syncwarp();
-    for (int t = lane; t < n; t += 32) {
-      const int64_t v = cb + t;
-      int lo = 0, hi = nn;  // largest j with spref[j] <= v
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (spref[warp][mid] <= v) lo = mid; else hi = mid;
-      }
-      const int64_t src = sbeg[warp][lo] + (v - spref[warp][lo]);
-      sx[warp][t] = k * (x[src] - cx);
-      sy[warp][t] = k * (y[src] - cy);
-      sz[warp][t] = k * (z[src] - cz);
-      const double2 qq = q[src];
-      sq[warp][t] = make_double2(qs * qq.x, qs * qq.y);
-    }
-    __syncwarp();
-    if (valid)
-      for (int t = sub; t < n; t += G)
-        p2p_pair<TAB>(xo, yo, zo, sx[warp][t], sy[warp][t], sz[warp][t], sq[warp][t], ar, ai, stab, tmax);
-  }
-  for (int off = G >> 1; off > 0; off >>= 1) {
-    ar += __shfl_xor_sync(0xffffffffu, ar, off);
-    ai += __shfl_xor_sync(0xffffffffu, ai, off);
-  }
-  if (valid && sub == 0) {
-    double2 cur = pot[p0 + o];
-    cur.x += ar;
-    cur.y += ai;
-    pot[p0 + o] = cur;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Adds the scratch rows other dense leaves wrote for leaf B (fixed order).
 __global__ void k_p2p_gather(const int* __restrict__ leaves, const int64_t* __restrict__ leaf_start,
