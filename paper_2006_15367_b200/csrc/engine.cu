@@ -166,6 +166,19 @@ void Engine::setup_interp(DevLevel& P, const DevLevel& C, const LevelData& tp, c
   P.dn_th_v = upload_vec(dth.v);
   P.dn_phi_B = upload_vec(dphi.B);
   P.dn_phi_v = upload_vec(dphi.v);
+  // Even / odd form of the theta passes, with the fold / unfold baked into the
+  // phi matrices (interp.hpp): what the fused and compile-time-shaped kernels take.
+  if (nc % 2 == 0 && np % 2 == 0 && (fz_pair(nc, np) || rb_pair(nc, np))) {
+    const EvenOdd ue = even_odd(uth, 2 * nc, 2 * np), de = even_odd(dth, 2 * np, 2 * nc);
+    const RealRank1 uf = fold_columns(uphi, nc, np), du = unfold_rows(dphi, np, nc);
+    P.up_phi_Bf = upload_vec(uf.B);
+    P.up_th_Be = upload_vec(ue.B);
+    P.up_th_ve = upload_vec(ue.v);
+    P.dn_th_Be = upload_vec(de.B);
+    P.dn_th_ve = upload_vec(de.v);
+    P.dn_phi_Bu = upload_vec(du.B);
+    P.dn_phi_vu = upload_vec(du.v);
+  }
   // Two-stage large-grid plans.
   {
     const int ldf = P.up_th[2];
@@ -605,7 +618,7 @@ void Engine::phase_m2m() {
     // 0. fused single-kernel pair (folded circles stay in shared memory)
 #ifndef HFMM_NO_FZ
     if (!hook_no_rb_ && fz_pair(nc, np)) {
-      launch_m2m_fz(rl, sms_, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up);
+      launch_m2m_fz(rl, sms_, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up);
       ++launches_;
       ck(cudaGetLastError(), "k_m2m_fz");
       continue;
@@ -613,7 +626,7 @@ void Engine::phase_m2m() {
 #endif
     // 1. compile-time-shaped streaming pairs (the BASELINE leaf-side pairs)
     if (!hook_no_rb_ && rb_pair(nc, np) &&
-        launch_m2m_rb(nc, np, rl, C.mp, P.mp, P.up_phi_B, P.up_phi_v, P.up_th_B, P.up_th_v, P.shift_up, d_tmp)) {
+        launch_m2m_rb(nc, np, rl, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up, d_tmp)) {
       launches_ += 2;
       ck(cudaGetLastError(), "k_m2m_rb");
       continue;
@@ -696,7 +709,7 @@ void Engine::phase_l2l(int lo, int hi) {
     if (rl.n_par == 0) continue;
     // 1. compile-time-shaped streaming pairs
     if (!hook_no_rb_ && rb_pair(nc, np) &&
-        launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_B, P.dn_th_v, P.dn_phi_B, P.dn_phi_v, P.shift_dn, d_tmp)) {
+        launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_Be, P.dn_th_ve, P.dn_phi_Bu, P.dn_phi_vu, P.shift_dn, d_tmp)) {
       launches_ += 2;
       ck(cudaGetLastError(), "k_l2l_rb");
       continue;

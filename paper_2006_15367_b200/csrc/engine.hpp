@@ -59,6 +59,14 @@ struct DevLevel {
   double* dn_th_v = nullptr;
   double* dn_phi_B = nullptr;
   double* dn_phi_v = nullptr;
+  // even / odd theta passes (fused and compile-time-shaped kernels; interp.hpp)
+  double* up_phi_Bf = nullptr;  // phi matrix with the (e, o) fold in its columns
+  double* up_th_Be = nullptr;   // [Be ; Bo]
+  double* up_th_ve = nullptr;
+  double* dn_th_Be = nullptr;
+  double* dn_th_ve = nullptr;
+  double* dn_phi_Bu = nullptr;  // phi matrix with the (e, o) unfold in its rows
+  double* dn_phi_vu = nullptr;
 };
 
 // Per-rank lists for one level acting as parent (distributed mode).

@@ -122,6 +122,98 @@ inline RealRank1 real_rank1(int64_t n_in, double s_in, int64_t n_out, double s_o
   return out;
 }
 
+// ---------------------------------------------------------------------------
+// Even / odd halving of the theta passes.
+//
+// The theta pass resamples a folded great circle of n_in = 2 n_c points at
+// (i + 1/2) 2 pi / n_in to n_out = 2 n_p points.  Both point sets are symmetric
+// under t -> -t (i <-> n_in - 1 - i, j <-> n_out - 1 - j) and the kernel is a
+// function of the angle difference with an even real part, so the real matrix
+// is centrosymmetric: R[J j][J i] = R[j][i].  With x_e = x + J x and
+// x_o = x - J x (first halves),
+//     y[j]   = Ye[j] + Yo[j],      Ye = Be x_e,  Be[j][i] = (R[j][i] + R[j][J i]) / 2,
+//     y[J j] = Ye[j] - Yo[j],      Yo = Bo x_o,  Bo[j][i] = (R[j][i] - R[j][J i]) / 2,
+// for j < n_out / 2: two half-size products, half the multiply-adds.  The
+// rank-1 part i u (v . x) splits the same way (u into its symmetric and
+// antisymmetric parts, v . x into v_e . x_e + v_o . x_o).
+//
+// Layout (B operand of the DMMA passes): B is (2 KH4) x NH row-major,
+// KH4 = round_up(n_in / 2 + 1, 4), NH = round_up(n_out / 2, 8): rows [0, KH4)
+// hold Be (row n_in / 2 = symmetric part of u), rows [KH4, 2 KH4) hold Bo
+// (row KH4 + n_in / 2 = antisymmetric part of u); v has 2 KH4 entries, laid
+// out like the rows.
+struct EvenOdd {
+  int KH4 = 0, NH = 0;
+  std::vector<double> B;  // 2 KH4 x NH
+  std::vector<double> v;  // 2 KH4
+};
+
+inline EvenOdd even_odd(const RealRank1& m, int64_t n_in, int64_t n_out) {
+  if (n_in % 2 || n_out % 2) throw std::logic_error("even_odd: odd circle length");
+  const int64_t hi = n_in / 2, ho = n_out / 2;
+  auto Bm = [&](int64_t k, int64_t n) { return m.B[size_t(k) * size_t(m.N) + size_t(n)]; };
+  double amax = 0;
+  for (int64_t k = 0; k < n_in; ++k)
+    for (int64_t n = 0; n < n_out; ++n) amax = std::max(amax, std::fabs(Bm(k, n)));
+  for (int64_t k = 0; k < n_in; ++k)
+    for (int64_t n = 0; n < n_out; ++n)
+      if (std::fabs(Bm(k, n) - Bm(n_in - 1 - k, n_out - 1 - n)) > 1e-13 * amax)
+        throw std::logic_error("even_odd: the theta map is not centrosymmetric");
+  EvenOdd out;
+  out.KH4 = int((hi + 1 + 3) / 4 * 4);
+  out.NH = int((ho + 7) / 8 * 8);
+  out.B.assign(size_t(2 * out.KH4) * size_t(out.NH), 0.0);
+  out.v.assign(size_t(2 * out.KH4), 0.0);
+  for (int64_t n = 0; n < ho; ++n) {
+    for (int64_t k = 0; k < hi; ++k) {
+      out.B[size_t(k) * out.NH + size_t(n)] = 0.5 * (Bm(k, n) + Bm(n_in - 1 - k, n));
+      out.B[size_t(out.KH4 + k) * out.NH + size_t(n)] = 0.5 * (Bm(k, n) - Bm(n_in - 1 - k, n));
+    }
+    out.B[size_t(hi) * out.NH + size_t(n)] = 0.5 * (Bm(n_in, n) + Bm(n_in, n_out - 1 - n));
+    out.B[size_t(out.KH4 + hi) * out.NH + size_t(n)] = 0.5 * (Bm(n_in, n) - Bm(n_in, n_out - 1 - n));
+  }
+  for (int64_t k = 0; k < hi; ++k) {
+    out.v[size_t(k)] = 0.5 * (m.v[size_t(k)] + m.v[size_t(n_in - 1 - k)]);
+    out.v[size_t(out.KH4 + k)] = 0.5 * (m.v[size_t(k)] - m.v[size_t(n_in - 1 - k)]);
+  }
+  return out;
+}
+
+// M2M phi pass with the fold into (x_e, x_o) baked into its output columns:
+// column 2 p + h of the result is column p of M plus (h = 0) or minus (h = 1)
+// column p + n_out / 2 -- the two phi samples that land on circle p's
+// positions i and J i.  Same K, N as the plain map.
+inline RealRank1 fold_columns(const RealRank1& m, int64_t n_in, int64_t n_out) {
+  RealRank1 out = m;
+  const int64_t half = n_out / 2;
+  for (int64_t k = 0; k <= n_in; ++k)
+    for (int64_t p = 0; p < half; ++p) {
+      const double a = m.B[size_t(k) * m.N + size_t(p)], b = m.B[size_t(k) * m.N + size_t(p + half)];
+      out.B[size_t(k) * m.N + size_t(2 * p)] = a + b;
+      out.B[size_t(k) * m.N + size_t(2 * p + 1)] = a - b;
+    }
+  return out;
+}
+
+// L2L phi pass reading (Ye, Yo) pairs: input column 2 p + h stands for
+// Ye_p (h = 0) or Yo_p (h = 1), where the plain inputs are x[p] = Ye + Yo and
+// x[p + n_in / 2] = Ye - Yo; rows of B and entries of v combine accordingly.
+inline RealRank1 unfold_rows(const RealRank1& m, int64_t n_in, int64_t n_out) {
+  RealRank1 out = m;
+  const int64_t half = n_in / 2;
+  (void)n_out;
+  for (int64_t p = 0; p < half; ++p) {
+    for (int64_t n = 0; n < m.N; ++n) {
+      const double a = m.B[size_t(p) * m.N + size_t(n)], b = m.B[size_t(p + half) * m.N + size_t(n)];
+      out.B[size_t(2 * p) * m.N + size_t(n)] = a + b;
+      out.B[size_t(2 * p + 1) * m.N + size_t(n)] = a - b;
+    }
+    out.v[size_t(2 * p)] = m.v[size_t(p)] + m.v[size_t(p + half)];
+    out.v[size_t(2 * p + 1)] = m.v[size_t(p)] - m.v[size_t(p + half)];
+  }
+  return out;
+}
+
 }  // namespace hfmm_b200
 
 #endif

@@ -26,7 +26,7 @@ __host__ __device__ constexpr int pad4mod8(int x) { return x + ((4 - x % 8) + 8)
 template <int NC, int NP>
 struct Lay {
   using D = rb::Dims<NC, NP>;
-  // M2M: F[c][p][ii] (c = child slot, p < HALF, ii < LDF), child stride CSF
+  // M2M: F[c][p][..] (c = child slot, p < HALF; x_e at [0, NC), x_o at [4 UTH_KH, ..)), child stride CSF
   static constexpr int CSF = pad4mod8(D::HALF * D::LDF);
   static constexpr int BPHI = D::UPHI_K * D::UPHI_LDB, BTH = D::UTH_K * D::UTH_LDB;  // doubles
   static constexpr int M2M_SMEM = (BPHI + BTH) * 8 + 8 * CSF * 16;
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(fz::kThreads, 2) k_m2m_fz(int n_par, const int
   using D = rb::Dims<NC, NP>;
   using Y = fz::Lay<NC, NP>;
   constexpr int KSP = D::UPHI_K / 4, NTP = D::UPHI_N / 8;
-  constexpr int KST = D::UTH_K / 4, NTT = D::UTH_N / 8, HALF = D::HALF, SP = D::SP, SC = D::SC;
+  constexpr int HALF = D::HALF, SP = D::SP, SC = D::SC;
   extern __shared__ __align__(16) double fz_smem[];
   double* Bp = fz_smem;
   double* Bt = Bp + Y::BPHI;
@@ -97,12 +97,8 @@ __global__ void __launch_bounds__(fz::kThreads, 2) k_m2m_fz(int n_par, const int
         for (int jn = 0; jn < NTP; ++jn)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
-            const int n = 8 * jn + 2 * tq + q;
-            if (n < NP) {
-              const int p = n < HALF ? n : n - HALF;
-              const int ii = n < HALF ? i : 2 * NC - 1 - i;
-              Fc[p * D::LDF + ii] = make_double2(cre[jn][q], cim[jn][q]);
-            }
+            const int n = 8 * jn + 2 * tq + q;  // column 2 p + h: circle p, part e / o
+            if (n < NP) Fc[(n >> 1) * D::LDF + (n & 1) * 4 * D::UTH_KH + i] = make_double2(cre[jn][q], cim[jn][q]);
           }
       }
     }
@@ -113,54 +109,7 @@ __global__ void __launch_bounds__(fz::kThreads, 2) k_m2m_fz(int n_par, const int
     double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
     for (int p = warp; p < HALF; p += NW) {
       const double2* frow = Fs + (ok ? g : 0) * Y::CSF + p * D::LDF;
-      double are[KST], aim[KST];
-#pragma unroll
-      for (int kk = 0; kk < KST; ++kk) {
-        const int k = 4 * kk + tq;
-        const double2 fv = (ok && k < 2 * NC) ? frow[k] : make_double2(0.0, 0.0);
-        are[kk] = fv.x;
-        aim[kk] = fv.y;
-      }
-      rb::rank1_inject<KST, 2 * NC>(are, aim, vth);
-      constexpr int NTC = 4;
-#pragma unroll
-      for (int j0 = 0; j0 < NTT; j0 += NTC) {
-        double2 shv[NTC][2];
-#pragma unroll
-        for (int jc = 0; jc < NTC; ++jc)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int n = 8 * (j0 + jc) + 2 * tq + q;
-            const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
-            shv[jc][q] = (ok && j0 + jc < NTT && n < 2 * NP) ? __ldg(sh + s) : make_double2(0.0, 0.0);
-          }
-        double cre[NTC][2] = {}, cim[NTC][2] = {};
-        const double* bp = Bt + tq * D::UTH_LDB + g + 8 * j0;
-#pragma unroll
-        for (int kk = 0; kk < KST; ++kk)
-#pragma unroll
-          for (int jc = 0; jc < NTC; ++jc)
-            if (j0 + jc < NTT) {
-              const double b = bp[4 * kk * D::UTH_LDB + 8 * jc];
-              dmma884(cre[jc][0], cre[jc][1], are[kk], b);
-              dmma884(cim[jc][0], cim[jc][1], aim[kk], b);
-            }
-        double v[16];
-#pragma unroll
-        for (int jc = 0; jc < NTC; ++jc)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const double2 f = shv[jc][q];
-            v[(2 * jc + q) * 2] = cre[jc][q] * f.x - cim[jc][q] * f.y;
-            v[(2 * jc + q) * 2 + 1] = cre[jc][q] * f.y + cim[jc][q] * f.x;
-          }
-        const double2 val = rb::child_sum_scatter(v);
-        const int jt = j0 + (g >> 1), n = 8 * jt + 2 * tq + (g & 1);
-        if (jt < NTT && n < 2 * NP) {
-          const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
-          out[s] = val;
-        }
-      }
+      rb::m2m_theta_item<NC, NP>([&](int k) { return frow[k]; }, ok, sh, out, p, Bt, vth);
     }
     __syncthreads();
   }

@@ -15,7 +15,14 @@
 //    (M2M: folded circles F; L2L: narrow rows Nb);
 //  * the M2M theta pass puts the 8 child slots of a parent in the 8 rows of a
 //    tile, so the child sum is a 3-level shuffle and every parent sample is
-//    written exactly once (no shared accumulator).
+//    written exactly once (no shared accumulator);
+//  * the theta passes of the compile-time-shaped kernels run in the even / odd
+//    form (interp.hpp:even_odd): the theta map of a folded great circle is
+//    centrosymmetric, so it splits into two half-size products on
+//    x_e = x + Jx and x_o = x - Jx -- 80 DMMA per (18, 28) circle tile instead
+//    of 140.  The fold is baked into the columns of the M2M phi matrix and the
+//    unfold into the rows of the L2L phi matrix (fold_columns / unfold_rows),
+//    so the phi passes deliver and consume (e, o) pairs at no cost.
 #ifndef HFMM_B200_INTERP_RB_CUH
 #define HFMM_B200_INTERP_RB_CUH
 
@@ -102,24 +109,129 @@ __device__ __forceinline__ void tile_mma(const double (&are)[KS], const double (
     }
 }
 
+// Rank-1 column of the even / odd theta passes: alpha = v_e . x_e + v_o . x_o
+// (v laid out like the B rows: v_o at 4 KH), injected as i alpha at column KIN
+// of both halves (the B rows there hold the symmetric / antisymmetric part of u).
+template <int KH, int KIN>
+__device__ __forceinline__ void rank1_inject_eo(double (&er)[KH], double (&ei)[KH], double (&qr)[KH], double (&qi)[KH],
+                                                const double* __restrict__ v) {
+  const int tq = threadIdx.x & 3;
+  double sr = 0.0, si = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < KH; ++kk) {
+    const int k = 4 * kk + tq;
+    if (k < KIN) {
+      const double ve = __ldg(v + k), vo = __ldg(v + 4 * KH + k);
+      sr = fma(ve, er[kk], sr);
+      si = fma(ve, ei[kk], si);
+      sr = fma(vo, qr[kk], sr);
+      si = fma(vo, qi[kk], si);
+    }
+  }
+  sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+  si += __shfl_xor_sync(0xffffffffu, si, 1);
+  sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+  si += __shfl_xor_sync(0xffffffffu, si, 2);
+  constexpr int KR = KIN / 4, TR = KIN % 4;
+  static_assert(KR < KH, "rank-1 column outside the padded K");
+  if (tq == TR) {
+    er[KR] = qr[KR] = -si;  // Re(i alpha)
+    ei[KR] = qi[KR] = sr;   // Im(i alpha)
+  }
+}
+
 template <int NC, int NP>
 struct Dims {
   static constexpr int HALF = NP / 2, SC = NC * NC, SP = NP * NP;
-  // M2M phi: X (NC x NC) rows -> NP outputs; theta: folded circles 2NC -> 2NP
+  // M2M phi: X (NC x NC) rows -> NP outputs (column 2 p + h: circle p, part e / o);
+  // theta, even / odd form: x_e, x_o (NC each, + rank-1 column) -> Ye, Yo (NP each)
   static constexpr int UPHI_K = r4(NC + 1), UPHI_N = r8(NP), UPHI_LDB = ldb(UPHI_N);
-  static constexpr int UTH_K = r4(2 * NC + 1), UTH_N = r8(2 * NP), UTH_LDB = ldb(UTH_N);
-  static constexpr int LDF = UTH_K;  // F scratch row stride (complex): the theta pass's K
-  // L2L theta: 2NP -> 2NC; phi: NP -> NC
-  static constexpr int DTH_K = r4(2 * NP + 1), DTH_N = r8(2 * NC), DTH_LDB = ldb(DTH_N);
+  static constexpr int UTH_KH = r4(NC + 1) / 4;  // k-steps per half
+  static constexpr int UTH_K = 8 * UTH_KH, UTH_N = r8(NP), UTH_LDB = ldb(UTH_N);  // B rows: [Be ; Bo]
+  static constexpr int LDF = UTH_K;  // F scratch row stride (complex): x_e at 0, x_o at 4 UTH_KH
+  // L2L theta, even / odd form: NP + NP -> NC + NC; phi: NP (pairs Ye, Yo) -> NC
+  static constexpr int DTH_KH = r4(NP + 1) / 4;
+  static constexpr int DTH_K = 8 * DTH_KH, DTH_N = r8(NC), DTH_LDB = ldb(DTH_N);
   static constexpr int DPHI_K = r4(NP + 1), DPHI_N = r8(NC), DPHI_LDB = ldb(DPHI_N);
   static constexpr int LDN = DPHI_K;  // Nb scratch row stride (complex): the phi pass's K
 };
 
+// M2M theta pass of one work item (parent, circle p), even / odd form: tile
+// rows = the parent's 8 child slots; ld(k) reads element k of the lane's F row
+// (x_e at [0, NC), x_o at [4 KH, 4 KH + NC)).  Ye +- Yo are the circle's front
+// (theta row n, column p) and back (column p + HALF) samples; both get their
+// shift factor and go through one child-sum reduce-scatter per 2 n8 tiles.
+template <int NC, int NP, class Ld>
+__device__ __forceinline__ void m2m_theta_item(Ld ld, bool ok, const double2* __restrict__ sh, double2* __restrict__ out,
+                                               int p, const double* __restrict__ Bt, const double* __restrict__ vth) {
+  using D = Dims<NC, NP>;
+  constexpr int KH = D::UTH_KH, NT = D::UTH_N / 8, HALF = D::HALF, LDB = D::UTH_LDB;
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  double er[KH], ei[KH], qr[KH], qi[KH];
+#pragma unroll
+  for (int kk = 0; kk < KH; ++kk) {
+    const int k = 4 * kk + tq;
+    const bool in = ok && k < NC;
+    const double2 e = in ? ld(k) : make_double2(0.0, 0.0);
+    const double2 o = in ? ld(4 * KH + k) : make_double2(0.0, 0.0);
+    er[kk] = e.x;
+    ei[kk] = e.y;
+    qr[kk] = o.x;
+    qi[kk] = o.y;
+  }
+  rank1_inject_eo<KH, NC>(er, ei, qr, qi, vth);
+  constexpr int NTC = 2;
+#pragma unroll
+  for (int j0 = 0; j0 < NT; j0 += NTC) {
+    double2 shf[NTC][2], shb[NTC][2];
+#pragma unroll
+    for (int jc = 0; jc < NTC; ++jc)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int n = 8 * (j0 + jc) + 2 * tq + q;
+        const bool live = ok && j0 + jc < NT && n < NP;
+        shf[jc][q] = live ? __ldg(sh + n * NP + p) : make_double2(0.0, 0.0);
+        shb[jc][q] = live ? __ldg(sh + n * NP + p + HALF) : make_double2(0.0, 0.0);
+      }
+    double cer[NTC][2] = {}, cei[NTC][2] = {}, cqr[NTC][2] = {}, cqi[NTC][2] = {};
+    const double* bp = Bt + tq * LDB + g + 8 * j0;
+#pragma unroll
+    for (int kk = 0; kk < KH; ++kk)
+#pragma unroll
+      for (int jc = 0; jc < NTC; ++jc)
+        if (j0 + jc < NT) {
+          const double be = bp[4 * kk * LDB + 8 * jc];
+          dmma884(cer[jc][0], cer[jc][1], er[kk], be);
+          dmma884(cei[jc][0], cei[jc][1], ei[kk], be);
+          const double bo = bp[4 * (KH + kk) * LDB + 8 * jc];
+          dmma884(cqr[jc][0], cqr[jc][1], qr[kk], bo);
+          dmma884(cqi[jc][0], cqi[jc][1], qi[kk], bo);
+        }
+    double v[16];  // child_sum_scatter slots: front tiles 0, 1, then back tiles 0, 1
+#pragma unroll
+    for (int jc = 0; jc < NTC; ++jc)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double fr = cer[jc][q] + cqr[jc][q], fi = cei[jc][q] + cqi[jc][q];
+        const double br = cer[jc][q] - cqr[jc][q], bi = cei[jc][q] - cqi[jc][q];
+        const double2 f = shf[jc][q], b = shb[jc][q];
+        v[(2 * jc + q) * 2] = fr * f.x - fi * f.y;
+        v[(2 * jc + q) * 2 + 1] = fr * f.y + fi * f.x;
+        v[(2 * (NTC + jc) + q) * 2] = br * b.x - bi * b.y;
+        v[(2 * (NTC + jc) + q) * 2 + 1] = br * b.y + bi * b.x;
+      }
+    const double2 val = child_sum_scatter(v);
+    const int slot = g >> 1, back = slot >= NTC, jt = j0 + slot - back * NTC, n = 8 * jt + 2 * tq + (g & 1);
+    if (jt < NT && n < NP) out[n * NP + p + back * HALF] = val;
+  }
+}
+
 }  // namespace rb
 
 // ---------------------------------------------------------------------------
-// M2M stage 1: phi pass of every child row -> folded circles F[j][p][ii]
-// (j = position in the children array, ii < 2 NC; columns >= 2 NC unused).
+// M2M stage 1: phi pass of every child row -> folded circles in (e, o) form,
+// F[j][p][..] (j = position in the children array): x_e[i] at i, x_o[i] at
+// 4 UTH_KH + i (the phi matrix's column 2 p + h carries part h of circle p).
 template <int NC, int NP>
 __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_phi_rb(int64_t nch, const int* __restrict__ children,
                                                                 const double2* __restrict__ mp_c,
@@ -158,11 +270,7 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_phi_rb(int64_t nch, con
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int n = 8 * jn + 2 * tq + q;
-          if (n < NP) {
-            const int p = n < HALF ? n : n - HALF;
-            const int ii = n < HALF ? i : 2 * NC - 1 - i;
-            Fj[p * D::LDF + ii] = make_double2(cre[jn][q], cim[jn][q]);
-          }
+          if (n < NP) Fj[(n >> 1) * D::LDF + (n & 1) * 4 * D::UTH_KH + i] = make_double2(cre[jn][q], cim[jn][q]);
         }
     }
   }
@@ -181,10 +289,10 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, con
                                                                   const double2* __restrict__ shift_up,
                                                                   double2* __restrict__ mp_p) {
   using D = rb::Dims<NC, NP>;
-  constexpr int KS = D::UTH_K / 4, NT = D::UTH_N / 8, HALF = D::HALF, SP = D::SP;
+  constexpr int HALF = D::HALF, SP = D::SP;
   extern __shared__ __align__(16) double Bsm[];
   rb::stage_b<D::UTH_K, D::UTH_N, D::UTH_LDB>(Bsm, B);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2;
   const int64_t items = int64_t(n_par) * HALF;
   for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
        it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
@@ -193,58 +301,8 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, con
     const bool ok = g < nchp;
     const double2* frow = F + (int64_t(cb + (ok ? g : 0)) * HALF + p) * D::LDF;
     const double2* sh = shift_up + int64_t(ok ? oct_c[children[cb + g]] : 0) * SP;
-    double are[KS], aim[KS];
-#pragma unroll
-    for (int kk = 0; kk < KS; ++kk) {
-      const int k = 4 * kk + tq;
-      const double2 fv = (ok && k < 2 * NC) ? __ldg(frow + k) : make_double2(0.0, 0.0);
-      are[kk] = fv.x;
-      aim[kk] = fv.y;
-    }
-    rb::rank1_inject<KS, 2 * NC>(are, aim, v);
     double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
-    // N in chunks of 4 n8 tiles (A stays in registers): shift factors of the
-    // chunk's outputs are loaded ahead of its DMMAs; the child sum is one
-    // reduce-scatter per chunk (child_sum_scatter).
-    constexpr int NTC = 4;
-#pragma unroll
-    for (int j0 = 0; j0 < NT; j0 += NTC) {
-      double2 shv[NTC][2];
-#pragma unroll
-      for (int jc = 0; jc < NTC; ++jc)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int n = 8 * (j0 + jc) + 2 * tq + q;
-          const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
-          shv[jc][q] = (ok && j0 + jc < NT && n < 2 * NP) ? __ldg(sh + s) : make_double2(0.0, 0.0);
-        }
-      double cre[NTC][2] = {}, cim[NTC][2] = {};
-      const double* bp = Bsm + tq * D::UTH_LDB + g + 8 * j0;
-#pragma unroll
-      for (int kk = 0; kk < KS; ++kk)
-#pragma unroll
-        for (int jc = 0; jc < NTC; ++jc)
-          if (j0 + jc < NT) {
-            const double b = bp[4 * kk * D::UTH_LDB + 8 * jc];
-            dmma884(cre[jc][0], cre[jc][1], are[kk], b);
-            dmma884(cim[jc][0], cim[jc][1], aim[kk], b);
-          }
-      double v[16];
-#pragma unroll
-      for (int jc = 0; jc < NTC; ++jc)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const double2 f = shv[jc][q];
-          v[(2 * jc + q) * 2] = cre[jc][q] * f.x - cim[jc][q] * f.y;
-          v[(2 * jc + q) * 2 + 1] = cre[jc][q] * f.y + cim[jc][q] * f.x;
-        }
-      const double2 val = rb::child_sum_scatter(v);
-      const int jt = j0 + (g >> 1), n = 8 * jt + 2 * tq + (g & 1);
-      if (jt < NT && n < 2 * NP) {
-        const int s = n < NP ? n * NP + p : (2 * NP - 1 - n) * NP + p + HALF;
-        out[s] = val;
-      }
-    }
+    rb::m2m_theta_item<NC, NP>([&](int k) { return __ldg(frow + k); }, ok, sh, out, p, Bsm, v);
   }
 }
 
@@ -264,7 +322,7 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_theta_rb(int n_par, con
                                                                   const double2* __restrict__ shift_dn,
                                                                   double2* __restrict__ Nb) {
   using D = rb::Dims<NC, NP>;
-  constexpr int KS = D::DTH_K / 4, NT = D::DTH_N / 8, HALF = D::HALF, SP = D::SP;
+  constexpr int KH = D::DTH_KH, NT = D::DTH_N / 8, HALF = D::HALF, SP = D::SP, LDB = D::DTH_LDB;
   extern __shared__ __align__(16) double Bsm[];
   rb::stage_b<D::DTH_K, D::DTH_N, D::DTH_LDB>(Bsm, B);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
@@ -277,44 +335,54 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_theta_rb(int n_par, con
     const bool ok = c < nchp;
     const double2* L = loc_p + int64_t(plist ? plist[par] : par) * SP;
     const double2* sh = shift_dn + int64_t(ok ? oct_c[children[cb + c]] : 0) * SP;
-    double are[KS], aim[KS];
+    // even / odd parts of the shifted circle: front sample (row k, column p)
+    // plus / minus back sample (row k, column p + HALF)
+    double er[KH], ei[KH], qr[KH], qi[KH];
 #pragma unroll
-    for (int kk = 0; kk < KS; ++kk) {
+    for (int kk = 0; kk < KH; ++kk) {
       const int k = 4 * kk + tq;
-      double2 f = make_double2(0.0, 0.0);
-      if (ok && k < 2 * NP) {
-        const int s = k < NP ? k * NP + p : (2 * NP - 1 - k) * NP + p + HALF;
+      double2 f = make_double2(0.0, 0.0), b = f;
+      if (ok && k < NP) {
+        const int s = k * NP + p;
         f = cmul(__ldg(L + s), __ldg(sh + s));
+        b = cmul(__ldg(L + s + HALF), __ldg(sh + s + HALF));
       }
-      are[kk] = f.x;
-      aim[kk] = f.y;
+      er[kk] = f.x + b.x;
+      ei[kk] = f.y + b.y;
+      qr[kk] = f.x - b.x;
+      qi[kk] = f.y - b.y;
     }
-    rb::rank1_inject<KS, 2 * NP>(are, aim, v);
+    rb::rank1_inject_eo<KH, NP>(er, ei, qr, qi, v);
     double2* Nc = Nb + int64_t(cb + (ok ? c : 0)) * NC * D::LDN;
-    constexpr int NTC = 4;
+    constexpr int NTC = 2;
 #pragma unroll
     for (int j0 = 0; j0 < NT; j0 += NTC) {
-      double cre[NTC][2] = {}, cim[NTC][2] = {};
-      const double* bp = Bsm + tq * D::DTH_LDB + g + 8 * j0;
+      double cer[NTC][2] = {}, cei[NTC][2] = {}, cqr[NTC][2] = {}, cqi[NTC][2] = {};
+      const double* bp = Bsm + tq * LDB + g + 8 * j0;
 #pragma unroll
-      for (int kk = 0; kk < KS; ++kk)
+      for (int kk = 0; kk < KH; ++kk)
 #pragma unroll
         for (int jc = 0; jc < NTC; ++jc)
           if (j0 + jc < NT) {
-            const double b = bp[4 * kk * D::DTH_LDB + 8 * jc];
-            dmma884(cre[jc][0], cre[jc][1], are[kk], b);
-            dmma884(cim[jc][0], cim[jc][1], aim[kk], b);
+            const double be = bp[4 * kk * LDB + 8 * jc];
+            dmma884(cer[jc][0], cer[jc][1], er[kk], be);
+            dmma884(cei[jc][0], cei[jc][1], ei[kk], be);
+            const double bo = bp[4 * (KH + kk) * LDB + 8 * jc];
+            dmma884(cqr[jc][0], cqr[jc][1], qr[kk], bo);
+            dmma884(cqi[jc][0], cqi[jc][1], qi[kk], bo);
           }
       if (ok) {
+        // theta row n of the child: (Ye, Yo) of circle p at columns 2 p, 2 p + 1
+        // (the phi matrix's rows undo the split, interp.hpp:unfold_rows)
 #pragma unroll
         for (int jc = 0; jc < NTC; ++jc)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int n = 8 * (j0 + jc) + 2 * tq + q;
-            if (j0 + jc < NT && n < 2 * NC) {
-              const int row = n < NC ? n : 2 * NC - 1 - n;
-              const int col = n < NC ? p : p + HALF;
-              Nc[row * D::LDN + col] = make_double2(cre[jc][q], cim[jc][q]);
+            if (j0 + jc < NT && n < NC) {
+              double2* d = Nc + n * D::LDN + 2 * p;
+              d[0] = make_double2(cer[jc][q], cei[jc][q]);
+              d[1] = make_double2(cqr[jc][q], cqi[jc][q]);
             }
           }
       }
@@ -666,7 +734,9 @@ inline bool rb_pair(int nc, int np) {
   return false;
 }
 // complex elements of the M2M F scratch / L2L Nb scratch for nch children
-inline size_t rb_m2m_scratch(int64_t nch, int nc, int np) { return size_t(nch) * size_t(np / 2) * size_t(rb::r4(2 * nc + 1)); }
+inline size_t rb_m2m_scratch(int64_t nch, int nc, int np) {
+  return size_t(nch) * size_t(np / 2) * size_t(std::max(rb::r4(2 * nc + 1), 2 * rb::r4(nc + 1)));
+}
 inline size_t rb_l2l_scratch(int64_t nch, int nc, int np) { return size_t(nch) * size_t(nc) * size_t(rb::r4(np + 1)); }
 
 struct RbLaunch {

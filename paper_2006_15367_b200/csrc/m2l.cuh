@@ -30,7 +30,11 @@ constexpr int ZS = MR * ROW + 2;    // double2 per z-slice: 2 ZS == 4 (mod 8) ke
                                     // 16-byte row loads of a warp bank-conflict free
 constexpr int REGION = MR * ZS;     // double2 in the region
 constexpr int CELLS = MR * MR * MR;  // region cells (node index table)
-constexpr int SMEM_BYTES = (REGION + kSlots * 2) * 16 + CELLS * 4;
+// Staged taps: per sample (ax + 3) TSX + (ay + 3) 7 + (az + 3); TSX == 2 (mod 8) keeps the
+// 16-byte tap gathers of a warp (lane parts (ox - cx) TSX + (oy - cy) 7 + oz) conflict free.
+constexpr int TSX = 50;
+constexpr int TAPS = 7 * TSX;       // double2 per sample
+constexpr int SMEM_BYTES = (REGION + TAPS * 2) * 16 + CELLS * 4;
 
 __host__ __device__ constexpr int fdiv2(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }
 __host__ __device__ constexpr int iabs(int v) { return v < 0 ? -v : v; }

@@ -111,7 +111,9 @@ def test_zero_and_linearity(hb):
     assert np.all(z == 0)
     a = eng.evaluate(q).potentials
     b = eng.evaluate(1j * q).potentials
-    assert rel_l2(b, 1j * a) < 1e-14
+    # the M2L's 3-multiplication complex product does not commute bit for bit with a
+    # multiplication by i (the 4-multiplication form did); rounding-level agreement
+    assert rel_l2(b, 1j * a) < 1e-13
     rng = np.random.default_rng(1)
     q2 = rng.standard_normal(q.size) + 1j * rng.standard_normal(q.size)
     c = eng.evaluate(q2).potentials
