@@ -168,7 +168,7 @@ void Engine::setup_interp(DevLevel& P, const DevLevel& C, const LevelData& tp, c
   P.dn_phi_v = upload_vec(dphi.v);
   // Even / odd form of the theta passes, with the fold / unfold baked into the
   // phi matrices (interp.hpp): what the fused and compile-time-shaped kernels take.
-  if (nc % 2 == 0 && np % 2 == 0 && (fz_pair(nc, np) || rb_pair(nc, np))) {
+  if (nc % 2 == 0 && np % 2 == 0) {
     const EvenOdd ue = even_odd(uth, 2 * nc, 2 * np), de = even_odd(dth, 2 * np, 2 * nc);
     const RealRank1 uf = fold_columns(uphi, nc, np), du = unfold_rows(dphi, np, nc);
     P.up_phi_Bf = upload_vec(uf.B);
@@ -596,11 +596,21 @@ void Engine::phase_c2m() {
 namespace {
 // Runtime-shaped streaming kernels: any even grid pair (the host B layouts
 // K = round4(n_in + 1), N = round8(n_out) are what they expect).
+constexpr int kRblSmemLim = 200 * 1024;
+// n8 tiles per CTA column block of the L2L theta pass: the most that fit shared memory
+int l2l_rbl_chb(int nc, int np) {
+  const int rows = 2 * rb::r4(np + 1), nt = rb::r8(nc) / 8;
+  int chb = nt;
+  while (chb > 1 && rows * rb::blk_ldb(8 * chb) * 8 > kRblSmemLim) --chb;
+  const int nblk = (nt + chb - 1) / chb;
+  return (nt + nblk - 1) / nblk;  // even blocks
+}
 bool rbl_ok(int nc, int np) {
-  // shared-memory B: whole phi matrices and one theta column block must fit (227 KB)
-  const int lim = 227 * 1024;
+  // shared-memory B: whole phi matrices and one theta column block must fit
+  const int lim = kRblSmemLim;
   const bool fits = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8 <= lim && rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8 <= lim &&
-                    rb::r4(2 * np + 1) * rb::blk_ldb(8 * rb::kChunk) * 8 <= lim;
+                    2 * rb::r4(nc + 1) * rb::blk_ldb(8 * rb::kChunkEO) * 8 <= lim &&
+                    2 * rb::r4(np + 1) * rb::blk_ldb(8 * l2l_rbl_chb(nc, np)) * 8 <= lim;
   return nc % 2 == 0 && np % 2 == 0 && fits;
 }
 }  // namespace
@@ -618,7 +628,11 @@ void Engine::phase_m2m() {
     // 0. fused single-kernel pair (folded circles stay in shared memory)
 #ifndef HFMM_NO_FZ
     if (!hook_no_rb_ && fz_pair(nc, np)) {
+#ifdef HFMM_FZ1
       launch_m2m_fz(rl, sms_, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up);
+#else
+      launch_m2m_fz2(rl, sms_, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up);
+#endif
       ++launches_;
       ck(cudaGetLastError(), "k_m2m_fz");
       continue;
@@ -634,16 +648,16 @@ void Engine::phase_m2m() {
     // 2. runtime-shaped streaming kernels (B matrices fit shared memory)
     if (!hook_no_rbl_ && rbl_ok(nc, np)) {
       const int s_phi = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8;
-      const int nchunk = (rb::r8(2 * np) / 8 + rb::kChunkM2M - 1) / rb::kChunkM2M;
-      const int s_th = rb::r4(2 * nc + 1) * rb::blk_ldb(8 * rb::kChunkM2M) * 8;
+      const int nchunk = (rb::r8(np) / 8 + rb::kChunkEO - 1) / rb::kChunkEO;
+      const int s_th = 2 * rb::r4(nc + 1) * rb::blk_ldb(8 * rb::kChunkEO) * 8;
       ck(cudaFuncSetAttribute(k_m2m_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
       ck(cudaFuncSetAttribute(k_m2m_theta_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_th), "attr");
       if (rl.nch > 0)
-        k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, C.mp, P.up_phi_B, P.up_phi_v,
+        k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, C.mp, P.up_phi_Bf, P.up_phi_v,
                                                               d_tmp);
       const dim3 gth(unsigned(std::max(1, 2 * sms_ / nchunk)), unsigned(nchunk));
       k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, rl.n_par, rl.plist, rl.child_off, rl.children,
-                                                        rl.oct_c, d_tmp, P.up_th_B, P.up_th_v, P.shift_up, P.mp);
+                                                        rl.oct_c, d_tmp, P.up_th_Be, P.up_th_ve, P.shift_up, P.mp);
       launches_ += 2;
       ck(cudaGetLastError(), "k_m2m_rbl");
       continue;
@@ -707,6 +721,15 @@ void Engine::phase_l2l(int lo, int hi) {
                       R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
                       oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
     if (rl.n_par == 0) continue;
+    // 0. fused single-kernel pair (narrow rows stay in shared memory)
+#ifdef HFMM_FZL
+    if (!hook_no_rb_ && fz_pair(nc, np)) {
+      launch_l2l_fz2(rl, sms_, P.loc, C.loc, P.dn_th_Be, P.dn_th_ve, P.dn_phi_Bu, P.dn_phi_vu, P.shift_dn);
+      ++launches_;
+      ck(cudaGetLastError(), "k_l2l_fz2");
+      continue;
+    }
+#endif
     // 1. compile-time-shaped streaming pairs
     if (!hook_no_rb_ && rb_pair(nc, np) &&
         launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_Be, P.dn_th_ve, P.dn_phi_Bu, P.dn_phi_vu, P.shift_dn, d_tmp)) {
@@ -718,10 +741,15 @@ void Engine::phase_l2l(int lo, int hi) {
     if (!hook_no_rbl_ && rbl_ok(nc, np)) {
       const int s_phi = rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8;
       ck(cudaFuncSetAttribute(k_l2l_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
-      k_l2l_theta_rbl<<<2 * sms_, rb::kThreads, 0, st_>>>(nc, np, rl.n_par, rl.plist, rl.child_off, rl.children,
-                                                          rl.oct_c, P.loc, P.dn_th_B, P.dn_th_v, P.shift_dn, d_tmp);
+      const int chb = l2l_rbl_chb(nc, np), nblk = (rb::r8(nc) / 8 + chb - 1) / chb;
+      const int s_th = 2 * rb::r4(np + 1) * rb::blk_ldb(8 * chb) * 8;
+      ck(cudaFuncSetAttribute(k_l2l_theta_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_th), "attr");
+      const int per_sm = std::max(1, std::min(2, (220 * 1024) / (s_th + 1024)));
+      const dim3 gth(unsigned(std::max(1, per_sm * sms_ / nblk)), unsigned(nblk));
+      k_l2l_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, chb, rl.n_par, rl.plist, rl.child_off, rl.children,
+                                                        rl.oct_c, P.loc, P.dn_th_Be, P.dn_th_ve, P.shift_dn, d_tmp);
       if (rl.nch > 0)
-        k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, d_tmp, P.dn_phi_B, P.dn_phi_v,
+        k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, d_tmp, P.dn_phi_Bu, P.dn_phi_vu,
                                                               C.loc);
       launches_ += 2;
       ck(cudaGetLastError(), "k_l2l_rbl");

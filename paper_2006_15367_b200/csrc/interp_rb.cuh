@@ -33,7 +33,12 @@ namespace rb {
 
 __host__ __device__ constexpr int r4(int v) { return (v + 3) / 4 * 4; }
 __host__ __device__ constexpr int r8(int v) { return (v + 7) / 8 * 8; }
-__host__ __device__ constexpr int ldb(int n) { return n % 16 == 0 ? n + 8 : n; }  // bank-conflict-free B fragments
+// B fragment of m8n8k4: lane (g, tq) reads B[4 kk + tq][8 j + g], an 8-byte load
+// served per half-warp (g in a group of 4, tq = 0..3): conflict free when the
+// four tq rows land 4 doubles apart (mod 16), i.e. row stride == 4 (mod 8).
+// (ncu showed the earlier stride == 8 (mod 16) at 4 wavefronts per load, 2 of
+// them bank conflicts.)
+__host__ __device__ constexpr int ldb(int n) { return n % 8 == 4 ? n : n + 4 + (8 - n % 8) % 8; }
 constexpr int kThreads = 256;
 
 // K x N row-major B (global) -> shared rows of stride LDB (persistent CTA, once).
@@ -50,15 +55,15 @@ __device__ __forceinline__ void stage_b(double* dst, const double* __restrict__ 
 
 // Rank-1 column: lane (g, tq) holds x_re / x_im of row g at columns 4 kk + tq
 // (zeros past KIN); inject i (v . x) at column KIN.
-template <int KS, int KIN>
-__device__ __forceinline__ void rank1_inject(double (&are)[KS], double (&aim)[KS], const double* __restrict__ v) {
+template <int KS, int KIN, class V>
+__device__ __forceinline__ void rank1_inject_f(double (&are)[KS], double (&aim)[KS], V vf) {
   const int tq = threadIdx.x & 3;
   double sr = 0.0, si = 0.0;
 #pragma unroll
   for (int kk = 0; kk < KS; ++kk) {
     const int k = 4 * kk + tq;
     if (k < KIN) {
-      const double vk = __ldg(v + k);
+      const double vk = vf(k);
       sr = fma(vk, are[kk], sr);
       si = fma(vk, aim[kk], si);
     }
@@ -72,6 +77,10 @@ __device__ __forceinline__ void rank1_inject(double (&are)[KS], double (&aim)[KS
     are[KR] = -si;  // Re(i alpha)
     aim[KR] = sr;   // Im(i alpha)
   }
+}
+template <int KS, int KIN>
+__device__ __forceinline__ void rank1_inject(double (&are)[KS], double (&aim)[KS], const double* __restrict__ v) {
+  rank1_inject_f<KS, KIN>(are, aim, [&](int k) { return __ldg(v + k); });
 }
 
 // Sum over the 8 child rows of a warp tile (lane bits 2..4 = g) of a chunk of
@@ -112,16 +121,16 @@ __device__ __forceinline__ void tile_mma(const double (&are)[KS], const double (
 // Rank-1 column of the even / odd theta passes: alpha = v_e . x_e + v_o . x_o
 // (v laid out like the B rows: v_o at 4 KH), injected as i alpha at column KIN
 // of both halves (the B rows there hold the symmetric / antisymmetric part of u).
-template <int KH, int KIN>
-__device__ __forceinline__ void rank1_inject_eo(double (&er)[KH], double (&ei)[KH], double (&qr)[KH], double (&qi)[KH],
-                                                const double* __restrict__ v) {
+template <int KH, int KIN, class V>
+__device__ __forceinline__ void rank1_inject_eo_f(double (&er)[KH], double (&ei)[KH], double (&qr)[KH], double (&qi)[KH],
+                                                  V vf) {
   const int tq = threadIdx.x & 3;
   double sr = 0.0, si = 0.0;
 #pragma unroll
   for (int kk = 0; kk < KH; ++kk) {
     const int k = 4 * kk + tq;
     if (k < KIN) {
-      const double ve = __ldg(v + k), vo = __ldg(v + 4 * KH + k);
+      const double ve = vf(k), vo = vf(4 * KH + k);
       sr = fma(ve, er[kk], sr);
       si = fma(ve, ei[kk], si);
       sr = fma(vo, qr[kk], sr);
@@ -138,6 +147,11 @@ __device__ __forceinline__ void rank1_inject_eo(double (&er)[KH], double (&ei)[K
     er[KR] = qr[KR] = -si;  // Re(i alpha)
     ei[KR] = qi[KR] = sr;   // Im(i alpha)
   }
+}
+template <int KH, int KIN>
+__device__ __forceinline__ void rank1_inject_eo(double (&er)[KH], double (&ei)[KH], double (&qr)[KH], double (&qi)[KH],
+                                                const double* __restrict__ v) {
+  rank1_inject_eo_f<KH, KIN>(er, ei, qr, qi, [&](int k) { return __ldg(v + k); });
 }
 
 template <int NC, int NP>
@@ -161,9 +175,11 @@ struct Dims {
 // (x_e at [0, NC), x_o at [4 KH, 4 KH + NC)).  Ye +- Yo are the circle's front
 // (theta row n, column p) and back (column p + HALF) samples; both get their
 // shift factor and go through one child-sum reduce-scatter per 2 n8 tiles.
-template <int NC, int NP, class Ld>
-__device__ __forceinline__ void m2m_theta_item(Ld ld, bool ok, const double2* __restrict__ sh, double2* __restrict__ out,
-                                               int p, const double* __restrict__ Bt, const double* __restrict__ vth) {
+// shf(n, back) -> the shift factor of the lane's child at (theta row n, column
+// p + back HALF); vf(k) -> entry k of the [v_e ; v_o] vector.
+template <int NC, int NP, class Ld, class Sh, class V>
+__device__ __forceinline__ void m2m_theta_item_f(Ld ld, bool ok, Sh shf_, double2* __restrict__ out, int p,
+                                                 const double* __restrict__ Bt, V vf) {
   using D = Dims<NC, NP>;
   constexpr int KH = D::UTH_KH, NT = D::UTH_N / 8, HALF = D::HALF, LDB = D::UTH_LDB;
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
@@ -179,7 +195,7 @@ __device__ __forceinline__ void m2m_theta_item(Ld ld, bool ok, const double2* __
     qr[kk] = o.x;
     qi[kk] = o.y;
   }
-  rank1_inject_eo<KH, NC>(er, ei, qr, qi, vth);
+  rank1_inject_eo_f<KH, NC>(er, ei, qr, qi, vf);
   constexpr int NTC = 2;
 #pragma unroll
   for (int j0 = 0; j0 < NT; j0 += NTC) {
@@ -190,8 +206,8 @@ __device__ __forceinline__ void m2m_theta_item(Ld ld, bool ok, const double2* __
       for (int q = 0; q < 2; ++q) {
         const int n = 8 * (j0 + jc) + 2 * tq + q;
         const bool live = ok && j0 + jc < NT && n < NP;
-        shf[jc][q] = live ? __ldg(sh + n * NP + p) : make_double2(0.0, 0.0);
-        shb[jc][q] = live ? __ldg(sh + n * NP + p + HALF) : make_double2(0.0, 0.0);
+        shf[jc][q] = live ? shf_(n, 0) : make_double2(0.0, 0.0);
+        shb[jc][q] = live ? shf_(n, 1) : make_double2(0.0, 0.0);
       }
     double cer[NTC][2] = {}, cei[NTC][2] = {}, cqr[NTC][2] = {}, cqi[NTC][2] = {};
     const double* bp = Bt + tq * LDB + g + 8 * j0;
@@ -224,6 +240,13 @@ __device__ __forceinline__ void m2m_theta_item(Ld ld, bool ok, const double2* __
     const int slot = g >> 1, back = slot >= NTC, jt = j0 + slot - back * NTC, n = 8 * jt + 2 * tq + (g & 1);
     if (jt < NT && n < NP) out[n * NP + p + back * HALF] = val;
   }
+}
+template <int NC, int NP, class Ld>
+__device__ __forceinline__ void m2m_theta_item(Ld ld, bool ok, const double2* __restrict__ sh, double2* __restrict__ out,
+                                               int p, const double* __restrict__ Bt, const double* __restrict__ vth) {
+  constexpr int HALF = NP / 2;
+  m2m_theta_item_f<NC, NP>(ld, ok, [&](int n, int back) { return __ldg(sh + n * NP + p + back * HALF); }, out, p, Bt,
+                           [&](int k) { return __ldg(vth + k); });
 }
 
 }  // namespace rb
@@ -453,18 +476,10 @@ namespace rb {
 #define HFMM_RBL_CHUNK 4
 #endif
 constexpr int kChunk = HFMM_RBL_CHUNK;
-#ifndef HFMM_M2M_RBL_CHUNK
-#define HFMM_M2M_RBL_CHUNK 4
-#endif
-constexpr int kChunkM2M = HFMM_M2M_RBL_CHUNK;
-#ifndef HFMM_RBL_UNROLL_G
-#define HFMM_RBL_UNROLL_G 8
-#endif
-constexpr int kRblUnrollG = HFMM_RBL_UNROLL_G;  // k-step unroll of the global-B chunk GEMM (L2L theta)
 #ifndef HFMM_RBL_UNROLL_S
 #define HFMM_RBL_UNROLL_S 8
 #endif
-constexpr int kRblUnrollS = HFMM_RBL_UNROLL_S;  // same, shared-memory B (M2M theta)  // M2M theta: B column block per CTA (n8 tiles)
+constexpr int kRblUnrollS = HFMM_RBL_UNROLL_S;  // k-step unroll of the chunk GEMM of the phi passes
 
 // Rows [0, K) x columns [c0, c0 + nc) of a row-major K x N matrix -> shared
 // rows of stride ldb (cp.async 16 B; nc and c0 even).
@@ -480,7 +495,7 @@ __device__ __forceinline__ void stage_block(double* dst, const double* __restric
   cp_async_wait_all();
   __syncthreads();
 }
-__host__ __device__ constexpr int blk_ldb(int cols) { return cols % 16 == 0 ? cols + 8 : cols; }
+__host__ __device__ constexpr int blk_ldb(int cols) { return ldb(cols); }
 
 // alpha = v . x over the K_in data columns of a complex row; fetch(k) -> double2.
 template <class Fetch>
@@ -502,20 +517,19 @@ __device__ __forceinline__ double2 row_alpha(int kin, const double* __restrict__
 
 // C chunk (8 complex rows x kChunk n8 tiles from n8 tile j0) over K = 4 ks:
 // column kin holds ia (rank-1), columns > kin are zero.
-template <bool GLOBAL_B = false, int CH = kChunk, class Fetch>
+template <int CH = kChunk, class Fetch>
 __device__ __forceinline__ void chunk_mma(int ks, int kin, double2 ia, Fetch fetch, const double* __restrict__ B, int N,
                                           int j0, int nt, double (&cre)[CH][2], double (&cim)[CH][2]) {
   const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const double* bp = B + tq * N + 8 * j0 + g;
-  // deeper unroll with B from global (L2): more loads in flight per warp
-#pragma unroll(GLOBAL_B ? kRblUnrollG : kRblUnrollS)
+#pragma unroll(kRblUnrollS)
   for (int kk = 0; kk < ks; ++kk) {
     const int k = 4 * kk + tq;
     const double2 x = k < kin ? fetch(k) : (k == kin ? ia : make_double2(0.0, 0.0));
 #pragma unroll
     for (int jc = 0; jc < CH; ++jc)
       if (j0 + jc < nt) {
-        const double b = GLOBAL_B ? __ldg(bp + 4 * kk * N + 8 * jc) : bp[4 * kk * N + 8 * jc];
+        const double b = bp[4 * kk * N + 8 * jc];
         dmma884(cre[jc][0], cre[jc][1], x.x, b);
         dmma884(cim[jc][0], cim[jc][1], x.y, b);
       }
@@ -527,7 +541,9 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_phi_rbl(int nc, int np, in
                                                               const double2* __restrict__ mp_c,
                                                               const double* __restrict__ B, const double* __restrict__ v,
                                                               double2* __restrict__ F) {
-  const int K = rb::r4(nc + 1), N = rb::r8(np), ks = K / 4, nt = N / 8, half = np / 2, ldf = rb::r4(2 * nc + 1);
+  // (B = the phi matrix with the (e, o) fold in its columns: output column
+  // 2 p + h is part h of circle p; F row (child, p): x_e at [0, nc), x_o at [K, K + nc))
+  const int K = rb::r4(nc + 1), N = rb::r8(np), ks = K / 4, nt = N / 8, half = np / 2, ldf = 2 * K;
   const int ldb = rb::blk_ldb(N);
   extern __shared__ __align__(16) double Bsh[];
   rb::stage_block(Bsh, B, K, N, 0, N, ldb);
@@ -552,17 +568,66 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_phi_rbl(int nc, int np, in
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int n = 8 * (j0 + jc) + 2 * tq + q;
-            if (j0 + jc < nt && n < np) {
-              const int p = n < half ? n : n - half;
-              const int ii = n < half ? i : 2 * nc - 1 - i;
-              Fj[int64_t(p) * ldf + ii] = make_double2(cre[jc][q], cim[jc][q]);
-            }
+            if (j0 + jc < nt && n < np) Fj[int64_t(n >> 1) * ldf + (n & 1) * K + i] = make_double2(cre[jc][q], cim[jc][q]);
           }
       }
     }
   }
 }
 
+// Even / odd chunk GEMM over a runtime K (interp.hpp:even_odd): rows [0, KH4) of
+// the staged B block hold Be, rows [KH4, 2 KH4) hold Bo; fetch(k, e, o) delivers
+// x_e[k], x_o[k] of the lane's row; column kin of both halves carries i alpha.
+namespace rb {
+template <int CH, class Fetch>
+__device__ __forceinline__ void chunk_mma_eo(int kh, int kin, double2 ia, Fetch fetch, const double* __restrict__ Bs,
+                                             int ldb, int KH4, int nt_left, double (&cer)[CH][2], double (&cei)[CH][2],
+                                             double (&cqr)[CH][2], double (&cqi)[CH][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const double* bpe = Bs + tq * ldb + g;
+  const double* bpo = bpe + KH4 * ldb;
+#pragma unroll 4
+  for (int kk = 0; kk < kh; ++kk) {
+    const int k = 4 * kk + tq;
+    double2 e = make_double2(0.0, 0.0), o = e;
+    if (k < kin) fetch(k, e, o);
+    else if (k == kin) e = o = ia;
+#pragma unroll
+    for (int jc = 0; jc < CH; ++jc)
+      if (jc < nt_left) {
+        const double be = bpe[4 * kk * ldb + 8 * jc];
+        dmma884(cer[jc][0], cer[jc][1], e.x, be);
+        dmma884(cei[jc][0], cei[jc][1], e.y, be);
+        const double bo = bpo[4 * kk * ldb + 8 * jc];
+        dmma884(cqr[jc][0], cqr[jc][1], o.x, bo);
+        dmma884(cqi[jc][0], cqi[jc][1], o.y, bo);
+      }
+  }
+}
+
+// i alpha of the even / odd form: alpha = v_e . x_e + v_o . x_o (v_o at v + KH4).
+template <class Fetch>
+__device__ __forceinline__ double2 row_alpha_eo(int kin, int KH4, const double* __restrict__ v, Fetch fetch) {
+  const int tq = threadIdx.x & 3;
+  double sr = 0.0, si = 0.0;
+  for (int k = tq; k < kin; k += 4) {
+    const double ve = __ldg(v + k), vo = __ldg(v + KH4 + k);
+    double2 e, o;
+    fetch(k, e, o);
+    sr = fma(ve, e.x, fma(vo, o.x, sr));
+    si = fma(ve, e.y, fma(vo, o.y, si));
+  }
+  sr += __shfl_xor_sync(0xffffffffu, sr, 1);
+  si += __shfl_xor_sync(0xffffffffu, si, 1);
+  sr += __shfl_xor_sync(0xffffffffu, sr, 2);
+  si += __shfl_xor_sync(0xffffffffu, si, 2);
+  return make_double2(-si, sr);
+}
+constexpr int kChunkEO = 2;  // M2M theta: n8 tiles of the half-size output per CTA column block
+}  // namespace rb
+
+// M2M theta pass, even / odd form (the runtime-shaped twin of rb::m2m_theta_item_f):
+// B = [Be ; Bo] (2 KH4 x NH), this CTA's block of kChunkEO n8 tiles in shared memory.
 __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, int n_par, const int* __restrict__ plist,
                                                                 const int* __restrict__ child_off,
                                                                 const int* __restrict__ children,
@@ -572,13 +637,12 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
                                                                 const double* __restrict__ v,
                                                                 const double2* __restrict__ shift_up,
                                                                 double2* __restrict__ mp_p) {
-  const int K = rb::r4(2 * nc + 1), N = rb::r8(2 * np), ks = K / 4, nt = N / 8, half = np / 2, ldf = K;
+  const int KH4 = rb::r4(nc + 1), kh = KH4 / 4, NH = rb::r8(np), nt = NH / 8, half = np / 2, ldf = 2 * KH4;
   const int64_t SP = int64_t(np) * np;
-  // this CTA's column block of B (CH n8 tiles) lives in shared memory
-  constexpr int CH = rb::kChunkM2M;
+  constexpr int CH = rb::kChunkEO;
   const int j0 = blockIdx.y * CH, ldb = rb::blk_ldb(8 * CH);
   extern __shared__ __align__(16) double Bsh[];
-  rb::stage_block(Bsh, B, K, N, 8 * j0, 8 * CH, ldb);
+  rb::stage_block(Bsh, B, 2 * KH4, NH, 8 * j0, 8 * CH, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t items = int64_t(n_par) * half;
   for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
@@ -588,45 +652,54 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
     const bool ok = g < nchp;
     const double2* frow = F + (int64_t(cb + (ok ? g : 0)) * half + p) * ldf;
     const double2* sh = shift_up + int64_t(ok ? oct_c[children[cb + g]] : 0) * SP;
-    auto fetch = [&](int k) { return ok ? __ldg(frow + k) : make_double2(0.0, 0.0); };
-    const double2 ia = rb::row_alpha(2 * nc, v, fetch);
+    auto fetch = [&](int k, double2& e, double2& o) {
+      e = ok ? __ldg(frow + k) : make_double2(0.0, 0.0);
+      o = ok ? __ldg(frow + KH4 + k) : make_double2(0.0, 0.0);
+    };
+    const double2 ia = rb::row_alpha_eo(nc, KH4, v, fetch);
     double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
-    {
-      double2 shv[CH][2];
+    double2 shf[CH][2], shb[CH][2];
 #pragma unroll
-      for (int jc = 0; jc < CH; ++jc)
+    for (int jc = 0; jc < CH; ++jc)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int n = 8 * (j0 + jc) + 2 * tq + q;
-          const int64_t s = n < np ? int64_t(n) * np + p : int64_t(2 * np - 1 - n) * np + p + half;
-          shv[jc][q] = (ok && n < 2 * np) ? __ldg(sh + s) : make_double2(0.0, 0.0);
-        }
-      double cre[CH][2] = {}, cim[CH][2] = {};
-      rb::chunk_mma<false, CH>(ks, 2 * nc, ia, fetch, Bsh, ldb, 0, nt - j0, cre, cim);
-      static_assert(CH == 4, "child_sum_scatter takes 4 n8 tiles");
-      double v[16];
-#pragma unroll
-      for (int jc = 0; jc < CH; ++jc)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const double2 f = shv[jc][q];
-          v[(2 * jc + q) * 2] = cre[jc][q] * f.x - cim[jc][q] * f.y;
-          v[(2 * jc + q) * 2 + 1] = cre[jc][q] * f.y + cim[jc][q] * f.x;
-        }
-      const double2 val = rb::child_sum_scatter(v);
-      const int jt = j0 + (g >> 1), n = 8 * jt + 2 * tq + (g & 1);
-      if (jt < nt && n < 2 * np) {
-        const int64_t s = n < np ? int64_t(n) * np + p : int64_t(2 * np - 1 - n) * np + p + half;
-        out[s] = val;
+      for (int q = 0; q < 2; ++q) {
+        const int n = 8 * (j0 + jc) + 2 * tq + q;
+        const bool live = ok && n < np;
+        shf[jc][q] = live ? __ldg(sh + int64_t(n) * np + p) : make_double2(0.0, 0.0);
+        shb[jc][q] = live ? __ldg(sh + int64_t(n) * np + p + half) : make_double2(0.0, 0.0);
       }
-    }
+    double cer[CH][2] = {}, cei[CH][2] = {}, cqr[CH][2] = {}, cqi[CH][2] = {};
+    rb::chunk_mma_eo<CH>(kh, nc, ia, fetch, Bsh, ldb, KH4, nt - j0, cer, cei, cqr, cqi);
+    static_assert(CH == 2, "child_sum_scatter takes the front and back halves of 2 n8 tiles");
+    double vv[16];  // front tiles 0, 1, then back tiles 0, 1
+#pragma unroll
+    for (int jc = 0; jc < CH; ++jc)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double fr = cer[jc][q] + cqr[jc][q], fi = cei[jc][q] + cqi[jc][q];
+        const double br = cer[jc][q] - cqr[jc][q], bi = cei[jc][q] - cqi[jc][q];
+        const double2 f = shf[jc][q], b = shb[jc][q];
+        vv[(2 * jc + q) * 2] = fr * f.x - fi * f.y;
+        vv[(2 * jc + q) * 2 + 1] = fr * f.y + fi * f.x;
+        vv[(2 * (CH + jc) + q) * 2] = br * b.x - bi * b.y;
+        vv[(2 * (CH + jc) + q) * 2 + 1] = br * b.y + bi * b.x;
+      }
+    const double2 val = rb::child_sum_scatter(vv);
+    const int slot = g >> 1, back = slot >= CH, jt = j0 + slot - back * CH, n = 8 * jt + 2 * tq + (g & 1);
+    if (jt < nt && n < np) out[int64_t(n) * np + p + back * half] = val;
   }
 }
 
 #ifndef HFMM_L2L_RBL_CHUNK
-#define HFMM_L2L_RBL_CHUNK 7
+#define HFMM_L2L_RBL_CHUNK 3
 #endif
-__global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, int n_par, const int* __restrict__ plist,
+// L2L theta pass, even / odd form: the lane's row (child c, circle p) is
+// x_e / x_o[k] = L_p[k][p] shift_c[k][p] +- L_p[k][p + half] shift_c[k][p + half],
+// built on the fly; B = [Be ; Bo] (2 KH4 x NH), this CTA's block of `chb` n8 tiles
+// in shared memory (blockIdx.y), walked in sub-chunks of CH tiles; output row n
+// of the child: (Ye, Yo) of circle p at columns 2 p, 2 p + 1 of the narrow rows.
+__global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, int chb, int n_par,
+                                                                const int* __restrict__ plist,
                                                                 const int* __restrict__ child_off,
                                                                 const int* __restrict__ children,
                                                                 const uint8_t* __restrict__ oct_c,
@@ -635,10 +708,12 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, 
                                                                 const double* __restrict__ v,
                                                                 const double2* __restrict__ shift_dn,
                                                                 double2* __restrict__ Nb) {
-  const int K = rb::r4(2 * np + 1), N = rb::r8(2 * nc), ks = K / 4, nt = N / 8, half = np / 2, ldn = rb::r4(np + 1);
+  const int KH4 = rb::r4(np + 1), kh = KH4 / 4, NH = rb::r8(nc), nt = NH / 8, half = np / 2, ldn = rb::r4(np + 1);
   const int64_t SP = int64_t(np) * np;
-  // (B through L1/L2, all column chunks per warp: this pass's A values are
-  // built on the fly from L_p x shift, so they are not re-built per chunk CTA.)
+  const int jb = blockIdx.y * chb, ldb = rb::blk_ldb(8 * chb);
+  const int jend = jb + chb < nt ? jb + chb : nt;
+  extern __shared__ __align__(16) double Bsh[];
+  rb::stage_block(Bsh, B, 2 * KH4, NH, 8 * jb, 8 * chb, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t items = int64_t(n_par) * half;
   for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
@@ -649,29 +724,32 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, 
     const bool ok = c < nchp;
     const double2* L = loc_p + int64_t(plist ? plist[par] : par) * SP;
     const double2* sh = shift_dn + int64_t(ok ? oct_c[children[cb + c]] : 0) * SP;
-    auto fetch = [&](int k) {
-      if (!ok) return make_double2(0.0, 0.0);
-      const int64_t s = k < np ? int64_t(k) * np + p : int64_t(2 * np - 1 - k) * np + p + half;
-      return cmul(__ldg(L + s), __ldg(sh + s));
+    auto fetch = [&](int k, double2& e, double2& o) {
+      if (!ok) {
+        e = o = make_double2(0.0, 0.0);
+        return;
+      }
+      const int64_t s = int64_t(k) * np + p;
+      const double2 f = cmul(__ldg(L + s), __ldg(sh + s)), b = cmul(__ldg(L + s + half), __ldg(sh + s + half));
+      e = make_double2(f.x + b.x, f.y + b.y);
+      o = make_double2(f.x - b.x, f.y - b.y);
     };
-    const double2 ia = rb::row_alpha(2 * np, v, fetch);
+    const double2 ia = rb::row_alpha_eo(np, KH4, v, fetch);
     double2* Nc = Nb + int64_t(cb + (ok ? c : 0)) * nc * ldn;
-    // wide column chunks: the A values (L_p x shift, two loads and a complex
-    // product each) are rebuilt once per chunk
     constexpr int CH = HFMM_L2L_RBL_CHUNK;
-    for (int j0 = 0; j0 < nt; j0 += CH) {
-      double cre[CH][2] = {}, cim[CH][2] = {};
-      rb::chunk_mma<true, CH>(ks, 2 * np, ia, fetch, B, N, j0, nt, cre, cim);
+    for (int j0 = jb; j0 < jend; j0 += CH) {
+      double cer[CH][2] = {}, cei[CH][2] = {}, cqr[CH][2] = {}, cqi[CH][2] = {};
+      rb::chunk_mma_eo<CH>(kh, np, ia, fetch, Bsh + 8 * (j0 - jb), ldb, KH4, jend - j0, cer, cei, cqr, cqi);
       if (ok) {
 #pragma unroll
         for (int jc = 0; jc < CH; ++jc)
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const int n = 8 * (j0 + jc) + 2 * tq + q;
-            if (j0 + jc < nt && n < 2 * nc) {
-              const int row = n < nc ? n : 2 * nc - 1 - n;
-              const int col = n < nc ? p : p + half;
-              Nc[int64_t(row) * ldn + col] = make_double2(cre[jc][q], cim[jc][q]);
+            if (j0 + jc < jend && n < nc) {
+              double2* d = Nc + int64_t(n) * ldn + 2 * p;
+              d[0] = make_double2(cer[jc][q], cei[jc][q]);
+              d[1] = make_double2(cqr[jc][q], cqi[jc][q]);
             }
           }
       }
