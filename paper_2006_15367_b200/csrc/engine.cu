@@ -596,20 +596,26 @@ void Engine::phase_c2m() {
 namespace {
 // Runtime-shaped streaming kernels: any even grid pair (the host B layouts
 // K = round4(n_in + 1), N = round8(n_out) are what they expect).
-constexpr int kRblSmemLim = 200 * 1024;
-// n8 tiles per CTA column block of the L2L theta pass: the most that fit shared memory
-int l2l_rbl_chb(int nc, int np) {
-  const int rows = 2 * rb::r4(np + 1), nt = rb::r8(nc) / 8;
-  int chb = nt;
-  while (chb > 1 && rows * rb::blk_ldb(8 * chb) * 8 > kRblSmemLim) --chb;
+#ifndef HFMM_RBL_SMEM_KB
+#define HFMM_RBL_SMEM_KB 100
+#endif
+constexpr int kRblSmemLim = HFMM_RBL_SMEM_KB * 1024;  // two CTAs per SM at the default
+// n8 tiles per CTA column block of a theta pass with n_in inputs and n_out outputs per
+// half circle: the most that fit shared memory, in even blocks of a multiple of `mult` tiles
+int rbl_chb(int n_in, int n_out, int mult) {
+  const int rows = 2 * rb::r4(n_in + 1), nt = rb::r8(n_out) / 8;
+  int chb = (nt + mult - 1) / mult * mult;
+  while (chb > mult && rows * rb::blk_ldb(8 * chb) * 8 > kRblSmemLim) chb -= mult;
   const int nblk = (nt + chb - 1) / chb;
-  return (nt + nblk - 1) / nblk;  // even blocks
+  return ((nt + nblk - 1) / nblk + mult - 1) / mult * mult;
 }
+int l2l_rbl_chb(int nc, int np) { return rbl_chb(np, nc, 1); }
+int m2m_rbl_chb(int nc, int np) { return rbl_chb(nc, np, rb::kChunkEO); }
 bool rbl_ok(int nc, int np) {
   // shared-memory B: whole phi matrices and one theta column block must fit
-  const int lim = kRblSmemLim;
-  const bool fits = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8 <= lim && rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8 <= lim &&
-                    2 * rb::r4(nc + 1) * rb::blk_ldb(8 * rb::kChunkEO) * 8 <= lim &&
+  const int lim = kRblSmemLim, lim_phi = 225 * 1024;
+  const bool fits = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8 <= lim_phi && rb::r4(np + 1) * rb::blk_ldb(rb::r8(nc)) * 8 <= lim_phi &&
+                    2 * rb::r4(nc + 1) * rb::blk_ldb(8 * m2m_rbl_chb(nc, np)) * 8 <= lim &&
                     2 * rb::r4(np + 1) * rb::blk_ldb(8 * l2l_rbl_chb(nc, np)) * 8 <= lim;
   return nc % 2 == 0 && np % 2 == 0 && fits;
 }
@@ -648,15 +654,16 @@ void Engine::phase_m2m() {
     // 2. runtime-shaped streaming kernels (B matrices fit shared memory)
     if (!hook_no_rbl_ && rbl_ok(nc, np)) {
       const int s_phi = rb::r4(nc + 1) * rb::blk_ldb(rb::r8(np)) * 8;
-      const int nchunk = (rb::r8(np) / 8 + rb::kChunkEO - 1) / rb::kChunkEO;
-      const int s_th = 2 * rb::r4(nc + 1) * rb::blk_ldb(8 * rb::kChunkEO) * 8;
+      const int chb = m2m_rbl_chb(nc, np), nchunk = (rb::r8(np) / 8 + chb - 1) / chb;
+      const int s_th = 2 * rb::r4(nc + 1) * rb::blk_ldb(8 * chb) * 8;
       ck(cudaFuncSetAttribute(k_m2m_phi_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_phi), "attr");
       ck(cudaFuncSetAttribute(k_m2m_theta_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_th), "attr");
       if (rl.nch > 0)
         k_m2m_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, C.mp, P.up_phi_Bf, P.up_phi_v,
                                                               d_tmp);
-      const dim3 gth(unsigned(std::max(1, 2 * sms_ / nchunk)), unsigned(nchunk));
-      k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, rl.n_par, rl.plist, rl.child_off, rl.children,
+      const int per_sm_u = std::max(1, std::min(2, (220 * 1024) / (s_th + 1024)));
+      const dim3 gth(unsigned(std::max(1, per_sm_u * sms_ / nchunk)), unsigned(nchunk));
+      k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, chb, rl.n_par, rl.plist, rl.child_off, rl.children,
                                                         rl.oct_c, d_tmp, P.up_th_Be, P.up_th_ve, P.shift_up, P.mp);
       launches_ += 2;
       ck(cudaGetLastError(), "k_m2m_rbl");

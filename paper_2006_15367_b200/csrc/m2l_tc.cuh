@@ -79,6 +79,10 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, i
   for (int64_t pr = pb; pr < pe; ++pr) {
     const int64_t s0 = pr * 2;
     __syncthreads();
+#ifdef HFMM_M2L_PROBE_NOSTAGE  // timing probe only (wrong results): stage the first pair, then recompute on it
+    if (pr == pb)
+#endif
+    {
     for (int t = threadIdx.x; t < kSlots * 2; t += blockDim.x) {
       // taps of adjacent boxes (|offset| <= 1 per axis) are never far: staged
       // as zeros, so K_D needs no per-entry mask
@@ -87,11 +91,25 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, i
       cp_async16(Ts + (t & 1) * TAPS + (ax + 3) * TSX + (ay + 3) * 7 + (az + 3),
                  T + (far_tap ? int64_t(sl) * S + s0 + (t & 1) : 0), far_tap);
     }
-    for (int t = threadIdx.x; t < CELLS * 2; t += blockDim.x) {
-      const int c = t >> 1, cz = c / (MR * MR), cy = (c / MR) % MR, cx = c % MR;
-      const int node = nodes[c];
-      cp_async16(Ms + cz * ZS + cy * ROW + 2 * cx + (t & 1), mp + (node >= 0 ? int64_t(node) * S + s0 + (t & 1) : 0),
-                 node >= 0);
+    // region: a thread keeps its (cell x, sample) entry `ent` of a 24-entry row and
+    // walks the 144 (z, y) rows five at a time -- no per-copy divisions
+    if (threadIdx.x < 5 * 2 * MR) {
+      const int rg = threadIdx.x / (2 * MR), ent = threadIdx.x - rg * (2 * MR);
+      int cy = rg, cz = 0;
+#pragma unroll 4
+      for (int k = 0; k < (MR * MR + 4) / 5; ++k) {
+        if (cz < MR) {
+          const int node = nodes[(cz * MR + cy) * MR + (ent >> 1)];
+          cp_async16(Ms + cz * ZS + cy * ROW + ent,
+                     mp + (node >= 0 ? uint64_t(uint32_t(node)) * uint32_t(S) + uint64_t(s0 + (ent & 1)) : 0), node >= 0);
+        }
+        cy += 5;
+        if (cy >= MR) {
+          cy -= MR;
+          ++cz;
+        }
+      }
+    }
     }
     cp_async_wait_all();
     __syncthreads();
