@@ -107,6 +107,19 @@ Engine::Engine(std::shared_ptr<const Setup> sp, int device, int rank)
   }
   upload();
   if (dist_) upload_rank_plan();
+  // Parent descriptors of the M2M / L2L work loops (rb::PDesc), per parent level.
+  pdesc_.assign(size_t(s.L + 1), nullptr);
+  for (int l = s.top; l < s.L; ++l) {
+    const DevLevel& P = lv_[size_t(l)];
+    const RankLevel* R = dist_ ? &rl_[size_t(l)] : nullptr;
+    const int n_par = R ? R->n_par : P.n_nodes;
+    int4* d = alloc<int4>(size_t(3) * size_t(std::max(n_par, 1)));
+    if (n_par > 0)
+      k_build_pdesc<<<(n_par + 127) / 128, 128, 0, st_>>>(n_par, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
+                                                         R ? R->children : P.children, oct_[size_t(l + 1)], d);
+    pdesc_[size_t(l)] = d;
+  }
+  ck(cudaGetLastError(), "k_build_pdesc");
   ck(cudaStreamSynchronize(st_), "upload sync");
 }
 
@@ -629,16 +642,12 @@ void Engine::phase_m2m() {
     const RankLevel* R = dist_ ? &rl_[size_t(l)] : nullptr;
     const RbLaunch rl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
                       R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
-                      oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
+                      oct_[size_t(l + 1)], pdesc_[size_t(l)], 2 * sms_, st_, kPhiCtas * sms_};
     if (rl.n_par == 0) continue;
     // 0. fused single-kernel pair (folded circles stay in shared memory)
 #ifndef HFMM_NO_FZ
     if (!hook_no_rb_ && fz_pair(nc, np)) {
-#ifdef HFMM_FZ1
-      launch_m2m_fz(rl, sms_, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up);
-#else
       launch_m2m_fz2(rl, sms_, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up);
-#endif
       ++launches_;
       ck(cudaGetLastError(), "k_m2m_fz");
       continue;
@@ -663,8 +672,7 @@ void Engine::phase_m2m() {
                                                               d_tmp);
       const int per_sm_u = std::max(1, std::min(2, (220 * 1024) / (s_th + 1024)));
       const dim3 gth(unsigned(std::max(1, per_sm_u * sms_ / nchunk)), unsigned(nchunk));
-      k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, chb, rl.n_par, rl.plist, rl.child_off, rl.children,
-                                                        rl.oct_c, d_tmp, P.up_th_Be, P.up_th_ve, P.shift_up, P.mp);
+      k_m2m_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, chb, rl.n_par, rl.pdesc, d_tmp, P.up_th_Be, P.up_th_ve, P.shift_up, P.mp);
       launches_ += 2;
       ck(cudaGetLastError(), "k_m2m_rbl");
       continue;
@@ -726,17 +734,8 @@ void Engine::phase_l2l(int lo, int hi) {
     const RankLevel* R = dist_ ? &rl_[size_t(l)] : nullptr;
     const RbLaunch rl{R ? R->n_par : P.n_nodes, R ? R->plist : nullptr, R ? R->child_off : P.child_off,
                       R ? R->children : P.children, dist_ ? R->n_children : int64_t(C.n_nodes),
-                      oct_[size_t(l + 1)], 2 * sms_, st_, kPhiCtas * sms_};
+                      oct_[size_t(l + 1)], pdesc_[size_t(l)], 2 * sms_, st_, kPhiCtas * sms_};
     if (rl.n_par == 0) continue;
-    // 0. fused single-kernel pair (narrow rows stay in shared memory)
-#ifdef HFMM_FZL
-    if (!hook_no_rb_ && fz_pair(nc, np)) {
-      launch_l2l_fz2(rl, sms_, P.loc, C.loc, P.dn_th_Be, P.dn_th_ve, P.dn_phi_Bu, P.dn_phi_vu, P.shift_dn);
-      ++launches_;
-      ck(cudaGetLastError(), "k_l2l_fz2");
-      continue;
-    }
-#endif
     // 1. compile-time-shaped streaming pairs
     if (!hook_no_rb_ && rb_pair(nc, np) &&
         launch_l2l_rb(nc, np, rl, P.loc, C.loc, P.dn_th_Be, P.dn_th_ve, P.dn_phi_Bu, P.dn_phi_vu, P.shift_dn, d_tmp)) {
@@ -753,8 +752,7 @@ void Engine::phase_l2l(int lo, int hi) {
       ck(cudaFuncSetAttribute(k_l2l_theta_rbl, cudaFuncAttributeMaxDynamicSharedMemorySize, s_th), "attr");
       const int per_sm = std::max(1, std::min(2, (220 * 1024) / (s_th + 1024)));
       const dim3 gth(unsigned(std::max(1, per_sm * sms_ / nblk)), unsigned(nblk));
-      k_l2l_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, chb, rl.n_par, rl.plist, rl.child_off, rl.children,
-                                                        rl.oct_c, P.loc, P.dn_th_Be, P.dn_th_ve, P.shift_dn, d_tmp);
+      k_l2l_theta_rbl<<<gth, rb::kThreads, s_th, st_>>>(nc, np, chb, rl.n_par, rl.pdesc, P.loc, P.dn_th_Be, P.dn_th_ve, P.shift_dn, d_tmp);
       if (rl.nch > 0)
         k_l2l_phi_rbl<<<2 * sms_, rb::kThreads, s_phi, st_>>>(nc, np, rl.nch, rl.children, d_tmp, P.dn_phi_Bu, P.dn_phi_vu,
                                                               C.loc);

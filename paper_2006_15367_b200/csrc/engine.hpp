@@ -169,6 +169,7 @@ class Engine {
   bool owns_stream_ = true;
   std::vector<DevLevel> lv_;
   std::vector<uint8_t*> oct_;  // per level: child octant (code & 7) of each node
+  std::vector<const int4*> pdesc_;  // per parent level: parent descriptors (interp_rb.cuh:PDesc)
   std::vector<void*> allocs_;
   int64_t launches_ = 0;
   // test hooks (HFMM_NO_RB, HFMM_NO_RBL, HFMM_NO_QUAD; tests/test_gpu_paths.py)

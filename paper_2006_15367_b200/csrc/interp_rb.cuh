@@ -42,6 +42,14 @@ __host__ __device__ constexpr int r8(int v) { return (v + 7) / 8 * 8; }
 __host__ __device__ constexpr int ldb(int n) { return n % 8 == 4 ? n : n + 4 + (8 - n % 8) % 8; }
 constexpr int kThreads = 256;
 
+// Parent descriptor (3 int4 per parent, built once per level by k_build_pdesc):
+// {first child position, child count, parent row, octants (4 bits per child
+// slot)} + the 8 child rows.  The work loops of the theta passes load it one
+// item ahead; before, every item began with a chain of dependent global loads
+// (child_off -> children -> octant -> shift table -> data), which ncu showed as
+// the long-scoreboard stall at the top of these kernels.
+__device__ __forceinline__ int pdesc_oct(const int4& d, int slot) { return (d.w >> (4 * slot)) & 7; }
+
 // K x N row-major B (global) -> shared rows of stride LDB (persistent CTA, once).
 template <int K, int N, int LDB>
 __device__ __forceinline__ void stage_b(double* dst, const double* __restrict__ src) {
@@ -59,24 +67,27 @@ __device__ __forceinline__ void stage_b(double* dst, const double* __restrict__ 
 template <int KS, int KIN, class V>
 __device__ __forceinline__ void rank1_inject_f(double (&are)[KS], double (&aim)[KS], V vf) {
   const int tq = threadIdx.x & 3;
-  double sr = 0.0, si = 0.0;
+  // two partial sums per part (even / odd k-steps): the dependent DFMA chain is
+  // KS / 2 deep instead of KS (FP64 latency is ~8 issue slots, tools/fp64_lat.cu)
+  double sr[2] = {0.0, 0.0}, si[2] = {0.0, 0.0};
 #pragma unroll
   for (int kk = 0; kk < KS; ++kk) {
     const int k = 4 * kk + tq;
     if (k < KIN) {
       const double vk = vf(k);
-      sr = fma(vk, are[kk], sr);
-      si = fma(vk, aim[kk], si);
+      sr[kk & 1] = fma(vk, are[kk], sr[kk & 1]);
+      si[kk & 1] = fma(vk, aim[kk], si[kk & 1]);
     }
   }
-  sr += __shfl_xor_sync(0xffffffffu, sr, 1);
-  si += __shfl_xor_sync(0xffffffffu, si, 1);
-  sr += __shfl_xor_sync(0xffffffffu, sr, 2);
-  si += __shfl_xor_sync(0xffffffffu, si, 2);
+  double tr = sr[0] + sr[1], ti = si[0] + si[1];
+  tr += __shfl_xor_sync(0xffffffffu, tr, 1);
+  ti += __shfl_xor_sync(0xffffffffu, ti, 1);
+  tr += __shfl_xor_sync(0xffffffffu, tr, 2);
+  ti += __shfl_xor_sync(0xffffffffu, ti, 2);
   constexpr int KR = KIN / 4, TR = KIN % 4;
   if (tq == TR) {
-    are[KR] = -si;  // Re(i alpha)
-    aim[KR] = sr;   // Im(i alpha)
+    are[KR] = -ti;  // Re(i alpha)
+    aim[KR] = tr;   // Im(i alpha)
   }
 }
 template <int KS, int KIN>
@@ -126,18 +137,22 @@ template <int KH, int KIN, class V>
 __device__ __forceinline__ void rank1_inject_eo_f(double (&er)[KH], double (&ei)[KH], double (&qr)[KH], double (&qi)[KH],
                                                   V vf) {
   const int tq = threadIdx.x & 3;
-  double sr = 0.0, si = 0.0;
+  // separate partial sums for the even and the odd half (and alternate k-steps):
+  // dependent chains of KH / 2 DFMA instead of 2 KH
+  double se[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, so[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int kk = 0; kk < KH; ++kk) {
     const int k = 4 * kk + tq;
     if (k < KIN) {
       const double ve = vf(k), vo = vf(4 * KH + k);
-      sr = fma(ve, er[kk], sr);
-      si = fma(ve, ei[kk], si);
-      sr = fma(vo, qr[kk], sr);
-      si = fma(vo, qi[kk], si);
+      se[kk & 1][0] = fma(ve, er[kk], se[kk & 1][0]);
+      se[kk & 1][1] = fma(ve, ei[kk], se[kk & 1][1]);
+      so[kk & 1][0] = fma(vo, qr[kk], so[kk & 1][0]);
+      so[kk & 1][1] = fma(vo, qi[kk], so[kk & 1][1]);
     }
   }
+  double sr = (se[0][0] + se[1][0]) + (so[0][0] + so[1][0]);
+  double si = (se[0][1] + se[1][1]) + (so[0][1] + so[1][1]);
   sr += __shfl_xor_sync(0xffffffffu, sr, 1);
   si += __shfl_xor_sync(0xffffffffu, si, 1);
   sr += __shfl_xor_sync(0xffffffffu, sr, 2);
@@ -253,6 +268,22 @@ __device__ __forceinline__ void m2m_theta_item(Ld ld, bool ok, const double2* __
 
 }  // namespace rb
 
+__global__ void k_build_pdesc(int n_par, const int* __restrict__ plist, const int* __restrict__ child_off,
+                              const int* __restrict__ children, const uint8_t* __restrict__ oct_c,
+                              int4* __restrict__ out) {
+  const int par = blockIdx.x * blockDim.x + threadIdx.x;
+  if (par >= n_par) return;
+  const int cb = child_off[par], n = child_off[par + 1] - cb;
+  int ch[8], octs = 0;
+  for (int c = 0; c < 8; ++c) {
+    ch[c] = c < n ? children[cb + c] : -1;
+    if (c < n) octs |= int(oct_c[ch[c]]) << (4 * c);
+  }
+  out[3 * par] = make_int4(cb, n, plist ? plist[par] : par, octs);
+  out[3 * par + 1] = make_int4(ch[0], ch[1], ch[2], ch[3]);
+  out[3 * par + 2] = make_int4(ch[4], ch[5], ch[6], ch[7]);
+}
+
 // ---------------------------------------------------------------------------
 // M2M stage 1: phi pass of every child row -> folded circles in (e, o) form,
 // F[j][p][..] (j = position in the children array): x_e[i] at i, x_o[i] at
@@ -304,10 +335,7 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_phi_rb(int64_t nch, con
 // M2M stage 2: theta pass + shift + child sum.  Work item = (parent, circle p);
 // tile rows = the parent's 8 child slots (absent children read as zero).
 template <int NC, int NP>
-__global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, const int* __restrict__ plist,
-                                                                  const int* __restrict__ child_off,
-                                                                  const int* __restrict__ children,
-                                                                  const uint8_t* __restrict__ oct_c,
+__global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, const int4* __restrict__ pdesc,
                                                                   const double2* __restrict__ F,
                                                                   const double* __restrict__ B,
                                                                   const double* __restrict__ v,
@@ -318,25 +346,18 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, con
   extern __shared__ __align__(16) double Bsm[];
   rb::stage_b<D::UTH_K, D::UTH_N, D::UTH_LDB>(Bsm, B);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2;
-  const int64_t items = int64_t(n_par) * HALF;
-  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
-       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+  const int64_t items = int64_t(n_par) * HALF, stride = int64_t(gridDim.x) * (rb::kThreads / 32);
+  int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp;
+  int4 dn = it < items ? __ldg(pdesc + 3 * (it / HALF)) : make_int4(0, 0, 0, 0);
+  for (; it < items; it += stride) {
+    const int4 dc = dn;  // parent descriptor, loaded one item ahead (rb::PDesc)
+    if (it + stride < items) dn = __ldg(pdesc + 3 * ((it + stride) / HALF));
     const int par = int(it / HALF), p = int(it - int64_t(par) * HALF);
-    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const int cb = dc.x, nchp = dc.y;
     const bool ok = g < nchp;
     const double2* frow = F + (int64_t(cb + (ok ? g : 0)) * HALF + p) * D::LDF;
-    const double2* sh = shift_up + int64_t(ok ? oct_c[children[cb + g]] : 0) * SP;
-    double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
-    {
-      // the F rows of this warp's next item -> L2, one round ahead (one row per child lane)
-      const int64_t it2 = it + int64_t(gridDim.x) * (rb::kThreads / 32);
-      if ((lane & 3) == 0 && it2 < items) {
-        const int par2 = int(it2 / HALF), p2 = int(it2 - int64_t(par2) * HALF);
-        const int cb2 = child_off[par2];
-        if (g < child_off[par2 + 1] - cb2)
-          bulk::prefetch_l2(F + (int64_t(cb2 + g) * HALF + p2) * D::LDF, uint32_t(D::LDF) * 16u);
-      }
-    }
+    const double2* sh = shift_up + int64_t(ok ? rb::pdesc_oct(dc, g) : 0) * SP;
+    double2* out = mp_p + int64_t(dc.z) * SP;
     rb::m2m_theta_item<NC, NP>([&](int k) { return __ldg(frow + k); }, ok, sh, out, p, Bsm, v);
   }
 }
@@ -347,10 +368,7 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_m2m_theta_rb(int n_par, con
 // (parent, 8 rows of the (child slot, circle) space); each lane builds its A
 // row on the fly, L_p[s] shift_c[s] (one complex product feeds both parts).
 template <int NC, int NP>
-__global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_theta_rb(int n_par, const int* __restrict__ plist,
-                                                                  const int* __restrict__ child_off,
-                                                                  const int* __restrict__ children,
-                                                                  const uint8_t* __restrict__ oct_c,
+__global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_theta_rb(int n_par, const int4* __restrict__ pdesc,
                                                                   const double2* __restrict__ loc_p,
                                                                   const double* __restrict__ B,
                                                                   const double* __restrict__ v,
@@ -362,23 +380,18 @@ __global__ void __launch_bounds__(rb::kThreads, 2) k_l2l_theta_rb(int n_par, con
   rb::stage_b<D::DTH_K, D::DTH_N, D::DTH_LDB>(Bsm, B);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const int64_t items = int64_t(n_par) * HALF;  // 8 HALF rows per parent = HALF tiles
-  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
-       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+  const int64_t stride = int64_t(gridDim.x) * (rb::kThreads / 32);
+  int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp;
+  int4 dn = it < items ? __ldg(pdesc + 3 * (it / HALF)) : make_int4(0, 0, 0, 0);
+  for (; it < items; it += stride) {
+    const int4 dc = dn;  // parent descriptor, loaded one item ahead (rb::PDesc)
+    if (it + stride < items) dn = __ldg(pdesc + 3 * ((it + stride) / HALF));
     const int par = int(it / HALF), tile = int(it - int64_t(par) * HALF);
-    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const int cb = dc.x, nchp = dc.y;
     const int rho = tile * 8 + g, c = rho / HALF, p = rho - c * HALF;
     const bool ok = c < nchp;
-    const double2* L = loc_p + int64_t(plist ? plist[par] : par) * SP;
-    const double2* sh = shift_dn + int64_t(ok ? oct_c[children[cb + c]] : 0) * SP;
-    {
-      // the parent local of this warp's NEXT item -> L2 (bulk prefetch, once per
-      // parent: by the warp that will take its first tile), one round ahead
-      const int64_t it2 = it + int64_t(gridDim.x) * (rb::kThreads / 32);
-      if (lane == 0 && it2 < items && it2 % HALF == 0) {
-        const int par2 = int(it2 / HALF);
-        bulk::prefetch_l2(loc_p + int64_t(plist ? plist[par2] : par2) * SP, uint32_t(SP) * 16u);
-      }
-    }
+    const double2* L = loc_p + int64_t(dc.z) * SP;
+    const double2* sh = shift_dn + int64_t(ok ? rb::pdesc_oct(dc, c) : 0) * SP;
     // even / odd parts of the shifted circle: front sample (row k, column p)
     // plus / minus back sample (row k, column p + HALF)
     double er[KH], ei[KH], qr[KH], qi[KH];
@@ -522,13 +535,24 @@ __host__ __device__ constexpr int blk_ldb(int cols) { return ldb(cols); }
 template <class Fetch>
 __device__ __forceinline__ double2 row_alpha(int kin, const double* __restrict__ v, Fetch fetch) {
   const int tq = threadIdx.x & 3;
-  double sr = 0.0, si = 0.0;
-  for (int k = tq; k < kin; k += 4) {
+  double pr[4] = {0.0, 0.0, 0.0, 0.0}, pi[4] = {0.0, 0.0, 0.0, 0.0};  // independent partial sums
+  int k = tq;
+  for (; k + 12 < kin; k += 16) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double vk = __ldg(v + k + 4 * u);
+      const double2 x = fetch(k + 4 * u);
+      pr[u] = fma(vk, x.x, pr[u]);
+      pi[u] = fma(vk, x.y, pi[u]);
+    }
+  }
+  for (int u = 0; k < kin; k += 4, ++u) {
     const double vk = __ldg(v + k);
     const double2 x = fetch(k);
-    sr = fma(vk, x.x, sr);
-    si = fma(vk, x.y, si);
+    pr[u & 3] = fma(vk, x.x, pr[u & 3]);
+    pi[u & 3] = fma(vk, x.y, pi[u & 3]);
   }
+  double sr = (pr[0] + pr[1]) + (pr[2] + pr[3]), si = (pi[0] + pi[1]) + (pi[2] + pi[3]);
   sr += __shfl_xor_sync(0xffffffffu, sr, 1);
   si += __shfl_xor_sync(0xffffffffu, si, 1);
   sr += __shfl_xor_sync(0xffffffffu, sr, 2);
@@ -630,14 +654,30 @@ __device__ __forceinline__ void chunk_mma_eo(int kh, int kin, double2 ia, Fetch 
 template <class Fetch>
 __device__ __forceinline__ double2 row_alpha_eo(int kin, int KH4, const double* __restrict__ v, Fetch fetch) {
   const int tq = threadIdx.x & 3;
-  double sr = 0.0, si = 0.0;
-  for (int k = tq; k < kin; k += 4) {
+  double pr[4] = {0.0, 0.0, 0.0, 0.0}, pi[4] = {0.0, 0.0, 0.0, 0.0};  // [2 u + half]: independent partial sums
+  int k = tq;
+  for (; k + 4 < kin; k += 8) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double ve = __ldg(v + k + 4 * u), vo = __ldg(v + KH4 + k + 4 * u);
+      double2 e, o;
+      fetch(k + 4 * u, e, o);
+      pr[2 * u] = fma(ve, e.x, pr[2 * u]);
+      pi[2 * u] = fma(ve, e.y, pi[2 * u]);
+      pr[2 * u + 1] = fma(vo, o.x, pr[2 * u + 1]);
+      pi[2 * u + 1] = fma(vo, o.y, pi[2 * u + 1]);
+    }
+  }
+  if (k < kin) {
     const double ve = __ldg(v + k), vo = __ldg(v + KH4 + k);
     double2 e, o;
     fetch(k, e, o);
-    sr = fma(ve, e.x, fma(vo, o.x, sr));
-    si = fma(ve, e.y, fma(vo, o.y, si));
+    pr[0] = fma(ve, e.x, pr[0]);
+    pi[0] = fma(ve, e.y, pi[0]);
+    pr[1] = fma(vo, o.x, pr[1]);
+    pi[1] = fma(vo, o.y, pi[1]);
   }
+  double sr = (pr[0] + pr[1]) + (pr[2] + pr[3]), si = (pi[0] + pi[1]) + (pi[2] + pi[3]);
   sr += __shfl_xor_sync(0xffffffffu, sr, 1);
   si += __shfl_xor_sync(0xffffffffu, si, 1);
   sr += __shfl_xor_sync(0xffffffffu, sr, 2);
@@ -653,10 +693,7 @@ constexpr int kChunkEO = 2;  // M2M theta: n8 tiles of the half-size output per 
 // the lane's F row is read from L2 once (the rank-1 pass) and re-read from L1
 // per sub-chunk.
 __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, int chb, int n_par,
-                                                                const int* __restrict__ plist,
-                                                                const int* __restrict__ child_off,
-                                                                const int* __restrict__ children,
-                                                                const uint8_t* __restrict__ oct_c,
+                                                                const int4* __restrict__ pdesc,
                                                                 const double2* __restrict__ F,
                                                                 const double* __restrict__ B,
                                                                 const double* __restrict__ v,
@@ -670,20 +707,23 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
   extern __shared__ __align__(16) double Bsh[];
   rb::stage_block(Bsh, B, 2 * KH4, NH, 8 * jb, 8 * chb, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const int64_t items = int64_t(n_par) * half;
-  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
-       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+  const int64_t items = int64_t(n_par) * half, stride = int64_t(gridDim.x) * (rb::kThreads / 32);
+  int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp;
+  int4 dn = it < items ? __ldg(pdesc + 3 * (it / half)) : make_int4(0, 0, 0, 0);
+  for (; it < items; it += stride) {
+    const int4 dc = dn;  // parent descriptor, loaded one item ahead (rb::PDesc)
+    if (it + stride < items) dn = __ldg(pdesc + 3 * ((it + stride) / half));
     const int par = int(it / half), p = int(it - int64_t(par) * half);
-    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const int cb = dc.x, nchp = dc.y;
     const bool ok = g < nchp;
     const double2* frow = F + (int64_t(cb + (ok ? g : 0)) * half + p) * ldf;
-    const double2* sh = shift_up + int64_t(ok ? oct_c[children[cb + g]] : 0) * SP;
+    const double2* sh = shift_up + int64_t(ok ? rb::pdesc_oct(dc, g) : 0) * SP;
     auto fetch = [&](int k, double2& e, double2& o) {
       e = ok ? __ldg(frow + k) : make_double2(0.0, 0.0);
       o = ok ? __ldg(frow + KH4 + k) : make_double2(0.0, 0.0);
     };
     const double2 ia = rb::row_alpha_eo(nc, KH4, v, fetch);
-    double2* out = mp_p + int64_t(plist ? plist[par] : par) * SP;
+    double2* out = mp_p + int64_t(dc.z) * SP;
     for (int j0 = jb; j0 < jend; j0 += CH) {
       double2 shf[CH][2], shb[CH][2];
 #pragma unroll
@@ -727,10 +767,7 @@ __global__ void __launch_bounds__(rb::kThreads) k_m2m_theta_rbl(int nc, int np, 
 // in shared memory (blockIdx.y), walked in sub-chunks of CH tiles; output row n
 // of the child: (Ye, Yo) of circle p at columns 2 p, 2 p + 1 of the narrow rows.
 __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, int chb, int n_par,
-                                                                const int* __restrict__ plist,
-                                                                const int* __restrict__ child_off,
-                                                                const int* __restrict__ children,
-                                                                const uint8_t* __restrict__ oct_c,
+                                                                const int4* __restrict__ pdesc,
                                                                 const double2* __restrict__ loc_p,
                                                                 const double* __restrict__ B,
                                                                 const double* __restrict__ v,
@@ -743,15 +780,18 @@ __global__ void __launch_bounds__(rb::kThreads) k_l2l_theta_rbl(int nc, int np, 
   extern __shared__ __align__(16) double Bsh[];
   rb::stage_block(Bsh, B, 2 * KH4, NH, 8 * jb, 8 * chb, ldb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const int64_t items = int64_t(n_par) * half;
-  for (int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp; it < items;
-       it += int64_t(gridDim.x) * (rb::kThreads / 32)) {
+  const int64_t items = int64_t(n_par) * half, stride = int64_t(gridDim.x) * (rb::kThreads / 32);
+  int64_t it = int64_t(blockIdx.x) * (rb::kThreads / 32) + warp;
+  int4 dn = it < items ? __ldg(pdesc + 3 * (it / half)) : make_int4(0, 0, 0, 0);
+  for (; it < items; it += stride) {
+    const int4 dc = dn;  // parent descriptor, loaded one item ahead (rb::PDesc)
+    if (it + stride < items) dn = __ldg(pdesc + 3 * ((it + stride) / half));
     const int par = int(it / half), tile = int(it - int64_t(par) * half);
-    const int cb = child_off[par], nchp = child_off[par + 1] - cb;
+    const int cb = dc.x, nchp = dc.y;
     const int rho = tile * 8 + g, c = rho / half, p = rho - c * half;
     const bool ok = c < nchp;
-    const double2* L = loc_p + int64_t(plist ? plist[par] : par) * SP;
-    const double2* sh = shift_dn + int64_t(ok ? oct_c[children[cb + c]] : 0) * SP;
+    const double2* L = loc_p + int64_t(dc.z) * SP;
+    const double2* sh = shift_dn + int64_t(ok ? rb::pdesc_oct(dc, c) : 0) * SP;
     auto fetch = [&](int k, double2& e, double2& o) {
       if (!ok) {
         e = o = make_double2(0.0, 0.0);
@@ -852,6 +892,7 @@ struct RbLaunch {
   const int* children;
   int64_t nch;           // total children (= child_off[n_par])
   const uint8_t* oct_c;
+  const int4* pdesc;     // rb::PDesc per parent (3 int4)
   int grid;              // persistent CTAs
   cudaStream_t st;
   int phi_grid = 0;      // persistent CTAs of the (HBM-bound) phi passes; 0 = grid
@@ -866,7 +907,7 @@ void m2m_rb(const RbLaunch& L, const double2* mp_c, double2* mp_p, const double*
                                                                                     vphi, F);
   const int smem = D::UTH_K * D::UTH_LDB * 8;
   cudaFuncSetAttribute(k_m2m_theta_rb<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_m2m_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c, F,
+  k_m2m_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.pdesc, F,
                                                             Bth, vth, shift_up, mp_p);
 }
 
@@ -876,7 +917,7 @@ void l2l_rb(const RbLaunch& L, const double2* loc_p, double2* loc_c, const doubl
   using D = rb::Dims<A, B>;
   const int smem = D::DTH_K * D::DTH_LDB * 8;
   cudaFuncSetAttribute(k_l2l_theta_rb<A, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_l2l_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.plist, L.child_off, L.children, L.oct_c,
+  k_l2l_theta_rb<A, B><<<L.grid, rb::kThreads, smem, L.st>>>(L.n_par, L.pdesc,
                                                             loc_p, Bth, vth, shift_dn, Nb);
   if (L.nch > 0)
     k_l2l_phi_rb<A, B><<<L.phi_grid ? L.phi_grid : L.grid, rb::kThreads, 0, L.st>>>(L.nch, L.children, Nb, Bphi,
