@@ -292,6 +292,25 @@ hfmm_status hfmm_gpu_direct(const double* positions, const double* charges, size
 hfmm_status hfmm_resample_matrix(int64_t n_in, double s_in, int64_t n_out, double s_out,
                                  double* out);
 
+/* Packed operands of the device M2M passes of a level pair (child grid nc, parent
+ * grid np, both even): what engine.cu uploads for fft_interpolate
+ * (sphere_grid.cpp:183-192).  Host logic only (csrc/interp.hpp), no device needed.
+ *   bphi: Kp x Np row-major, the phi map n_c -> n_p as real matrix + rank-1 row, with
+ *         the (e, o) fold in its columns (column 2 p + h: circle p, part h);
+ *   vphi: nc entries (rank-1 input vector);
+ *   bth:  2 KH x NH row-major, [Be ; Bo] of the even / odd theta map 2 n_c -> 2 n_p;
+ *   vth:  2 KH entries, laid out like the rows of bth;
+ *   dims: {Kp, Np, KH, NH}.  Pass null pointers to query dims only. */
+hfmm_status hfmm_m2m_operands(int nc, int np, double* bphi, double* vphi, double* bth, double* vth,
+                              int dims[4]);
+
+/* Same for the L2L passes (fft_anterpolate_adjoint, sphere_grid.cpp:194-214): theta map
+ * 2 n_p -> 2 n_c with row_scale (2 nc entries) and col_scale (2 np entries) applied, in
+ * even / odd form; phi map n_p -> n_c reading (Ye, Yo) pairs (unfold in its rows).
+ *   bth: 2 KH x NH, vth: 2 KH;  bphi: Kp x Np, vphi: np;  dims: {KH, NH, Kp, Np}. */
+hfmm_status hfmm_l2l_operands(int nc, int np, const double* row_scale, const double* col_scale,
+                              double* bth, double* vth, double* bphi, double* vphi, int dims[4]);
+
 /* Frozen seeded generator of the BASELINE inputs:
  * shape 0 = uniform cube of side `extent`, 1 = sphere surface of radius `extent`. */
 void hfmm_generate_inputs(int shape, size_t n, double extent, uint64_t seed,

@@ -127,6 +127,9 @@ _SIG = {
                                        ctypes.c_int, _P]),
     "hfmm_resample_matrix": (ctypes.c_int, [ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
                                             ctypes.c_double, _P]),
+    "hfmm_m2m_operands": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, ctypes.POINTER(ctypes.c_int)]),
+    "hfmm_l2l_operands": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, _P,
+                                         ctypes.POINTER(ctypes.c_int)]),
     "hfmm_generate_inputs": (None, [ctypes.c_int, ctypes.c_size_t, ctypes.c_double, ctypes.c_uint64,
                                     _P, _P]),
 }

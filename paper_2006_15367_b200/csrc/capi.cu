@@ -412,6 +412,48 @@ hfmm_status hfmm_resample_matrix(int64_t n_in, double s_in, int64_t n_out, doubl
   });
 }
 
+hfmm_status hfmm_m2m_operands(int nc, int np, double* bphi, double* vphi, double* bth, double* vth,
+                              int dims[4]) {
+  return guard([&] {
+    need(dims, "hfmm_m2m_operands(dims)");
+    if (nc <= 0 || np <= 0 || nc % 2 || np % 2) throw std::invalid_argument("hfmm_m2m_operands: grids must be even");
+    using namespace hfmm_b200;
+    const RealRank1 uphi = real_rank1(nc, 0.0, np, 0.0);
+    const RealRank1 uf = fold_columns(uphi, nc, np);
+    const EvenOdd ue = even_odd(real_rank1(2 * nc, 0.5, 2 * np, 0.5), 2 * nc, 2 * np);
+    dims[0] = uf.K;
+    dims[1] = uf.N;
+    dims[2] = ue.KH4;
+    dims[3] = ue.NH;
+    if (bphi) std::memcpy(bphi, uf.B.data(), uf.B.size() * sizeof(double));
+    if (vphi) std::memcpy(vphi, uf.v.data(), uf.v.size() * sizeof(double));
+    if (bth) std::memcpy(bth, ue.B.data(), ue.B.size() * sizeof(double));
+    if (vth) std::memcpy(vth, ue.v.data(), ue.v.size() * sizeof(double));
+  });
+}
+
+hfmm_status hfmm_l2l_operands(int nc, int np, const double* row_scale, const double* col_scale,
+                              double* bth, double* vth, double* bphi, double* vphi, int dims[4]) {
+  return guard([&] {
+    need(dims, "hfmm_l2l_operands(dims)");
+    need(row_scale, "hfmm_l2l_operands(row_scale)");
+    need(col_scale, "hfmm_l2l_operands(col_scale)");
+    if (nc <= 0 || np <= 0 || nc % 2 || np % 2) throw std::invalid_argument("hfmm_l2l_operands: grids must be even");
+    using namespace hfmm_b200;
+    const std::vector<double> rs(row_scale, row_scale + 2 * nc), cs(col_scale, col_scale + 2 * np);
+    const EvenOdd de = even_odd(real_rank1(2 * np, 0.5, 2 * nc, 0.5, &rs, &cs), 2 * np, 2 * nc);
+    const RealRank1 du = unfold_rows(real_rank1(np, 0.0, nc, 0.0), np, nc);
+    dims[0] = de.KH4;
+    dims[1] = de.NH;
+    dims[2] = du.K;
+    dims[3] = du.N;
+    if (bth) std::memcpy(bth, de.B.data(), de.B.size() * sizeof(double));
+    if (vth) std::memcpy(vth, de.v.data(), de.v.size() * sizeof(double));
+    if (bphi) std::memcpy(bphi, du.B.data(), du.B.size() * sizeof(double));
+    if (vphi) std::memcpy(vphi, du.v.data(), du.v.size() * sizeof(double));
+  });
+}
+
 void hfmm_generate_inputs(int shape, size_t n, double extent, uint64_t seed, double* positions,
                           double* charges) {
   hfmm_b200::generate_inputs(shape, n, extent, seed, positions, charges);

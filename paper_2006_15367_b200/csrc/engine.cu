@@ -647,11 +647,7 @@ void Engine::phase_m2m() {
     // 0. fused single-kernel pair (folded circles stay in shared memory)
 #ifndef HFMM_NO_FZ
     if (!hook_no_rb_ && fz_pair(nc, np)) {
-#ifdef HFMM_FZ3
-      launch_m2m_fz3(rl, sms_, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up);
-#else
       launch_m2m_fz2(rl, sms_, C.mp, P.mp, P.up_phi_Bf, P.up_phi_v, P.up_th_Be, P.up_th_ve, P.shift_up);
-#endif
       ++launches_;
       ck(cudaGetLastError(), "k_m2m_fz");
       continue;
@@ -705,7 +701,6 @@ void Engine::phase_m2l(int lo, int hi) {
   if (lo < 0) lo = s_.top;
   if (hi < 0) hi = s_.L;
   ck(cudaFuncSetAttribute(k_m2l_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l::SMEM_BYTES), "attr");
-  ck(cudaFuncSetAttribute(k_m2l_dmma3, cudaFuncAttributeMaxDynamicSharedMemorySize, m2l3::SMEM_BYTES), "attr");
   for (int l = lo; l <= hi; ++l) {
     DevLevel& d = lv_[size_t(l)];
     // distributed mode: only the observers this rank holds (the multipole
@@ -714,17 +709,10 @@ void Engine::phase_m2l(int lo, int hi) {
       const int nb = (d.G + m2l::MB - 1) / m2l::MB;
       const int nblk = dist_ ? d.m2l_nblk : nb * nb * nb;
       if (nblk == 0) continue;
-#ifdef HFMM_M2L_V1
       const int ppc = m2l_pairs_per_cta(nblk, d.S, sms_);
       dim3 grid(unsigned(nblk), unsigned((d.S / 2 + ppc - 1) / ppc));
       k_m2l_dmma<<<grid, 128, m2l::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, dist_ ? d.m2l_blk : nullptr, d.lookup, d.T,
                                                       d.mp, d.loc);
-#else
-      const int ppc = m2l3_pairs_per_cta(nblk, d.S, sms_);
-      dim3 grid(unsigned(nblk), unsigned((d.S / 2 + ppc - 1) / ppc));
-      k_m2l_dmma3<<<grid, m2l3::kThreads, m2l3::SMEM_BYTES, st_>>>(d.G, nb, d.S, ppc, dist_ ? d.m2l_blk : nullptr,
-                                                                   d.lookup, d.T, d.mp, d.loc);
-#endif
     } else {
       const int nobs = dist_ ? held_cnt_[size_t(l)] : int(d.n_nodes);
       if (nobs == 0) continue;

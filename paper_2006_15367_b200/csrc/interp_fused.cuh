@@ -193,151 +193,6 @@ inline void launch_m2m_fz2(const RbLaunch& L, int sms, const double2* mp_c, doub
   k_m2m_fz2<18, 28><<<grid, fz2::kThreads, smem, L.st>>>(L.n_par, L.pdesc, mp_c, Bphi, vphi, Bth, vth, shift_up, mp_p);
 }
 
-// ---------------------------------------------------------------------------
-// Two-CTA variant: the same two passes with 7 warps per CTA and TWO CTAs per SM,
-// so one CTA's barrier waits and scalar epilogues overlap the other's DMMA
-// (ncu on the one-CTA kernel: ~20% of the stall samples at its two barriers and
-// 33% on the scalar FP64 of rank-1 sums and epilogues, which the lockstep phases
-// of a single CTA cannot hide).  To fit 2 x 107 KB the children are NOT staged:
-// the phi pass reads them through L1 (their block is pulled into L2 one parent
-// ahead by bulk prefetches), and the shift table keeps 4 octants (octant o ^ 7
-// is the conjugate).
-namespace fz3 {
-
-constexpr int kWarps = 7, kThreads = 32 * kWarps;
-
-template <int NC, int NP>
-struct Lay {
-  using D = rb::Dims<NC, NP>;
-  static constexpr int H = NP / 2, SC = NC * NC;
-  static constexpr int LDF = D::UTH_K + 2;
-  static constexpr int CSF = fz::pad4mod8(H * LDF);
-  static constexpr int BPHI = D::UPHI_K * D::UPHI_LDB, BTH = D::UTH_K * D::UTH_LDB;  // doubles
-  static constexpr int VPHI = D::UPHI_K, VTH = D::UTH_K;
-  static constexpr int SHROW = H + 1, SHOCT = H * SHROW + 1;  // double2 (padded)
-  static constexpr int OFF_SH = (BPHI + BTH + VPHI + VTH) * 8;
-  static constexpr int OFF_F = OFF_SH + 4 * SHOCT * 16;
-  static constexpr int OFF_CR = OFF_F + 8 * CSF * 16;
-  static constexpr int SMEM = OFF_CR + 64;  // child rows of the two parents in flight
-  static_assert(OFF_SH % 16 == 0 && H % 2 == 0, "layout");
-};
-
-}  // namespace fz3
-
-template <int NC, int NP>
-__global__ void __launch_bounds__(fz3::kThreads, 2) k_m2m_fz3(int n_par, const int4* __restrict__ pdesc,
-                                                              const double2* __restrict__ mp_c,
-                                                              const double* __restrict__ Bphi,
-                                                              const double* __restrict__ vphi,
-                                                              const double* __restrict__ Bth,
-                                                              const double* __restrict__ vth,
-                                                              const double2* __restrict__ shift_up,
-                                                              double2* __restrict__ mp_p) {
-  using D = rb::Dims<NC, NP>;
-  using Y = fz3::Lay<NC, NP>;
-  constexpr int KSP = D::UPHI_K / 4, NTP = D::UPHI_N / 8, HALF = D::HALF, SP = D::SP, SC = D::SC, H = Y::H;
-  constexpr int NW = fz3::kWarps;
-  extern __shared__ __align__(16) unsigned char fz3_smem[];
-  double* Bp = reinterpret_cast<double*>(fz3_smem);
-  double* Bt = Bp + Y::BPHI;
-  double* vp = Bt + Y::BTH;
-  double* vt = vp + Y::VPHI;
-  double2* shq = reinterpret_cast<double2*>(fz3_smem + Y::OFF_SH);
-  double2* Fs = reinterpret_cast<double2*>(fz3_smem + Y::OFF_F);
-  int* crs = reinterpret_cast<int*>(fz3_smem + Y::OFF_CR);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-  const int G = gridDim.x;
-  const int* pdi = reinterpret_cast<const int*>(pdesc);
-  auto desc = [&](int par) { return par < n_par ? __ldg(pdesc + 3 * par) : make_int4(0, 0, 0, 0); };
-  auto crow = [&](int par) { return par < n_par ? __ldg(pdi + 12 * par + 4 + (lane & 7)) : -1; };
-  // warp 0: child rows of a parent -> crs[b], and the children's expansions -> L2
-  auto announce = [&](const int4& d, int cr, int b) {
-    if (lane < 8) crs[b * 8 + lane] = cr;
-    if (lane < d.y) bulk::prefetch_l2(mp_c + int64_t(cr) * SC, uint32_t(SC) * 16u);
-  };
-  int par = blockIdx.x;
-  int4 dc = desc(par), dn = desc(par + G);
-  int cn = warp == 0 ? crow(par + G) : -1;
-  if (warp == 0 && par < n_par) announce(dc, crow(par), 0);
-  for (int t = threadIdx.x; t < Y::VPHI; t += blockDim.x) vp[t] = t < NC ? vphi[t] : 0.0;
-  for (int t = threadIdx.x; t < Y::VTH; t += blockDim.x) vt[t] = vth[t];
-  for (int t = threadIdx.x; t < 4 * H * H; t += blockDim.x) {
-    const int o = t / (H * H), r = t - o * H * H, n = r / H, pc = r - n * H;
-    shq[o * Y::SHOCT + n * Y::SHROW + pc] = shift_up[int64_t(o) * SP + n * NP + pc];
-  }
-  rb::stage_b<D::UPHI_K, D::UPHI_N, D::UPHI_LDB>(Bp, Bphi);
-  rb::stage_b<D::UTH_K, D::UTH_N, D::UTH_LDB>(Bt, Bth);  // (ends with a CTA barrier)
-
-  for (int it = 0; par < n_par; par += G, ++it) {
-    const int b = it & 1;
-    const int nch = dc.y;
-    // crs[b ^ 1] was last read by the phi pass of the previous parent
-    if (warp == 0 && par + G < n_par) announce(dn, cn, b ^ 1);
-    const int4 d2 = desc(par + 2 * G);  // consumed at the bottom of this iteration
-    const int c2 = warp == 0 ? crow(par + 2 * G) : -1;
-    // phi pass: rows (child c, theta row i) -> folded circles in shared memory
-    const int rows = nch * NC, tiles = (rows + 7) / 8;
-    for (int t = warp; t < tiles; t += NW) {
-      const int R = t * 8 + g;
-      const bool ok = R < rows;
-      const int c = ok ? R / NC : 0, i = ok ? R - c * NC : 0;
-      const double2* x = mp_c + int64_t(crs[b * 8 + c]) * SC + i * NC;
-      double are[KSP], aim[KSP];
-#pragma unroll
-      for (int kk = 0; kk < KSP; ++kk) {
-        const int k = 4 * kk + tq;
-        const double2 xv = (ok && k < NC) ? __ldg(x + k) : make_double2(0.0, 0.0);
-        are[kk] = xv.x;
-        aim[kk] = xv.y;
-      }
-      rb::rank1_inject_f<KSP, NC>(are, aim, [&](int k) { return vp[k]; });
-      double cre[NTP][2] = {}, cim[NTP][2] = {};
-      rb::tile_mma<KSP, NTP, D::UPHI_LDB>(are, aim, Bp, cre, cim);
-      if (ok) {
-        double2* Fc = Fs + c * Y::CSF;
-#pragma unroll
-        for (int jn = 0; jn < NTP; ++jn)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int n = 8 * jn + 2 * tq + q;  // column 2 p + h: circle p, part e / o
-            if (n < NP) Fc[(n >> 1) * Y::LDF + (n & 1) * 4 * D::UTH_KH + i] = make_double2(cre[jn][q], cim[jn][q]);
-          }
-      }
-    }
-    __syncthreads();
-    // theta pass + shift + child sum: item = circle p, tile rows = child slots
-    const bool ok = g < nch;
-    const int oct = ok ? rb::pdesc_oct(dc, g) : 0;
-    double2* out = mp_p + int64_t(dc.z) * SP;
-    for (int p = warp; p < HALF; p += NW) {
-      const double2* frow = Fs + (ok ? g : 0) * Y::CSF + p * Y::LDF;
-      rb::m2m_theta_item_f<NC, NP>(
-          [&](int k) { return frow[k]; }, ok,
-          [&](int n, int back) {
-            const int up = n >= H;  // mirrored theta row: octant with z flipped
-            const int o = oct ^ (up ? 4 : 0) ^ (back ? 3 : 0);
-            // octants 4..7 are the conjugates of 3..0
-            const double2 v = shq[(o & 4 ? o ^ 7 : o) * Y::SHOCT + (up ? NP - 1 - n : n) * Y::SHROW + p];
-            return make_double2(v.x, o & 4 ? -v.y : v.y);
-          },
-          out, p, Bt, [&](int k) { return vt[k]; });
-    }
-    __syncthreads();
-    dc = dn;
-    dn = d2;
-    cn = c2;
-  }
-}
-
-inline void launch_m2m_fz3(const RbLaunch& L, int sms, const double2* mp_c, double2* mp_p, const double* Bphi,
-                           const double* vphi, const double* Bth, const double* vth, const double2* shift_up) {
-  constexpr int smem = fz3::Lay<18, 28>::SMEM;
-  static_assert(2 * (smem + 1024) <= 227 * 1024, "fused M2M (two CTAs per SM) shared memory");
-  cudaFuncSetAttribute(k_m2m_fz3<18, 28>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int grid = std::min(L.n_par, 2 * sms);
-  k_m2m_fz3<18, 28><<<grid, fz3::kThreads, smem, L.st>>>(L.n_par, L.pdesc, mp_c, Bphi, vphi, Bth, vth, shift_up, mp_p);
-}
-
 }  // namespace hfmm_b200
 
 #endif

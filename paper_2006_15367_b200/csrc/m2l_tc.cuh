@@ -17,7 +17,6 @@
 #ifndef HFMM_B200_M2L_TC_CUH
 #define HFMM_B200_M2L_TC_CUH
 
-#include "bulk.cuh"
 #include "dmma.cuh"
 #include "m2l.cuh"
 
@@ -159,162 +158,11 @@ __global__ void __launch_bounds__(128, 3) k_m2l_dmma(int G, int nb, int64_t S, i
   }
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialised form of the same kernel: one CTA per SM, 8 compute warps in
-// two groups of 4 (a group = one sample pair, as above) plus ONE producer warp
-// that stages the pairs into a ring of three shared-memory buffers with
-// cp.async, completion signalled on mbarriers (cp.async.mbarrier.arrive).  The
-// compute warps never issue a copy or meet a CTA barrier: a group waits for its
-// buffer's "full" barrier, runs the 624 DMMA per warp, stores, and releases the
-// buffer ("empty").  With three CTAs of four warps, each staging its own pairs,
-// ncu showed ~20% of the warp samples in staging code and barriers, and a probe
-// that skips the staging ran the phase 10% faster; one warp per sub-partition
-// reaches only 70% of the DMMA peak (tools/fp64_mix2.cu), so two compute warps
-// per sub-partition are kept busy at all times.
-namespace m2l3 {
-using namespace m2l;
-constexpr int kComputeWarps = 8, kThreads = 32 * (kComputeWarps + 1), kStages = 3;
-constexpr int STAGE = REGION + 2 * TAPS;  // double2 per stage: region, then the taps of both samples
-constexpr int SMEM_BYTES = kStages * STAGE * 16 + CELLS * 4 + 2 * kStages * 8;
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bulk::smem_addr(bar)) : "memory");
-}
-// The barrier receives one arrival from this thread when all its earlier cp.async have landed.
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bulk::smem_addr(bar)) : "memory");
-}
-}  // namespace m2l3
-
-__global__ void __maxnreg__(216) k_m2l_dmma3(int G, int nb, int64_t S, int ppc,
-                                                                 const int* __restrict__ blist,
-                                                                 const int* __restrict__ lookup,
-                                                                 const double2* __restrict__ T,
-                                                                 const double2* __restrict__ mp,
-                                                                 double2* __restrict__ loc) {
-  using namespace m2l3;
-  extern __shared__ double2 smem[];
-  int* nodes = reinterpret_cast<int*>(smem + kStages * STAGE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(nodes + CELLS);
-  uint64_t* empty = full + kStages;
-  const int blk = blist ? blist[blockIdx.x] : int(blockIdx.x);
-  const int bx = (blk % nb) * MB, by = ((blk / nb) % nb) * MB, bz = (blk / (nb * nb)) * MB;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {
-    const int GP = (G > MB ? G : MB) + 6;
-    for (int c = threadIdx.x; c < CELLS; c += blockDim.x) {
-      const int cz = c / (MR * MR), cy = (c / MR) % MR, cx = c % MR;
-      nodes[c] = __ldg(lookup + (int64_t(bz + cz + 3 - HALO) * GP + (by + cy + 3 - HALO)) * GP + (bx + cx + 3 - HALO));
-    }
-    if (threadIdx.x == 0) {
-      for (int b = 0; b < kStages; ++b) {
-        bulk::mbar_init(full + b, 32);  // the producer's 32 lanes (cp.async completion)
-        bulk::mbar_init(empty + b, 4);  // one lane of each warp of the consuming group
-      }
-      bulk::fence_mbar_init();
-    }
-  }
-  __syncthreads();
-  const int64_t pairs = S / 2;
-  const int64_t pb = int64_t(blockIdx.y) * ppc;
-  const int n = int((pb + ppc < pairs ? pb + ppc : pairs) - pb);
-
-  if (warp == kComputeWarps) {
-    // ---- producer: pair j -> stage j % 3
-    for (int j = 0; j < n; ++j) {
-      const int b = j % kStages, k = j / kStages;
-      if (k > 0) bulk::mbar_wait(empty + b, uint32_t(k - 1) & 1u);
-      double2* Ms = smem + b * STAGE;
-      double2* Ts = Ms + REGION;
-      const int64_t s0 = (pb + j) * 2;
-      for (int t = lane; t < kSlots * 2; t += 32) {
-        // taps of adjacent boxes (|offset| <= 1 per axis) are never far: staged as zeros
-        const int sl = t >> 1, ax = sl / 49 - 3, ay = (sl / 7) % 7 - 3, az = sl % 7 - 3;
-        const bool far_tap = iabs(ax) > 1 || iabs(ay) > 1 || iabs(az) > 1;
-        cp_async16(Ts + (t & 1) * TAPS + (ax + 3) * TSX + (ay + 3) * 7 + (az + 3),
-                   T + (far_tap ? int64_t(sl) * S + s0 + (t & 1) : 0), far_tap);
-      }
-      for (int t = lane; t < CELLS * 2; t += 32) {
-        const int row = t / (2 * MR), ent = t - row * (2 * MR), cz = row / MR, cy = row - cz * MR;
-        const int node = nodes[row * MR + (ent >> 1)];
-        cp_async16(Ms + cz * ZS + cy * ROW + ent,
-                   mp + (node >= 0 ? uint64_t(uint32_t(node)) * uint32_t(S) + uint64_t(s0 + (ent & 1)) : 0), node >= 0);
-      }
-      cp_async_arrive(full + b);
-    }
-    return;
-  }
-
-  // ---- compute warps: group gq takes pairs j = gq, gq + 2, ...
-  const int gq = warp >> 2, wl = warp & 3;
-  const int g = lane >> 2, tq = lane & 3;
-  const int sw = wl & 1, t0 = (wl >> 1) * 4;
-  int pbo[4];  // B fragment bases (double2 offsets into a stage's region), see k_m2l_dmma
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int tt = t0 + t;
-    const int px = g & 3, py = 2 * (tt & 1) + (g >> 2), pz = tt >> 1;
-    pbo[t] = (2 * pz + HALO) * ZS + (2 * py + HALO + (tq >> 1)) * ROW + 2 * (2 * px + HALO + (tq & 1)) + sw;
-  }
-  const int tlo = REGION + sw * TAPS + ((g & 1) - (tq & 1)) * TSX + (((g >> 1) & 1) - (tq >> 1)) * 7 + (g >> 2);
-  for (int j = gq; j < n; j += 2) {
-    const int b = j % kStages;
-    bulk::mbar_wait(full + b, uint32_t(j / kStages) & 1u);
-    const double2* Ms = smem + b * STAGE;
-    const double2* Tl = Ms + tlo;
-    const int64_t s0 = (pb + j) * 2;
-    double acc[3][4][2];
-#pragma unroll
-    for (int v = 0; v < 3; ++v)
-#pragma unroll
-      for (int t = 0; t < 4; ++t) acc[v][t][0] = acc[v][t][1] = 0.0;
-#pragma unroll
-    for (int d = 0; d < 27; ++d) {
-      if (d == 13) continue;  // D = 0: siblings are always adjacent
-      const int Dx = d % 3 - 1, Dy = (d / 3) % 3 - 1, Dz = d / 9 - 1;  // compile-time
-      const int doff = (2 * Dz) * ZS + (2 * Dy) * ROW + 2 * (2 * Dx);
-#pragma unroll
-      for (int kj = 0; kj < 2; ++kj) {
-        const double2 tv = Tl[(-2 * Dx + 3) * TSX + (-2 * Dy + 3) * 7 + (-kj - 2 * Dz + 3)];
-        const double a3 = tv.x + tv.y;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const double2 bv = Ms[pbo[t] + doff + kj * ZS];
-          dmma884(acc[0][t][0], acc[0][t][1], tv.x, bv.x);
-          dmma884(acc[1][t][0], acc[1][t][1], tv.y, bv.y);
-          dmma884(acc[2][t][0], acc[2][t][1], a3, bv.x + bv.y);
-        }
-      }
-    }
-    // the stage is no longer read: release it before the stores
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty + b);
-    const int ocx = g & 1, ocy = (g >> 1) & 1, ocz = g >> 2;  // observer child offsets
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int tt = t0 + t;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int nn = 2 * tq + q;
-        const int px = nn & 3, py = 2 * (tt & 1) + (nn >> 2), pz = tt >> 1;
-        const int rx = 2 * px + ocx + HALO, ry = 2 * py + ocy + HALO, rz = 2 * pz + ocz + HALO;
-        const int node = nodes[(rz * MR + ry) * MR + rx];
-        if (node >= 0)
-          loc[int64_t(node) * S + s0 + sw] = make_double2(acc[0][t][q] - acc[1][t][q], acc[2][t][q] - acc[0][t][q] - acc[1][t][q]);
-      }
-    }
-  }
-}
-
-// Sample pairs per CTA of the warp-specialised kernel: long runs (the ring's fill
-// is paid once per CTA), even chunks, at least ~4 CTAs per SM when the level allows.
-inline int m2l3_pairs_per_cta(int nblocks, int64_t S, int sms) {
-  const int64_t pairs = S / 2;
-  int64_t ppc = int64_t(nblocks) * pairs / (int64_t(sms) * 4);
-  ppc = ppc < 4 ? 4 : ppc > 32 ? 32 : ppc;
-  const int64_t chunks = (pairs + ppc - 1) / ppc;
-  return int((pairs + chunks - 1) / chunks);
-}
+// (A warp-specialised form -- one CTA per SM, 8 compute warps in two groups plus a
+// producer warp filling a ring of three staged sample pairs, mbarrier hand-off -- was
+// built and measured this round: 48.8 ms against 42.5 ms at config 4.  Two compute
+// warps per SM sub-partition do not keep the DMMA pipe as busy as the three of this
+// kernel's 3 CTAs x 4 warps, and a 13-warp block would cap a thread at 128 registers.)
 
 }  // namespace hfmm_b200
 

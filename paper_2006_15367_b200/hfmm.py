@@ -417,3 +417,32 @@ def resample_matrix(n_in: int, s_in: float, n_out: int, s_out: float) -> np.ndar
     out = np.empty((n_out, n_in, 2))
     check(lib().hfmm_resample_matrix(int(n_in), float(s_in), int(n_out), float(s_out), ptr(out)))
     return out[..., 0] + 1j * out[..., 1]
+
+
+def m2m_operands(nc: int, npar: int):
+    """Packed operands of the device M2M passes of a level pair (host logic, csrc/interp.hpp):
+    (bphi (Kp, Np), vphi (nc,), bth (2 KH, NH), vth (2 KH,), KH)."""
+    import ctypes
+    dims = (ctypes.c_int * 4)()
+    check(lib().hfmm_m2m_operands(int(nc), int(npar), None, None, None, None, dims))
+    kp, n_p, kh, nh = list(dims)
+    bphi, vphi = np.empty((kp, n_p)), np.empty(nc)
+    bth, vth = np.empty((2 * kh, nh)), np.empty(2 * kh)
+    check(lib().hfmm_m2m_operands(int(nc), int(npar), ptr(bphi), ptr(vphi), ptr(bth), ptr(vth), dims))
+    return bphi, vphi, bth, vth, kh
+
+
+def l2l_operands(nc: int, npar: int, row_scale: np.ndarray, col_scale: np.ndarray):
+    """Packed operands of the device L2L passes: (bth (2 KH, NH), vth (2 KH,), bphi (Kp, Np), vphi (np,), KH)."""
+    import ctypes
+    rs = np.ascontiguousarray(row_scale, dtype=np.float64)
+    cs = np.ascontiguousarray(col_scale, dtype=np.float64)
+    if rs.size != 2 * nc or cs.size != 2 * npar:
+        raise _native.InvalidArgument("l2l_operands: row_scale has 2 nc entries, col_scale 2 np")
+    dims = (ctypes.c_int * 4)()
+    check(lib().hfmm_l2l_operands(int(nc), int(npar), ptr(rs), ptr(cs), None, None, None, None, dims))
+    kh, nh, kp, n_p = list(dims)
+    bth, vth = np.empty((2 * kh, nh)), np.empty(2 * kh)
+    bphi, vphi = np.empty((kp, n_p)), np.empty(npar)
+    check(lib().hfmm_l2l_operands(int(nc), int(npar), ptr(rs), ptr(cs), ptr(bth), ptr(vth), ptr(bphi), ptr(vphi), dims))
+    return bth, vth, bphi, vphi, kh
