@@ -25,7 +25,7 @@ from bench import CONFIGS  # noqa: E402
 from paper_2006_15367_b200.distributed import schedule  # noqa: E402
 
 cfg = sys.argv[1]
-counts = [int(a) for a in sys.argv[2:]] or [1, 2, 4, 8]
+counts = [int(a) for a in sys.argv[2:] if not a.startswith("--")] or [1, 2, 4, 8]
 shape, n, ext, seed, digits = CONFIGS[cfg]
 pos, q = hb.generate_inputs(shape, n, ext, seed)
 KN = {0: "halo", 1: "ghost", 2: "reduce", 3: "gather"}
@@ -44,6 +44,7 @@ for P in counts:
     for it in range(3):  # warm-up + 2 timed
         xb = dict.fromkeys(KN.values(), 0)
         times = [{} for _ in range(P)]
+        lvl_times = [{} for _ in range(P)]
         for what, a, lvl in sched:
             if what == "run":
                 for r, (e, st) in enumerate(zip(engs, streams)):
@@ -54,6 +55,8 @@ for P in counts:
                     ev1.synchronize()
                     nm = hb.Phase(a).name
                     times[r][nm] = times[r].get(nm, 0.0) + ev0.elapsed_time(ev1)
+                    if lvl >= 0:
+                        lvl_times[r][f"{nm}@{lvl}"] = round(ev0.elapsed_time(ev1), 3)
             elif P > 1:
                 bufs = {}
                 for r, e in enumerate(engs):
@@ -77,6 +80,8 @@ for P in counts:
     split = {nm: round(float(np.mean([t[worst][nm] for t in per_rank])), 3) for nm in per_rank[0][worst]}
     print(f"{cfg} P={P}: max-over-ranks compute {max(tot):.3f} ms (rank {worst}; min {min(tot):.3f}) "
           f"phases {split} exchanged GB/eval {({k: round(v / 1e9, 4) for k, v in xb.items()})}", flush=True)
+    if "--levels" in sys.argv:
+        print(f"   per-level stages of rank {worst} (last pass): {lvl_times[worst]}", flush=True)
     for e in engs:
         e.close()
     del engs
